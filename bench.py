@@ -1,0 +1,531 @@
+#!/usr/bin/env python
+"""Fier decode-step benchmark (BASELINE.json metric: "Fier decode µs/layer & HBM GB/s at
+32k ctx; speedup vs full-KV attn").
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl ours|reference]
+
+One step = one decode step of one attention layer: append the new token
+(write k/v row + re-pack its open group) -> score every token from the packed
+keys -> per-head Top-n -> sparse attention over the selected rows.  Inputs
+(the per-step q, k_new, v_new) are resident in HBM for `value`; `e2e` copies
+them from pinned host memory and reads the attention output back inside the
+timed region, through the public API (DecodeLayer graph).  The KV cache of
+several layer instances is rotated so the bytes touched between visits exceed
+2x L2 (config.l2).  N > 1 (torchrun): every rank runs its own independent
+sequence (weak scaling, no data-path collective); time = max over ranks.
+
+--impl reference times the reference's own CPU implementation (oracle/_ref,
+compiled from the reference's headers) of the same step on the host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Fier decode µs/layer & HBM GB/s at 32k ctx; speedup vs full-KV attn"
+UNIT = "us/step"
+
+CONFIGS = {
+    "c1": dict(B=1, Hq=32, Hkv=32, L=4096, d=128, n=512, g=32, dtype="f32",
+               desc="C1: single-layer decode, 32 MHA heads, d=128, 4k ctx, fp32, Top-k 512"),
+    "c2": dict(B=1, Hq=32, Hkv=32, L=32768, d=128, n=3604, g=32, dtype="bf16",
+               desc="C2: LLaMA-2-7B decode layer, 32 MHA heads, d=128, 32k ctx, 11% budget "
+                    "(n=3604), batch 1, bf16"),
+    "c3": dict(B=1, Hq=32, Hkv=8, L=131072, d=128, n=4096, g=32, dtype="bf16",
+               desc="C3: Llama-3-8B GQA layer (32 q / 8 kv), d=128, 128k ctx, n=4096, batch 1, bf16"),
+    "c4": dict(B=32, Hq=32, Hkv=8, L=32768, d=128, n=3604, g=32, dtype="bf16",
+               desc="C4: batched decode, batch 32, 32k ctx, Llama-3-8B GQA shape, 11% budget, bf16"),
+}
+KERNELS_PER_STEP = 5  # append, score, top-k, sparse attention, LSE merge
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        j = json.load(open(p))
+        return float(j["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def elem_size(dt: str) -> int:
+    return 4 if dt == "f32" else 2
+
+
+def algorithmic_bytes(cfg, unique_rows=None):
+    """packed keys + selected K/V rows + Q/O, per step (one layer)."""
+    B, Hq, Hkv, L, d, n, g = (cfg[k] for k in ("B", "Hq", "Hkv", "L", "d", "n", "g"))
+    es = elem_size(cfg["dtype"])
+    packed = B * Hkv * (L * ((d + 7) // 8) + ((L + g - 1) // g) * d * 4)
+    rows = B * Hq * n if unique_rows is None else unique_rows
+    kv = rows * d * 2 * es
+    qo = B * Hq * d * (es + 4)  # q in the cache dtype, o in fp32
+    return packed, kv, qo
+
+
+def full_kv_bytes(cfg):
+    es = elem_size(cfg["dtype"])
+    return cfg["B"] * cfg["Hkv"] * cfg["L"] * cfg["d"] * 2 * es + cfg["B"] * cfg["Hq"] * cfg["d"] * (es + 4)
+
+
+class ClockSampler:
+    """NVML sampling of SM clock and throttle reasons during the timed region."""
+
+    NAMES = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
+             0x4: "sw_power_cap", 0x80: "hw_power_brake_slowdown", 0x1: "gpu_idle",
+             0x2: "applications_clocks_setting", 0x100: "display_clock_setting"}
+
+    def __init__(self, index: int):
+        self.samples, self.reasons, self.ok = [], set(), False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception as e:  # noqa: BLE001
+            self.err = str(e)
+        self._stop = threading.Event()
+
+    def _run(self):
+        while not self._stop.is_set():
+            self.sample()
+            time.sleep(0.002)
+
+    def sample(self):
+        if not self.ok:
+            return
+        try:
+            self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+            r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+            for bit, name in self.NAMES.items():
+                if r & bit and name != "gpu_idle":
+                    self.reasons.add(name)
+        except Exception:  # noqa: BLE001
+            pass
+
+    def __enter__(self):
+        self.sample()
+        self.t = threading.Thread(target=self._run, daemon=True)
+        self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self.t.join()
+        self.sample()
+
+    def summary(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "note": getattr(self, "err", "")}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def dist_setup(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl" if args.impl == "ours" else "gloo", device_id=torch.device("cuda", local)
+                                if args.impl == "ours" else None)
+    return world, rank, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def make_inputs(cfg, seed, device):
+    """Synthetic random-init Q/K/V of the named shape (torch Philox, fixed seed)."""
+    import torch
+    dt = {"bf16": torch.bfloat16, "f16": torch.float16, "f32": torch.float32}[cfg["dtype"]]
+    gen = torch.Generator(device=device).manual_seed(seed)
+    B, Hq, Hkv, L, d = cfg["B"], cfg["Hq"], cfg["Hkv"], cfg["L"], cfg["d"]
+    K = torch.randn((B, Hkv, L, d), generator=gen, device=device, dtype=torch.float32).to(dt)
+    V = torch.randn((B, Hkv, L, d), generator=gen, device=device, dtype=torch.float32).to(dt)
+    q = torch.randn((B, Hq, d), generator=gen, device=device, dtype=torch.float32).to(dt)
+    kn = torch.randn((B, Hkv, d), generator=gen, device=device, dtype=torch.float32).to(dt)
+    vn = torch.randn((B, Hkv, d), generator=gen, device=device, dtype=torch.float32).to(dt)
+    return K, V, q, kn, vn
+
+
+# ---------------------------------------------------------------------------------------
+def run_ours(args, cfg, world, rank, local):
+    import torch
+
+    import paper_2508_08256_b200 as F
+    from paper_2508_08256_b200 import _lib
+    from paper_2508_08256_b200.api import _p, _stream
+
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    lib = _lib.load()
+    B, Hq, Hkv, L, d, n, g = (cfg[k] for k in ("B", "Hq", "Hkv", "L", "d", "n", "g"))
+    pos = L - 1  # the step appends token L-1: a decode step at context L
+    packed, kvb, qo = algorithmic_bytes(cfg)
+    touched = packed + kvb + qo
+    l2 = torch.cuda.get_device_properties(dev).L2_cache_size
+    n_layers = max(1, min(16, math.ceil(2.5 * l2 / touched)))
+    if args.layers:
+        n_layers = args.layers
+    layers, inputs = [], []
+    for i in range(n_layers):
+        K, V, q, kn, vn = make_inputs(cfg, 1234 + 1000 * rank + i, dev)
+        layer = F.DecodeLayer(B, Hq, Hkv, L, d, g, dtype=K.dtype, device=dev, K=K, V=V)
+        layer.prefill(pos)
+        layer.workspace(pos + 1, n)
+        layers.append(layer)
+        inputs.append((q, kn, vn))
+    outs = [torch.empty((B, Hq, d), dtype=torch.float32, device=dev) for _ in range(n_layers)]
+    sels = [torch.empty((B, Hq, n), dtype=torch.int32, device=dev) for _ in range(n_layers)]
+    torch.cuda.synchronize()
+
+    stream = torch.cuda.Stream(device=dev)
+    torch.cuda.set_stream(stream)
+
+    def step(i):
+        li = i % n_layers
+        q, kn, vn = inputs[li]
+        layers[li].step(q, kn, vn, pos, n, out=outs[li], sel=sels[li])
+
+    # capture one CUDA graph per layer instance (launch-bound inner loop)
+    graphs = []
+    for li in range(n_layers):
+        step(li)  # warm the plan / attributes outside capture
+    torch.cuda.synchronize()
+    for li in range(n_layers):
+        gph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(gph, stream=stream):
+            step(li)
+        graphs.append(gph)
+    torch.cuda.synchronize()
+
+    for i in range(args.warmup):
+        graphs[i % n_layers].replay()
+    torch.cuda.synchronize()
+    barrier(world)
+    torch.cuda.synchronize()
+    sampler = ClockSampler(local)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with sampler:
+        e0.record(stream)
+        for i in range(args.steps):
+            graphs[i % n_layers].replay()
+        e1.record(stream)
+        torch.cuda.synchronize()
+    barrier(world)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    ms = max_over_ranks(ms, world)
+    us_per_step = ms * 1000.0 / args.steps
+
+    # ---- per-kernel breakdown (events between the same C-ABI launches, same stream) ----
+    ld = lib.fier_step_scores_ld(pos + 1)
+    scores = [torch.empty((B, Hq, ld), dtype=torch.float32, device=dev) for _ in range(n_layers)]
+    part_bytes = lib.fier_sparse_attention_workspace(__import__("ctypes").byref(layers[0].shape), n)
+    parts = [torch.empty(part_bytes, dtype=torch.uint8, device=dev) for _ in range(n_layers)]
+    names = ["append", "score", "topk", "sparse_attn"]
+    reps = max(3 * n_layers, 30)
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(reps)]
+    import ctypes as C
+    for r in range(reps + n_layers):
+        li = r % n_layers
+        lay, (q, kn, vn) = layers[li], inputs[li]
+        sh = C.byref(lay.shape)
+        e = ev[r - n_layers] if r >= n_layers else None
+        if e: e[0].record(stream)
+        _lib.check(lib.fier_append(sh, _p(lay.K), _p(lay.V), _p(kn), _p(vn), pos, _p(lay.pk.bits),
+                                   _p(lay.pk.params), None, _stream()))
+        if e: e[1].record(stream)
+        _lib.check(lib.fier_score(sh, _p(q), _p(lay.pk.bits), _p(lay.pk.params), pos + 1, _p(scores[li]),
+                                  ld, _stream()))
+        if e: e[2].record(stream)
+        _lib.check(lib.fier_topk(_p(scores[li]), B * Hq, pos + 1, ld, n, _p(sels[li]), None, 0, _stream()))
+        if e: e[3].record(stream)
+        _lib.check(lib.fier_sparse_attention(sh, _p(q), _p(lay.K), _p(lay.V), _p(sels[li]), n, pos + 1,
+                                             1.0 / math.sqrt(d), _p(outs[li]), _p(parts[li]),
+                                             parts[li].numel(), _stream()))
+        if e: e[4].record(stream)
+    torch.cuda.synchronize()
+    per = {k: statistics.mean(ev[r][i].elapsed_time(ev[r][i + 1]) * 1000.0 for r in range(reps))
+           for i, k in enumerate(names)}
+
+    # ---- K0: in-house full-KV decode attention on the same caches ----
+    fws = torch.empty(lib.fier_full_attention_workspace(C.byref(layers[0].shape), pos + 1),
+                      dtype=torch.uint8, device=dev)
+    for i in range(max(args.warmup, n_layers)):
+        layers[i % n_layers].full_step(inputs[i % n_layers][0], pos + 1, out=outs[i % n_layers], ws=fws)
+    torch.cuda.synchronize()
+    fsteps = max(n_layers * 4, min(args.steps, 400))
+    e0.record(stream)
+    for i in range(fsteps):
+        layers[i % n_layers].full_step(inputs[i % n_layers][0], pos + 1, out=outs[i % n_layers], ws=fws)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    full_us = e0.elapsed_time(e1) * 1000.0 / fsteps
+
+    # ---- e2e: public API with host buffers, H2D + step + D2H inside the timed region ----
+    hq_in = [tuple(t.cpu().pin_memory() for t in inp) for inp in inputs]
+    hout = [torch.empty((B, Hq, d), dtype=torch.float32).pin_memory() for _ in range(n_layers)]
+    dq = [tuple(torch.empty_like(t) for t in inp) for inp in inputs]
+    h2d = sum(t.numel() * t.element_size() for t in hq_in[0])
+    d2h = hout[0].numel() * 4
+
+    def e2e_step(li):
+        for dst, src in zip(dq[li], hq_in[li]):
+            dst.copy_(src, non_blocking=True)
+        layers[li].step(dq[li][0], dq[li][1], dq[li][2], pos, n, out=outs[li], sel=sels[li])
+        hout[li].copy_(outs[li], non_blocking=True)
+
+    egraphs = []
+    for li in range(n_layers):
+        e2e_step(li)
+    torch.cuda.synchronize()
+    for li in range(n_layers):
+        gph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(gph, stream=stream):
+            e2e_step(li)
+        egraphs.append(gph)
+    for i in range(args.warmup):
+        egraphs[i % n_layers].replay()
+    torch.cuda.synchronize()
+    barrier(world)
+    e0.record(stream)
+    for i in range(args.steps):
+        egraphs[i % n_layers].replay()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_us = max_over_ranks(e0.elapsed_time(e1), world) * 1000.0 / args.steps
+
+    # unique (kv head, token) rows actually selected (GQA overlap), last step of layer 0
+    s0 = sels[0].view(B, Hkv, Hq // Hkv, n).long()
+    key = (torch.arange(B * Hkv, device=dev).view(B, Hkv, 1, 1) * L + s0).flatten()
+    unique_rows = int(torch.unique(key).numel())
+
+    # ---- roofline of the dominant kernel ----
+    peak, peak_src = peaks()
+    es = elem_size(cfg["dtype"])
+    alg = {
+        "score": packed + B * Hq * d * es,
+        "sparse_attn": B * Hq * n * d * 2 * es + qo,
+        "append": B * Hkv * (g * d * es + 2 * d * es + g * d // 8 + d * 4),
+        "topk": None,
+    }
+    dom = max(per, key=per.get)
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        traffic = json.load(open(tpath)).get(args.config, {}).get(dom)
+    roof = None
+    if alg.get(dom):
+        ach = alg[dom] / (per[dom] * 1e-6) / 1e9
+        roof = {"bound": "hbm", "kernel": dom, "achieved": round(ach, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(ach / peak, 4), "traffic": traffic, "alg_bytes": alg[dom],
+                "peak_source": peak_src}
+    pk_u, kv_u, qo_u = algorithmic_bytes(cfg, unique_rows)
+    step_bytes = packed + kvb + qo
+    step_gbs = step_bytes / (us_per_step * 1e-6) / 1e9
+    res = {
+        "per_kernel_us": {k: round(v, 3) for k, v in per.items()},
+        "roofline": roof,
+        "step_roofline": {"alg_bytes": step_bytes, "alg_bytes_unique_rows": pk_u + kv_u + qo_u,
+                          "unique_rows": unique_rows, "achieved_gbs": round(step_gbs, 1),
+                          "frac_of_measured": round(step_gbs / peak, 4),
+                          "frac_of_8TBs": round(step_gbs / 8000.0, 4)},
+        "full_kv": {"us_per_step": round(full_us, 3),
+                    "achieved_gbs": round(full_kv_bytes(cfg) / (full_us * 1e-6) / 1e9, 1),
+                    "speedup_fier_vs_full": round(full_us / us_per_step, 3)},
+        "e2e": {"value": round(e2e_us, 3), "unit": UNIT, "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h},
+        "clocks": sampler.summary(),
+        "n_layers": n_layers,
+    }
+    # data for the CPU baseline: layer 0's caches and step-0 query, exactly as the GPU saw them
+    res["_cpu_inputs"] = (layers[0].K, layers[0].V, inputs[0])
+    return us_per_step, ms, res
+
+
+def cpu_baseline(cfg, K, V, inp, budget_s=20.0):
+    """oracle/_ref (the reference compiled from its headers) on the host cores: a full
+    decode step of this layer (every q head), all host threads, median of reps."""
+    import numpy as np
+    import torch
+
+    from oracle.oracle import REF_SO, Port, Ref, RefLayer
+    kind = "reference" if os.path.exists(REF_SO) else "port"
+    threads = os.cpu_count() or 1
+    q, kn, vn = inp
+    b = 0
+    Kc = K[b].float().cpu().numpy()
+    Vc = V[b].float().cpu().numpy()
+    Kc[:, -1] = kn[b].float().cpu().numpy()  # the appended token
+    Vc[:, -1] = vn[b].float().cpu().numpy()
+    Q = q[b].float().cpu().numpy()
+    if kind != "reference":
+        return {"value": None, "unit": UNIT, "cores": threads, "kind": "port",
+                "sample": "oracle/_ref missing; not timed"}
+    ref = Ref()
+    t0 = time.time()
+    layer = RefLayer(ref, Kc, Vc, g=cfg["g"], threads=threads)
+    build_s = time.time() - t0
+    n = cfg["n"]
+    Hq = cfg["Hq"]
+    # first rep on all heads sizes the sample
+    secs, _, _ = layer.step(Q, n)
+    reps = [secs]
+    while sum(reps) < budget_s / 4 and len(reps) < 5:
+        reps.append(layer.step(Q, n)[0])
+    layer.close()
+    med = statistics.median(reps)
+    scale = cfg["B"]  # the sample is one sequence of the batch
+    return {"value": round(med * scale * 1e6, 1), "unit": UNIT, "cores": threads, "kind": kind,
+            "sample": f"one full decode step of sequence 0 ({Hq} q heads, l={cfg['L']}, n={n}, fp64) x "
+                      f"{scale} sequences, median of {len(reps)} reps; index built once ({build_s:.1f}s, "
+                      f"hoisted)", "cpu": _cpu_model()}
+
+
+def _cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
+# ---------------------------------------------------------------------------------------
+def run_reference(args, cfg, world, rank):
+    """The reference's own CPU path (oracle/_ref) on this host, same config/metric."""
+    import numpy as np
+    import torch
+
+    from oracle.oracle import REF_SO, Ref, RefLayer
+    if rank != 0:
+        return None
+    if not os.path.exists(REF_SO):
+        return {"impl": "reference", "unavailable": "oracle/_ref/libfier_ref.so not built"}
+    threads = os.cpu_count() or 1
+    K, V, q, kn, vn = make_inputs(cfg, 1234, "cpu")
+    Kc = K[0].float().numpy()
+    Vc = V[0].float().numpy()
+    Kc[:, -1] = kn[0].float().numpy()
+    Vc[:, -1] = vn[0].float().numpy()
+    Q = q[0].float().numpy()
+    ref = Ref()
+    layer = RefLayer(ref, Kc, Vc, g=cfg["g"], threads=threads)
+    Hq, n = cfg["Hq"], cfg["n"]
+    # size each timed step so the whole run stays within ~2 minutes
+    t_full = layer.step(Q, n)[0]
+    budget = 120.0
+    heads = max(1, min(Hq, int(Hq * budget / max(1e-9, (args.steps + args.warmup) * t_full))))
+    heads = max(heads, min(Hq, threads))
+    times = []
+    for i in range(args.warmup + args.steps):
+        h0 = (i * heads) % Hq
+        h1 = min(Hq, h0 + heads)
+        secs = layer.step(Q, n, heads=(h0, h1))[0] * Hq / (h1 - h0)
+        if i >= args.warmup:
+            times.append(secs)
+    layer.close()
+    us = statistics.mean(times) * 1e6 * cfg["B"]
+    sample = (f"each step: fier_attend (approx_scores -> topk_oracle -> gather_attention, fp64) over "
+              f"{heads} of {Hq} q heads of sequence 0, scaled x{Hq}/{heads} heads and x{cfg['B']} "
+              f"sequences; {threads} std::threads; index hoisted (quantize once)")
+    return {
+        "impl": "reference", "metric": METRIC, "value": round(us, 1), "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(us / 1000.0, 3),
+        "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (torch Philox seed 1234, bf16-rounded, widened to fp64)",
+        "config": config_block(args, cfg, world),
+        "cpu_baseline": {"value": round(us, 1), "unit": UNIT, "cores": threads, "kind": "reference",
+                         "sample": sample, "cpu": _cpu_model()},
+        "e2e": {"value": round(us, 1), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+
+
+def config_block(args, cfg, world, n_layers=None, touched=None):
+    c = {"workload": cfg["desc"], "batch": cfg["B"], "q_heads": cfg["Hq"], "kv_heads": cfg["Hkv"],
+         "context": cfg["L"], "head_dim": cfg["d"], "budget_n": cfg["n"], "group_g": cfg["g"],
+         "parallelism": f"replicas x{world} (independent sequences, no collective)" if world > 1 else "1 GPU",
+         "config_id": args.config}
+    if n_layers:
+        c["l2"] = (f"inputs larger than L2: {n_layers} layer instances rotated, "
+                   f"{n_layers * touched / 1e6:.0f} MB touched per rotation")
+    return c
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=2000)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--layers", type=int, default=0, help="override the layer-rotation count")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    cfg = CONFIGS[args.config]
+    world, rank, local = dist_setup(args)
+
+    if args.impl == "reference":
+        out = run_reference(args, cfg, world, rank)
+        if rank == 0 and out is not None:
+            print(json.dumps(out))
+        return
+
+    us, ms, res = run_ours(args, cfg, world, rank, local)
+    K, V, inp = res.pop("_cpu_inputs")
+    if rank == 0:
+        packed, kvb, qo = algorithmic_bytes(cfg)
+        cpu = None
+        if world == 1 and not args.no_cpu_baseline:
+            cpu = cpu_baseline(cfg, K, V, inp)
+        line = {
+            "metric": METRIC, "value": round(us, 3), "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(us / 1000.0, 6),
+            "higher_is_better": False, "scaling": "weak", "vs_baseline": None,
+            "dtype": cfg["dtype"], "data": "synthetic random-init Q/K/V (torch Philox), prefix index pre-packed",
+            "config": config_block(args, cfg, world, res["n_layers"], packed + kvb + qo),
+            "roofline": res["roofline"], "cpu_baseline": cpu, "e2e": res["e2e"],
+            "gpu_launches": args.steps * KERNELS_PER_STEP, "clocks": res["clocks"],
+            "per_kernel_us": res["per_kernel_us"], "step_roofline": res["step_roofline"],
+            "full_kv": res["full_kv"],
+        }
+        print(json.dumps(line))
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

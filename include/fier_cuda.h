@@ -1,0 +1,146 @@
+/*
+ * fier_cuda.h -- C ABI of the B200 (sm_100a) Fier decode-time KV retrieval path.
+ *
+ * This is the drop-in boundary for the reference's hot path (arxiv 2508.08256,
+ * reference at proj/include/fier/).  Every entry point below replaces one
+ * reference function; the citation names the reference interface.  A C++
+ * shim with the reference's own signatures (fier::cuda::quantize,
+ * approx_scores, topk_oracle, gather_attention, fier_select, fier_attend)
+ * lives in fier_cuda.hpp; see INTEGRATION.md for ctypes / C++ bindings.
+ *
+ * Conventions
+ *  - Plain C: device pointers, sizes and a cudaStream_t passed as void*.
+ *  - Nothing allocates: the caller owns every buffer and workspace
+ *    (size-query functions below).  Calls are stream-ordered, never block,
+ *    and are CUDA-graph capturable.
+ *  - Return 0 on success, else FIER_EINVAL (1, the reference's
+ *    std::invalid_argument from require(), core.hpp:19-21), FIER_EDATA (2,
+ *    fier::DataError, io.hpp:29-31) or FIER_ECUDA (3).  fier_last_error()
+ *    returns the thread's last message, using the reference's message text.
+ *  - Data races: concurrent calls need distinct output/workspace buffers.
+ *
+ * Device layouts (one "layer" of a batch of B sequences):
+ *   K, V   : dtype [B][Hkv][cap][d]           token rows contiguous
+ *   bits   : uint32 [B][Hkv][cap][W], W=ceil(d/32); bit i of word w is channel
+ *            32w+i, 1 <=> code +1.  Byte-identical to the reference's in-memory
+ *            code_words (quant1bit.hpp:38-49) and FIER bit plane when 32 | d.
+ *   params : half2 [B][Hkv][ceil(cap/g)][d] = (s, z) as IEEE binary16
+ *            (the on-disk precision of io.hpp:205-211), group-major like the
+ *            in-memory scales/zeros [gi*d + j] (quant1bit.hpp:39-42).
+ *   q      : dtype [B][Hq][d];  scores : float [B][Hq][ld];  sel : int32 [B][Hq][n]
+ *            ascending (core.hpp:146);  out : float [B][Hq][d].
+ *   GQA    : q head h reads kv head h / (Hq/Hkv); selection is per q head.
+ */
+#ifndef FIER_CUDA_H_
+#define FIER_CUDA_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define FIER_API __attribute__((visibility("default")))
+#else
+#define FIER_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum fier_status { FIER_OK = 0, FIER_EINVAL = 1, FIER_EDATA = 2, FIER_ECUDA = 3 };
+enum fier_dtype { FIER_F32 = 0, FIER_F16 = 1, FIER_BF16 = 2 };
+
+/* Shape of one layer's cache.  All fields are plain integers. */
+typedef struct fier_shape {
+    int32_t batch;     /* B sequences                               */
+    int32_t q_heads;   /* Hq (multiple of kv_heads)                 */
+    int32_t kv_heads;  /* Hkv                                       */
+    int32_t capacity;  /* allocated tokens per sequence (cap)       */
+    int32_t dim;       /* head dim d (1..1024)                      */
+    int32_t group;     /* g, tokens per quantization group (>= 1)   */
+    int32_t dtype;     /* enum fier_dtype of K, V, q                */
+} fier_shape;
+
+/* ---- errors / sizes --------------------------------------------------------- */
+FIER_API const char* fier_last_error(void);
+FIER_API int fier_version(void);
+/* Bytes of the bit plane / the (s,z) table for the whole layer. */
+FIER_API size_t fier_bits_bytes(const fier_shape* s);
+FIER_API size_t fier_params_bytes(const fier_shape* s);
+/* Exact accounted payload of one (sequence, kv head) index at `tokens`
+ * (PackedKeys::payload_bytes, quant1bit.hpp:60-62). */
+FIER_API size_t fier_payload_bytes(int32_t tokens, int32_t dim, int32_t group);
+
+/* ---- K1: 1-bit key packer ---------------------------------------------------- */
+/* quantize (quant1bit.hpp:65-103) of tokens [0, tokens) of every (b, kv head).
+ * Bits compare against the fp64 midpoint; (s, z) stored RNE to binary16
+ * (half.hpp:30-61).  *nonfinite (device int, may be NULL) is set to 1 if any
+ * key is not finite ("quantize: non-finite key entry", quant1bit.hpp:68). */
+FIER_API int fier_pack_keys(const fier_shape* s, const void* K, int32_t tokens, uint32_t* bits,
+                   void* params, int32_t* nonfinite, void* stream);
+
+/* Decode-time append: write k_new/v_new ([B][Hkv][d]) as token `pos` of K/V
+ * and re-pack the open group [floor(pos/g)*g, pos] so the index equals
+ * quantize(K[0:pos+1]) bit for bit (quant1bit.hpp:84 short final group). */
+FIER_API int fier_append(const fier_shape* s, void* K, void* V, const void* k_new, const void* v_new,
+                int32_t pos, uint32_t* bits, void* params, int32_t* nonfinite, void* stream);
+
+/* ---- K2: packed-key scorer --------------------------------------------------- */
+/* approx_scores (quant1bit.hpp:121-140) for all (b, q head): scores[b][h][t],
+ * t < tokens, row stride ld >= tokens.  fp32 accumulation. */
+FIER_API int fier_score(const fier_shape* s, const void* q, const uint32_t* bits, const void* params,
+               int32_t tokens, float* scores, int64_t ld, void* stream);
+
+/* ---- K3: Top-k selector -------------------------------------------------------- */
+/* topk_oracle (core.hpp:134-148) on `rows` rows of `tokens` fp32 scores
+ * (row stride ld): the k largest, ties to the lower index, ascending output
+ * in sel[row][0..k).  Requires 1 <= k <= tokens ("topk_oracle: k out of range"). */
+FIER_API size_t fier_topk_workspace(int32_t rows, int32_t tokens, int32_t k);
+FIER_API int fier_topk(const float* scores, int32_t rows, int32_t tokens, int64_t ld, int32_t k,
+              int32_t* sel, void* workspace, size_t workspace_bytes, void* stream);
+
+/* ---- K4: sparse attention over the selected rows ------------------------------ */
+/* gather_attention (core.hpp:152-179): out[b][h] = softmax(scale * q K[sel]^T) V[sel]
+ * over the n ascending indices sel[b][h][0..n) (< tokens).  Partial softmaxes
+ * of KV splits are merged by log-sum-exp.  scale = 1/sqrt(d) reproduces the
+ * reference default (scaled=true, core.hpp:154). */
+FIER_API size_t fier_sparse_attention_workspace(const fier_shape* s, int32_t n);
+FIER_API int fier_sparse_attention(const fier_shape* s, const void* q, const void* K, const void* V,
+                          const int32_t* sel, int32_t n, int32_t tokens, float scale, float* out,
+                          void* workspace, size_t workspace_bytes, void* stream);
+
+/* ---- K0: full-KV decode attention (the in-house baseline) --------------------- */
+/* gather_attention over all indices (the `full` policy, retrieval.hpp:159-166). */
+FIER_API size_t fier_full_attention_workspace(const fier_shape* s, int32_t tokens);
+FIER_API int fier_full_attention(const fier_shape* s, const void* q, const void* K, const void* V,
+                        int32_t tokens, float scale, float* out, void* workspace,
+                        size_t workspace_bytes, void* stream);
+
+/* ---- fused decode step --------------------------------------------------------- */
+/* fier_attend (retrieval.hpp:136-146) for a decode step of every (b, q head):
+ * append(pos) -> score -> Top-n -> sparse attention, over tokens = pos + 1.
+ * scores_out (may be NULL) receives the estimated logits (ld = tokens rounded
+ * up to 32, see fier_step_scores_ld). */
+FIER_API size_t fier_decode_workspace(const fier_shape* s, int32_t tokens, int32_t n);
+FIER_API int64_t fier_step_scores_ld(int32_t tokens);
+FIER_API int fier_decode_step(const fier_shape* s, const void* q, const void* k_new, const void* v_new,
+                     int32_t pos, void* K, void* V, uint32_t* bits, void* params, int32_t n,
+                     float scale, float* out, int32_t* sel, float* scores_out, void* workspace,
+                     size_t workspace_bytes, void* stream);
+
+/* ---- host-side format conversion (no GPU) -------------------------------------- */
+/* serialize_packed_keys (io.hpp:197-225) of one (b, kv head) index copied to
+ * host: bits [tokens][W] uint32, params [ceil(tokens/g)][d] (s, z) binary16
+ * pairs.  out must hold 18 + fier_payload_bytes(tokens, d, g) bytes. */
+FIER_API int fier_index_to_fier(const uint32_t* bits, const uint16_t* params, int32_t tokens, int32_t dim,
+                       int32_t group, uint8_t* out, size_t out_bytes);
+/* parse_packed_keys (io.hpp:227-277) into the device layout (host buffers).
+ * Returns FIER_EDATA with the reference's diagnostics on malformed input. */
+FIER_API int fier_fier_to_index(const uint8_t* buf, size_t len, int32_t* tokens, int32_t* dim,
+                       int32_t* group, uint32_t* bits, size_t bits_cap, uint16_t* params,
+                       size_t params_cap);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FIER_CUDA_H_ */

@@ -1,0 +1,28 @@
+"""B200-native (sm_100a) Fier decode-time KV retrieval (arxiv 2508.08256).
+
+Hot path: 1-bit key packing -> packed q.K scoring -> per-head Top-k -> sparse
+attention over the selected K/V rows, as hand-written CUDA kernels behind the
+C ABI in include/fier_cuda.h.  ``api`` mirrors the reference's C++ entry points
+(quantize, approx_scores, topk_oracle, gather_attention, fier_select,
+fier_attend) on torch CUDA tensors.
+"""
+from . import _lib  # noqa: F401
+from .api import (  # noqa: F401
+    DecodeLayer,
+    PackedKeys,
+    RetrievalResult,
+    alloc_index,
+    append_token,
+    approx_scores,
+    fier_attend,
+    fier_select,
+    full_attention,
+    gather_attention,
+    quantize,
+    topk_oracle,
+)
+
+__all__ = [
+    "DecodeLayer", "PackedKeys", "RetrievalResult", "alloc_index", "append_token", "approx_scores",
+    "fier_attend", "fier_select", "full_attention", "gather_attention", "quantize", "topk_oracle",
+]

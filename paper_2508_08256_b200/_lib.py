@@ -1,0 +1,105 @@
+"""ctypes binding of libfier_cuda.so (include/fier_cuda.h).
+
+There is no fallback: if the library is missing or no CUDA device is present,
+every compute entry point raises.  The .so is built in-tree by
+``python -m paper_2508_08256_b200.build`` (``__graft_entry__.build()``).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libfier_cuda.so")
+
+FIER_OK, FIER_EINVAL, FIER_EDATA, FIER_ECUDA = 0, 1, 2, 3
+FIER_F32, FIER_F16, FIER_BF16 = 0, 1, 2
+
+# every symbol include/fier_cuda.h declares
+EXPORTS = (
+    "fier_last_error", "fier_version", "fier_bits_bytes", "fier_params_bytes", "fier_payload_bytes",
+    "fier_pack_keys", "fier_append", "fier_score", "fier_topk_workspace", "fier_topk",
+    "fier_sparse_attention_workspace", "fier_sparse_attention", "fier_full_attention_workspace",
+    "fier_full_attention", "fier_decode_workspace", "fier_step_scores_ld", "fier_decode_step",
+    "fier_index_to_fier", "fier_fier_to_index",
+)
+
+
+class FierShape(C.Structure):
+    _fields_ = [("batch", C.c_int32), ("q_heads", C.c_int32), ("kv_heads", C.c_int32),
+                ("capacity", C.c_int32), ("dim", C.c_int32), ("group", C.c_int32),
+                ("dtype", C.c_int32)]
+
+
+class FierDataError(RuntimeError):
+    """fier::DataError (io.hpp:29-31)."""
+
+
+class FierCudaError(RuntimeError):
+    """A CUDA launch/runtime failure inside the library."""
+
+
+_vp = C.c_void_p
+_sz = C.c_size_t
+_i32 = C.c_int32
+_i64 = C.c_int64
+_SP = C.POINTER(FierShape)
+
+_SIGS = {
+    "fier_last_error": ([], C.c_char_p),
+    "fier_version": ([], C.c_int),
+    "fier_bits_bytes": ([_SP], _sz),
+    "fier_params_bytes": ([_SP], _sz),
+    "fier_payload_bytes": ([_i32, _i32, _i32], _sz),
+    "fier_pack_keys": ([_SP, _vp, _i32, _vp, _vp, _vp, _vp], C.c_int),
+    "fier_append": ([_SP, _vp, _vp, _vp, _vp, _i32, _vp, _vp, _vp, _vp], C.c_int),
+    "fier_score": ([_SP, _vp, _vp, _vp, _i32, _vp, _i64, _vp], C.c_int),
+    "fier_topk_workspace": ([_i32, _i32, _i32], _sz),
+    "fier_topk": ([_vp, _i32, _i32, _i64, _i32, _vp, _vp, _sz, _vp], C.c_int),
+    "fier_sparse_attention_workspace": ([_SP, _i32], _sz),
+    "fier_sparse_attention": ([_SP, _vp, _vp, _vp, _vp, _i32, _i32, C.c_float, _vp, _vp, _sz, _vp],
+                              C.c_int),
+    "fier_full_attention_workspace": ([_SP, _i32], _sz),
+    "fier_full_attention": ([_SP, _vp, _vp, _vp, _i32, C.c_float, _vp, _vp, _sz, _vp], C.c_int),
+    "fier_decode_workspace": ([_SP, _i32, _i32], _sz),
+    "fier_step_scores_ld": ([_i32], _i64),
+    "fier_decode_step": ([_SP, _vp, _vp, _vp, _i32, _vp, _vp, _vp, _vp, _i32, C.c_float, _vp, _vp,
+                          _vp, _vp, _sz, _vp], C.c_int),
+    "fier_index_to_fier": ([_vp, _vp, _i32, _i32, _i32, _vp, _sz], C.c_int),
+    "fier_fier_to_index": ([_vp, _sz, C.POINTER(_i32), C.POINTER(_i32), C.POINTER(_i32), _vp, _sz, _vp,
+                            _sz], C.c_int),
+}
+
+_lib = None
+
+
+def load(path: str = LIB_PATH) -> C.CDLL:
+    """Load the library (once).  Raises if it is missing: no fallback path."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise ImportError(
+            f"{path} not found: the Fier CUDA library is required (build it with "
+            "`python -m paper_2508_08256_b200.build`); there is no CPU fallback")
+    lib = C.CDLL(path)
+    for name, (args, res) in _SIGS.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = res
+    _lib = lib
+    return lib
+
+
+def last_error() -> str:
+    return load().fier_last_error().decode()
+
+
+def check(rc: int) -> None:
+    if rc == FIER_OK:
+        return
+    msg = last_error()
+    if rc == FIER_EINVAL:
+        raise ValueError(msg)  # std::invalid_argument (core.hpp:19-21)
+    if rc == FIER_EDATA:
+        raise FierDataError(msg)
+    raise FierCudaError(msg)

@@ -1,0 +1,372 @@
+"""Torch-facing mirror of the reference's Fier API, running on the sm_100a kernels.
+
+Same names, argument meaning and error behaviour as the reference's C++ entry
+points (proj/include/fier/):
+
+=====================  =========================================  ==============================
+this module            reference                                   kernel
+=====================  =========================================  ==============================
+quantize               quantize            quant1bit.hpp:65-103    K1 pack  (fier_pack_keys)
+append_token           (decode-time growth, quant1bit.hpp:84)      K1 append (fier_append)
+approx_scores          approx_scores       quant1bit.hpp:121-140   K2 score (fier_score)
+topk_oracle            topk_oracle         core.hpp:134-148        K3 top-k (fier_topk)
+gather_attention       gather_attention    core.hpp:152-179        K4 sparse attention
+full_attention         full policy         retrieval.hpp:159-166   K0 full-KV attention
+fier_select            fier_select         retrieval.hpp:130-133   K2 -> K3
+fier_attend            fier_attend         retrieval.hpp:136-146   K2 -> K3 -> K4
+DecodeLayer.step       fier_attend per decode step, batched       fier_decode_step
+=====================  =========================================  ==============================
+
+Tensors live on the GPU.  Single-head calls take the reference's shapes
+(K: [l, d], q: [d]); batched calls take K: [B, Hkv, l, d], q: [B, Hq, d].
+Precondition failures raise ValueError with the reference's message
+(std::invalid_argument from require(), core.hpp:19-21); malformed FIER bytes
+raise FierDataError (fier::DataError, io.hpp:29-31).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass
+from typing import Optional
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import FierShape, check
+
+_DT = {torch.float32: _lib.FIER_F32, torch.float16: _lib.FIER_F16, torch.bfloat16: _lib.FIER_BF16}
+
+
+def _stream() -> C.c_void_p:
+    return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _p(t: Optional[torch.Tensor]) -> C.c_void_p:
+    return C.c_void_p(t.data_ptr() if t is not None else 0)
+
+
+def _require(ok: bool, msg: str) -> None:
+    if not ok:
+        raise ValueError(msg)
+
+
+def _dtype_code(t: torch.Tensor) -> int:
+    _require(t.dtype in _DT, f"unsupported dtype {t.dtype}: expected float32, float16 or bfloat16")
+    return _DT[t.dtype]
+
+
+def _cuda(t: torch.Tensor, what: str) -> torch.Tensor:
+    _require(isinstance(t, torch.Tensor) and t.is_cuda, f"{what}: expected a CUDA tensor")
+    return t.contiguous()
+
+
+def _as4(K: torch.Tensor) -> torch.Tensor:
+    if K.dim() == 2:
+        return K.unsqueeze(0).unsqueeze(0)
+    _require(K.dim() == 4, "expected a [l, d] or [B, H, l, d] cache")
+    return K
+
+
+def _as3(q: torch.Tensor) -> torch.Tensor:
+    if q.dim() == 1:
+        return q.view(1, 1, -1)
+    _require(q.dim() == 3, "expected a [d] or [B, H, d] query")
+    return q
+
+
+def make_shape(batch, q_heads, kv_heads, capacity, dim, group, dtype) -> FierShape:
+    return FierShape(batch, q_heads, kv_heads, capacity, dim, group, dtype)
+
+
+@dataclass
+class PackedKeys:
+    """Device-resident Fier index (PackedKeys, quant1bit.hpp:32-63).
+
+    bits   : int32 view of uint32 [B, Hkv, cap, ceil(d/32)] (bit i of word w = channel 32w+i)
+    params : float16 [B, Hkv, ceil(cap/g), d, 2] = (s, z) rounded to binary16
+    """
+    bits: torch.Tensor
+    params: torch.Tensor
+    tokens: int
+    dim: int
+    group_size: int
+    batch: int
+    kv_heads: int
+    capacity: int
+    single: bool = False
+
+    @property
+    def groups_per_channel(self) -> int:
+        return (self.tokens + self.group_size - 1) // self.group_size
+
+    def payload_bytes(self) -> int:
+        """Per (sequence, kv head): l*ceil(d/8) + d*ceil(l/g)*4 (quant1bit.hpp:60-62)."""
+        return int(_lib.load().fier_payload_bytes(self.tokens, self.dim, self.group_size))
+
+    def scales(self) -> torch.Tensor:
+        """(s) as fp64, [B, Hkv, G, d] (or [G*d] single-head) -- half-rounded."""
+        s = self.params[:, :, : self.groups_per_channel, :, 0].double()
+        return s.reshape(-1) if self.single else s
+
+    def zeros(self) -> torch.Tensor:
+        z = self.params[:, :, : self.groups_per_channel, :, 1].double()
+        return z.reshape(-1) if self.single else z
+
+    def to_fier(self, b: int = 0, h: int = 0) -> bytes:
+        """serialize_packed_keys (io.hpp:197-225) of sequence b, kv head h."""
+        W = (self.dim + 31) // 32
+        bits = self.bits[b, h, : self.tokens].contiguous().cpu().numpy().view(np.uint32)
+        par = self.params[b, h, : self.groups_per_channel].contiguous().cpu().numpy().view(np.uint16)
+        out = np.zeros(18 + self.payload_bytes(), np.uint8)
+        check(_lib.load().fier_index_to_fier(bits.ctypes.data, par.ctypes.data, self.tokens, self.dim,
+                                             self.group_size, out.ctypes.data, out.size))
+        assert bits.size == self.tokens * W
+        return out.tobytes()
+
+    @staticmethod
+    def from_fier(buf: bytes, device="cuda", capacity: Optional[int] = None) -> "PackedKeys":
+        """parse_packed_keys (io.hpp:227-277) into a device index."""
+        lib = _lib.load()
+        b = np.frombuffer(buf, np.uint8)
+        l, d, g = C.c_int32(), C.c_int32(), C.c_int32()
+        check(lib.fier_fier_to_index(b.ctypes.data, b.size, C.byref(l), C.byref(d), C.byref(g),
+                                     None, 0, None, 0))
+        l, d, g = l.value, d.value, g.value
+        cap = capacity or l
+        W, G = (d + 31) // 32, (cap + g - 1) // g
+        bits = np.zeros((1, 1, cap, W), np.uint32)
+        par = np.zeros((1, 1, G, d, 2), np.uint16)
+        check(lib.fier_fier_to_index(b.ctypes.data, b.size, C.byref(C.c_int32()), C.byref(C.c_int32()),
+                                     C.byref(C.c_int32()), bits.ctypes.data, bits.size, par.ctypes.data,
+                                     par.size))
+        return PackedKeys(torch.from_numpy(bits.view(np.int32)).to(device),
+                          torch.from_numpy(par.view(np.float16)).to(device), l, d, g, 1, 1, cap,
+                          single=True)
+
+
+def alloc_index(batch, kv_heads, capacity, dim, group, device="cuda") -> PackedKeys:
+    W, G = (dim + 31) // 32, (capacity + group - 1) // group
+    bits = torch.zeros((batch, kv_heads, capacity, W), dtype=torch.int32, device=device)
+    params = torch.zeros((batch, kv_heads, G, dim, 2), dtype=torch.float16, device=device)
+    return PackedKeys(bits, params, 0, dim, group, batch, kv_heads, capacity)
+
+
+def _shape_of(pk: PackedKeys, q_heads: int, dtype: int) -> FierShape:
+    return make_shape(pk.batch, q_heads, pk.kv_heads, pk.capacity, pk.dim, pk.group_size, dtype)
+
+
+def quantize(K: torch.Tensor, group_size: int = 32, tokens: Optional[int] = None,
+             out: Optional[PackedKeys] = None) -> PackedKeys:
+    """quantize (quant1bit.hpp:65-103) on the GPU.  K: [l, d] or [B, Hkv, cap, d]."""
+    _require(group_size >= 1, "quantize: group size must be >= 1")
+    single = K.dim() == 2
+    K4 = _as4(_cuda(K, "quantize"))
+    B, H, cap, d = K4.shape
+    _require(cap >= 1 and d >= 1, "quantize: empty key cache")
+    tokens = cap if tokens is None else tokens
+    _require(1 <= tokens <= cap, "quantize: empty key cache")
+    pk = out or alloc_index(B, H, cap, d, group_size, K4.device)
+    flag = torch.zeros(1, dtype=torch.int32, device=K4.device)
+    shape = make_shape(B, H, H, cap, d, group_size, _dtype_code(K4))
+    check(_lib.load().fier_pack_keys(C.byref(shape), _p(K4), tokens, _p(pk.bits), _p(pk.params),
+                                     _p(flag), _stream()))
+    if int(flag.item()) != 0:
+        raise ValueError("quantize: non-finite key entry")
+    pk.tokens, pk.single = tokens, single
+    return pk
+
+
+def append_token(K: torch.Tensor, V: torch.Tensor, k_new: torch.Tensor, v_new: torch.Tensor,
+                 pos: int, pk: PackedKeys, check_finite: bool = True) -> PackedKeys:
+    """Write token `pos` of K/V and re-pack its open group in place (K1b)."""
+    K4, V4 = _as4(K), _as4(V)
+    B, H, cap, d = K4.shape
+    flag = torch.zeros(1, dtype=torch.int32, device=K4.device) if check_finite else None
+    shape = make_shape(B, H, H, cap, d, pk.group_size, _dtype_code(K4))
+    check(_lib.load().fier_append(C.byref(shape), _p(K4), _p(V4), _p(k_new.contiguous()),
+                                  _p(v_new.contiguous()), pos, _p(pk.bits), _p(pk.params), _p(flag),
+                                  _stream()))
+    if check_finite and int(flag.item()) != 0:
+        raise ValueError("quantize: non-finite key entry")
+    pk.tokens = max(pk.tokens, pos + 1)
+    return pk
+
+
+def approx_scores(q: torch.Tensor, pk: PackedKeys) -> torch.Tensor:
+    """approx_scores (quant1bit.hpp:121-140): fp32 [l] or [B, Hq, l]."""
+    single = q.dim() == 1
+    _require(q.shape[-1] == pk.dim, "approx_scores: query length does not match key dim")
+    q3 = _as3(_cuda(q, "approx_scores"))
+    B, Hq, d = q3.shape
+    _require(B == pk.batch and Hq % pk.kv_heads == 0, "approx_scores: query heads do not match index")
+    ld = pk.tokens
+    scores = torch.empty((B, Hq, ld), dtype=torch.float32, device=q3.device)
+    shape = _shape_of(pk, Hq, _dtype_code(q3))
+    check(_lib.load().fier_score(C.byref(shape), _p(q3), _p(pk.bits), _p(pk.params), pk.tokens,
+                                 _p(scores), ld, _stream()))
+    return scores.view(-1) if single else scores
+
+
+def topk_oracle(scores: torch.Tensor, k: int) -> torch.Tensor:
+    """topk_oracle (core.hpp:134-148): int32 ascending indices [k] or [..., k]."""
+    s = _cuda(scores, "topk_oracle")
+    _require(s.dtype == torch.float32, "topk_oracle: scores must be float32")
+    l = s.shape[-1]
+    _require(1 <= k <= l, "topk_oracle: k out of range")
+    rows = s.numel() // l
+    sel = torch.empty(s.shape[:-1] + (k,), dtype=torch.int32, device=s.device)
+    check(_lib.load().fier_topk(_p(s), rows, l, l, k, _p(sel), None, 0, _stream()))
+    return sel
+
+
+def _validate_selection(sel: torch.Tensor, tokens: int) -> None:
+    # Selection::valid_against (core.hpp:86-93)
+    _require(sel.shape[-1] >= 1, "gather_attention: empty selection")
+    ok = bool(((sel >= 0) & (sel < tokens)).all().item())
+    if sel.shape[-1] > 1:
+        ok = ok and bool((sel[..., 1:] > sel[..., :-1]).all().item())
+    _require(ok, "gather_attention: selection invalid for cache")
+
+
+def gather_attention(q: torch.Tensor, K: torch.Tensor, V: torch.Tensor, sel: torch.Tensor,
+                     scaled: bool = True, tokens: Optional[int] = None,
+                     validate: bool = True) -> torch.Tensor:
+    """gather_attention (core.hpp:152-179): fp32 [d] or [B, Hq, d]."""
+    single = q.dim() == 1
+    K4, V4 = _as4(_cuda(K, "gather_attention")), _as4(_cuda(V, "gather_attention"))
+    _require(K4.shape == V4.shape, "gather_attention: K and V are not row-aligned")
+    q3 = _as3(_cuda(q, "gather_attention"))
+    B, Hkv, cap, d = K4.shape
+    _require(q3.shape[-1] == d, "gather_attention: query length does not match key dim")
+    Hq = q3.shape[1]
+    sel3 = sel.to(torch.int32).reshape(B, Hq, -1).contiguous()
+    n = sel3.shape[-1]
+    tokens = cap if tokens is None else tokens
+    if validate:
+        _validate_selection(sel3, tokens)
+    shape = make_shape(B, Hq, Hkv, cap, d, 32, _dtype_code(K4))
+    lib = _lib.load()
+    ws_bytes = lib.fier_sparse_attention_workspace(C.byref(shape), n)
+    ws = torch.empty(max(ws_bytes, 4), dtype=torch.uint8, device=q3.device)
+    out = torch.empty((B, Hq, d), dtype=torch.float32, device=q3.device)
+    scale = 1.0 / math.sqrt(d) if scaled else 1.0
+    check(lib.fier_sparse_attention(C.byref(shape), _p(q3.to(K4.dtype)), _p(K4), _p(V4), _p(sel3), n,
+                                    tokens, scale, _p(out), _p(ws), ws.numel(), _stream()))
+    return out.view(-1) if single else out
+
+
+def full_attention(q: torch.Tensor, K: torch.Tensor, V: torch.Tensor, scaled: bool = True,
+                   tokens: Optional[int] = None) -> torch.Tensor:
+    """gather_attention over every index (`full` policy, retrieval.hpp:159-166) -- K0."""
+    single = q.dim() == 1
+    K4, V4 = _as4(_cuda(K, "gather_attention")), _as4(_cuda(V, "gather_attention"))
+    q3 = _as3(_cuda(q, "gather_attention"))
+    B, Hkv, cap, d = K4.shape
+    Hq = q3.shape[1]
+    tokens = cap if tokens is None else tokens
+    shape = make_shape(B, Hq, Hkv, cap, d, 32, _dtype_code(K4))
+    lib = _lib.load()
+    ws = torch.empty(max(lib.fier_full_attention_workspace(C.byref(shape), tokens), 4),
+                     dtype=torch.uint8, device=q3.device)
+    out = torch.empty((B, Hq, d), dtype=torch.float32, device=q3.device)
+    scale = 1.0 / math.sqrt(d) if scaled else 1.0
+    check(lib.fier_full_attention(C.byref(shape), _p(q3.to(K4.dtype)), _p(K4), _p(V4), tokens, scale,
+                                  _p(out), _p(ws), ws.numel(), _stream()))
+    return out.view(-1) if single else out
+
+
+def fier_select(q: torch.Tensor, pk: PackedKeys, n: int) -> torch.Tensor:
+    """fier_select (retrieval.hpp:130-133)."""
+    _require(1 <= n <= pk.tokens, "fier_select: budget out of range")
+    return topk_oracle(approx_scores(q, pk), n)
+
+
+@dataclass
+class RetrievalResult:
+    """RetrievalResult (retrieval.hpp:122-127)."""
+    selection: torch.Tensor
+    output: torch.Tensor
+    est_scores: torch.Tensor
+    bytes_loaded_for_estimation: int
+
+
+def fier_attend(q: torch.Tensor, K: torch.Tensor, V: torch.Tensor, pk: PackedKeys,
+                n: int) -> RetrievalResult:
+    """fier_attend (retrieval.hpp:136-146): estimate, select, exact attention on the subset."""
+    K4 = _as4(K)
+    _require(pk.tokens == K4.shape[2] and pk.dim == K4.shape[3],
+             "fier_attend: packed keys do not match cache")
+    est = approx_scores(q, pk)
+    _require(1 <= n <= pk.tokens, "topk_oracle: k out of range")
+    sel = topk_oracle(est, n)
+    out = gather_attention(q, K, V, sel, scaled=True, validate=False)
+    return RetrievalResult(sel, out, est, pk.payload_bytes())
+
+
+class DecodeLayer:
+    """One attention layer's decode-time state on the GPU, batched over B sequences.
+
+    Holds the KV cache [B, Hkv, cap, d], the Fier index, and the workspace of
+    ``fier_decode_step``; ``step`` is graph-capturable (no host sync, no
+    allocation).
+    """
+
+    def __init__(self, batch, q_heads, kv_heads, capacity, dim, group=32, dtype=torch.bfloat16,
+                 device="cuda", K=None, V=None):
+        self.B, self.Hq, self.Hkv, self.cap, self.d, self.g = batch, q_heads, kv_heads, capacity, dim, group
+        self.dtype = dtype
+        self.device = torch.device(device)
+        self.K = K if K is not None else torch.zeros((batch, kv_heads, capacity, dim), dtype=dtype,
+                                                     device=device)
+        self.V = V if V is not None else torch.zeros_like(self.K)
+        self.pk = alloc_index(batch, kv_heads, capacity, dim, group, device)
+        self.shape = make_shape(batch, q_heads, kv_heads, capacity, dim, group, _DT[dtype])
+        self.tokens = 0
+        self._ws = None
+        self._ws_key = None
+
+    def prefill(self, tokens: int) -> None:
+        """Pack the prefix [0, tokens) of the cache (hoisted quantize)."""
+        quantize(self.K, self.g, tokens=tokens, out=self.pk)
+        self.tokens = tokens
+
+    def workspace(self, tokens: int, n: int) -> torch.Tensor:
+        key = (tokens, n)
+        need = _lib.load().fier_decode_workspace(C.byref(self.shape), tokens, n)
+        if self._ws is None or self._ws.numel() < need:
+            self._ws = torch.empty(need, dtype=torch.uint8, device=self.device)
+        self._ws_key = key
+        return self._ws
+
+    def step(self, q, k_new, v_new, pos: int, n: int, out=None, sel=None, scores_out=None,
+             scale: Optional[float] = None):
+        """fier_attend for a decode step: append token `pos`, score, select n, attend."""
+        lib = _lib.load()
+        tokens = pos + 1
+        ws = self.workspace(tokens, n) if self._ws_key != (tokens, n) else self._ws
+        if out is None:
+            out = torch.empty((self.B, self.Hq, self.d), dtype=torch.float32, device=self.device)
+        if sel is None:
+            sel = torch.empty((self.B, self.Hq, n), dtype=torch.int32, device=self.device)
+        scale = 1.0 / math.sqrt(self.d) if scale is None else scale
+        check(lib.fier_decode_step(C.byref(self.shape), _p(q), _p(k_new), _p(v_new), pos, _p(self.K),
+                                   _p(self.V), _p(self.pk.bits), _p(self.pk.params), n, scale, _p(out),
+                                   _p(sel), _p(scores_out), _p(ws), ws.numel(), _stream()))
+        self.pk.tokens = max(self.pk.tokens, tokens)
+        self.tokens = max(self.tokens, tokens)
+        return out, sel
+
+    def full_step(self, q, tokens: int, out=None, ws=None, scale: Optional[float] = None):
+        """K0: full-KV decode attention over [0, tokens) (the baseline)."""
+        lib = _lib.load()
+        need = lib.fier_full_attention_workspace(C.byref(self.shape), tokens)
+        if ws is None or ws.numel() < need:
+            ws = torch.empty(need, dtype=torch.uint8, device=self.device)
+        if out is None:
+            out = torch.empty((self.B, self.Hq, self.d), dtype=torch.float32, device=self.device)
+        scale = 1.0 / math.sqrt(self.d) if scale is None else scale
+        check(lib.fier_full_attention(C.byref(self.shape), _p(q), _p(self.K), _p(self.V), tokens, scale,
+                                      _p(out), _p(ws), ws.numel(), _stream()))
+        return out

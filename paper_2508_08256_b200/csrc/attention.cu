@@ -1,0 +1,476 @@
+// attention.cu -- K4 sparse decode attention over the selected rows, K0 full-KV
+// decode attention (the in-house baseline), and the log-sum-exp merge.
+//
+// K4 replaces gather_attention (reference core.hpp:152-179) on the Top-k
+// selection; K0 is gather_attention over every index (the `full` policy,
+// retrieval.hpp:159-166).  Both are split-KV ("flash-decoding"): a CTA owns a
+// range of rows of one (sequence, head), each of its 4 warps streams its
+// sub-range through a private ring of shared-memory stages filled by the
+// bulk-copy engine (cp.async.bulk, one 256-B K row and one V row per copy for
+// the gather, one contiguous 8-row block per copy for K0), completion tracked
+// by mbarriers.  Per stage of 8 rows: 4 lanes per row compute q.k over d/4
+// channels each (fp32), an online softmax in the log2 domain, and lane L
+// accumulates p * V over channels [L*d/32, (L+1)*d/32).  The 4 warp states
+// are merged in shared memory into one partial (m, l, o[d]) per CTA; the
+// merge kernel combines the CTA partials by log-sum-exp.
+//
+// K0 shares every K/V row across the Hq/Hkv query heads of its GQA group.
+#include "common.cuh"
+
+namespace fier_cuda {
+
+constexpr int kAttnWarps = 4;
+constexpr int kRowsPerStage = 8;
+
+template <typename T, int D>
+struct AttnTraits {
+    static constexpr int RB = D * (int)sizeof(T);          // bytes per row
+    static constexpr int CH = D / 4;                        // channels per lane (logits)
+    static constexpr int EPV = 16 / (int)sizeof(T);         // elements per 16-B vector
+    static constexpr int VEC = CH / EPV;                    // 16-B vectors per lane (logits)
+    static constexpr int CPL = D / 32;                      // channels per lane (PV)
+    static constexpr int STAGE_BYTES = kRowsPerStage * RB;  // per K (or V) stage
+};
+
+__device__ __forceinline__ void load_channels(const float* p, float* f, int n) {
+    for (int i = 0; i < n; ++i) f[i] = p[i];
+}
+
+// PV operand: CPL consecutive channels of a V row in shared memory.
+template <typename T, int CPL>
+__device__ __forceinline__ void load_v(const T* row, int lane, float* f) {
+    if constexpr (sizeof(T) == 4) {
+        const float* p = reinterpret_cast<const float*>(row) + lane * CPL;
+        if constexpr (CPL == 4) {
+            const float4 v = *reinterpret_cast<const float4*>(p);
+            f[0] = v.x; f[1] = v.y; f[2] = v.z; f[3] = v.w;
+        } else {
+#pragma unroll
+            for (int i = 0; i < CPL; ++i) f[i] = p[i];
+        }
+    } else {
+        const uint32_t* p = reinterpret_cast<const uint32_t*>(row + lane * CPL);
+#pragma unroll
+        for (int i = 0; i < CPL / 2; ++i) {
+            const uint32_t w = p[i];
+            if constexpr (std::is_same<T, __nv_bfloat16>::value) {
+                f[2 * i] = __uint_as_float(w << 16);
+                f[2 * i + 1] = __uint_as_float(w & 0xFFFF0000u);
+            } else {
+                const float2 x = __half22float2(*reinterpret_cast<const __half2*>(&w));
+                f[2 * i] = x.x;
+                f[2 * i + 1] = x.y;
+            }
+        }
+    }
+}
+
+template <typename T>
+__device__ __forceinline__ void unpack_vec(const uint4& v, float* f) {
+    if constexpr (sizeof(T) == 4) {
+        unpack4(v, f);
+    } else {
+        unpack8(v, f, static_cast<const T*>(nullptr));
+    }
+}
+
+// One CTA = 4 warps over rows [r_begin, r_end) of one (b, head-set).
+// GATHER: rows are sel[r] of q head `head` (HPG must be 1).
+// !GATHER: rows are tokens r of kv head `head`, for HPG query heads.
+template <typename T, int D, int HPG, bool GATHER, int NST>
+__global__ void __launch_bounds__(kAttnWarps * 32) attn_kernel(
+    const T* __restrict__ q, const T* __restrict__ K, const T* __restrict__ V,
+    const int32_t* __restrict__ sel, int n, int tokens, int cap, int hkv, int hq, float scale_log2,
+    int rows_per_cta, float* __restrict__ part, int nsplit) {
+    using TR = AttnTraits<T, D>;
+    constexpr int CH = TR::CH, VEC = TR::VEC, EPV = TR::EPV, CPL = TR::CPL, RB = TR::RB;
+    constexpr int QSTRIDE = CH + 4;  // padded per-part q rows (bank spread)
+
+    extern __shared__ __align__(128) uint8_t smem[];
+    uint8_t* ring = smem;  // [warp][stage][K|V][8 rows]
+    float* qs = reinterpret_cast<float*>(ring + (size_t)kAttnWarps * NST * 2 * TR::STAGE_BYTES);
+    float* wres = qs + HPG * 4 * QSTRIDE;               // [warp][HPG][D+2]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(wres + kAttnWarps * HPG * (D + 2));
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int split = blockIdx.x, head = blockIdx.y, b = blockIdx.z;
+    const int kvh = GATHER ? head / (hq / hkv) : head;
+    const int64_t seq = (int64_t)b * hkv + kvh;
+    const T* Kseq = K + seq * cap * D;
+    const T* Vseq = V + seq * cap * D;
+    const int total = GATHER ? n : tokens;
+    const int r_begin = split * rows_per_cta;
+    const int r_end = min(r_begin + rows_per_cta, total);
+    const int rpw = (int)((((r_end - r_begin) + kAttnWarps - 1) / kAttnWarps + kRowsPerStage - 1) /
+                          kRowsPerStage * kRowsPerStage);
+    const int wr0 = min(r_begin + warp * rpw, r_end);
+    const int wr1 = min(wr0 + rpw, r_end);
+    const int nstages = (wr1 - wr0 + kRowsPerStage - 1) / kRowsPerStage;
+    const int32_t* selrow = GATHER ? sel + ((int64_t)b * hq + head) * n : nullptr;
+
+    // q heads -> shared memory, fp32, [hh][part][CH] padded
+    const int qh0 = GATHER ? head : head * HPG;
+    for (int i = threadIdx.x; i < HPG * D; i += blockDim.x) {
+        const int hh = i / D, c = i % D;
+        qs[hh * 4 * QSTRIDE + (c / CH) * QSTRIDE + (c % CH)] =
+            to_f32(q[((int64_t)b * hq + qh0 + hh) * D + c]);
+    }
+    uint64_t* wbar = bars + warp * NST;
+    if (lane == 0)
+        for (int s = 0; s < NST; ++s) mbar_init(&wbar[s], 1);
+    fence_barrier_init();
+    __syncthreads();
+
+    uint8_t* wring = ring + (size_t)warp * NST * 2 * TR::STAGE_BYTES;
+    const uint64_t pol = policy_evict_first();
+
+    auto issue = [&](int st) {  // fill ring slot st % NST with stage st
+        if (st >= nstages) return;
+        uint8_t* kdst = wring + (size_t)(st % NST) * 2 * TR::STAGE_BYTES;
+        uint8_t* vdst = kdst + TR::STAGE_BYTES;
+        const int r0 = wr0 + st * kRowsPerStage;
+        const int nr = min(kRowsPerStage, wr1 - r0);
+        if (lane == 0) mbar_arrive_expect_tx(&wbar[st % NST], (uint32_t)(2 * nr * RB));
+        __syncwarp();
+        if constexpr (GATHER) {
+            int tok = 0;
+            if (lane < nr) tok = selrow[r0 + lane];
+            const int tv = __shfl_sync(0xffffffffu, tok, lane & 7);
+            if (lane < nr)
+                bulk_g2s_evict_first(kdst + lane * RB, Kseq + (int64_t)tok * D, RB, &wbar[st % NST], pol);
+            else if (lane >= 8 && lane < 8 + nr)
+                bulk_g2s_evict_first(vdst + (lane - 8) * RB, Vseq + (int64_t)tv * D, RB,
+                                     &wbar[st % NST], pol);
+        } else {
+            if (lane == 0)
+                bulk_g2s_evict_first(kdst, Kseq + (int64_t)r0 * D, nr * RB, &wbar[st % NST], pol);
+            else if (lane == 1)
+                bulk_g2s_evict_first(vdst, Vseq + (int64_t)r0 * D, nr * RB, &wbar[st % NST], pol);
+        }
+    };
+
+    for (int s = 0; s < NST; ++s) issue(s);
+
+    const int row = lane >> 2, prt = lane & 3;
+    float m[HPG], l[HPG], acc[HPG][CPL];
+#pragma unroll
+    for (int hh = 0; hh < HPG; ++hh) {
+        m[hh] = -INFINITY;
+        l[hh] = 0.f;
+#pragma unroll
+        for (int i = 0; i < CPL; ++i) acc[hh][i] = 0.f;
+    }
+
+    for (int st = 0; st < nstages; ++st) {
+        mbar_wait(&wbar[st % NST], (uint32_t)((st / NST) & 1));
+        const uint8_t* kst = wring + (size_t)(st % NST) * 2 * TR::STAGE_BYTES;
+        const uint8_t* vst = kst + TR::STAGE_BYTES;
+        const int nr = min(kRowsPerStage, wr1 - (wr0 + st * kRowsPerStage));
+
+        // K vectors of this lane's (row, part): kept in registers across heads
+        float kf[CH];
+        if (row < nr) {
+            const uint4* kp = reinterpret_cast<const uint4*>(kst + row * RB + prt * CH * sizeof(T));
+#pragma unroll
+            for (int v = 0; v < VEC; ++v) unpack_vec<T>(kp[v], kf + v * EPV);
+        } else {
+#pragma unroll
+            for (int i = 0; i < CH; ++i) kf[i] = 0.f;
+        }
+        float p[HPG];
+#pragma unroll
+        for (int hh = 0; hh < HPG; ++hh) {
+            const float* qp = qs + hh * 4 * QSTRIDE + prt * QSTRIDE;
+            float dot0 = 0.f, dot1 = 0.f;
+#pragma unroll
+            for (int i = 0; i < CH; i += 4) {
+                const float4 qq = *reinterpret_cast<const float4*>(qp + i);
+                dot0 = fmaf(qq.x, kf[i], dot0);
+                dot1 = fmaf(qq.y, kf[i + 1], dot1);
+                dot0 = fmaf(qq.z, kf[i + 2], dot0);
+                dot1 = fmaf(qq.w, kf[i + 3], dot1);
+            }
+            float dot = dot0 + dot1;
+            dot += __shfl_xor_sync(0xffffffffu, dot, 1);
+            dot += __shfl_xor_sync(0xffffffffu, dot, 2);
+            const float logit = row < nr ? dot * scale_log2 : -INFINITY;
+            float mst = fmaxf(logit, __shfl_xor_sync(0xffffffffu, logit, 4));
+            mst = fmaxf(mst, __shfl_xor_sync(0xffffffffu, mst, 8));
+            mst = fmaxf(mst, __shfl_xor_sync(0xffffffffu, mst, 16));
+            const float mnew = fmaxf(m[hh], mst);
+            const float alpha = exp2f(m[hh] - mnew);
+            p[hh] = exp2f(logit - mnew);
+            float ps = prt == 0 ? p[hh] : 0.f;
+            ps = warp_sum(ps);
+            l[hh] = l[hh] * alpha + ps;
+            m[hh] = mnew;
+#pragma unroll
+            for (int i = 0; i < CPL; ++i) acc[hh][i] *= alpha;
+        }
+        for (int r = 0; r < nr; ++r) {
+            float vf[CPL];
+            load_v<T, CPL>(reinterpret_cast<const T*>(vst + r * RB), lane, vf);
+#pragma unroll
+            for (int hh = 0; hh < HPG; ++hh) {
+                const float pr = __shfl_sync(0xffffffffu, p[hh], r * 4);
+#pragma unroll
+                for (int i = 0; i < CPL; ++i) acc[hh][i] = fmaf(pr, vf[i], acc[hh][i]);
+            }
+        }
+        __syncwarp();
+        fence_proxy_async();
+        issue(st + NST);
+    }
+
+    // warp states -> smem -> CTA partial
+    float* wr = wres + warp * HPG * (D + 2);
+#pragma unroll
+    for (int hh = 0; hh < HPG; ++hh) {
+#pragma unroll
+        for (int i = 0; i < CPL; ++i) wr[hh * (D + 2) + lane * CPL + i] = acc[hh][i];
+        if (lane == 0) {
+            wr[hh * (D + 2) + D] = m[hh];
+            wr[hh * (D + 2) + D + 1] = l[hh];
+        }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < HPG * D; i += blockDim.x) {
+        const int hh = i / D, c = i % D;
+        float M = -INFINITY;
+#pragma unroll
+        for (int w = 0; w < kAttnWarps; ++w) M = fmaxf(M, wres[(w * HPG + hh) * (D + 2) + D]);
+        float o = 0.f, L = 0.f;
+#pragma unroll
+        for (int w = 0; w < kAttnWarps; ++w) {
+            const float* x = wres + (w * HPG + hh) * (D + 2);
+            const float mw = x[D];
+            const float sc = mw == -INFINITY ? 0.f : exp2f(mw - M);
+            o = fmaf(x[c], sc, o);
+            L = fmaf(x[D + 1], sc, L);
+        }
+        float* dst = part + (((int64_t)b * hq + qh0 + hh) * nsplit + split) * (D + 2);
+        dst[c] = o;
+        if (c == 0) {
+            dst[D] = M;
+            dst[D + 1] = L;
+        }
+    }
+}
+
+// LSE merge of nsplit partials per (b, q head): out = sum_s o_s 2^(m_s-M) / sum_s l_s 2^(m_s-M).
+__global__ void merge_kernel(const float* __restrict__ part, int nsplit, int d, int hq,
+                             float* __restrict__ out) {
+    const int h = blockIdx.x, b = blockIdx.y;
+    const float* p = part + ((int64_t)b * hq + h) * nsplit * (d + 2);
+    float M = -INFINITY;
+    for (int s = 0; s < nsplit; ++s) M = fmaxf(M, p[s * (d + 2) + d]);
+    float L = 0.f;
+    for (int s = 0; s < nsplit; ++s) {
+        const float ms = p[s * (d + 2) + d];
+        if (ms != -INFINITY) L += p[s * (d + 2) + d + 1] * exp2f(ms - M);
+    }
+    const float inv = 1.f / L;
+    for (int c = threadIdx.x; c < d; c += blockDim.x) {
+        float o = 0.f;
+        for (int s = 0; s < nsplit; ++s) {
+            const float ms = p[s * (d + 2) + d];
+            if (ms != -INFINITY) o = fmaf(p[s * (d + 2) + c], exp2f(ms - M), o);
+        }
+        out[((int64_t)b * hq + h) * d + c] = o * inv;
+    }
+}
+
+// Generic fallback (any d <= 1024, any row width): one warp per (b, q head,
+// split), lanes over channels, same online softmax.
+template <typename T, bool GATHER>
+__global__ void attn_generic_kernel(const T* __restrict__ q, const T* __restrict__ K,
+                                    const T* __restrict__ V, const int32_t* __restrict__ sel, int n,
+                                    int tokens, int cap, int d, int hkv, int hq, float scale_log2,
+                                    int rows_per_cta, float* __restrict__ part, int nsplit) {
+    const int lane = threadIdx.x;
+    const int split = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
+    const int kvh = h / (hq / hkv);
+    const int64_t seq = (int64_t)b * hkv + kvh;
+    const T* qp = q + ((int64_t)b * hq + h) * d;
+    const int total = GATHER ? n : tokens;
+    const int r0 = split * rows_per_cta, r1 = min(r0 + rows_per_cta, total);
+    constexpr int MAXC = 32;  // d <= 1024
+    float acc[MAXC];
+    for (int i = 0; i < MAXC; ++i) acc[i] = 0.f;
+    float m = -INFINITY, l = 0.f;
+    for (int r = r0; r < r1; ++r) {
+        const int tok = GATHER ? sel[((int64_t)b * hq + h) * n + r] : r;
+        const T* kr = K + (seq * cap + tok) * d;
+        const T* vr = V + (seq * cap + tok) * d;
+        float dot = 0.f;
+        for (int c = lane; c < d; c += 32) dot = fmaf(to_f32(qp[c]), to_f32(kr[c]), dot);
+        const float logit = warp_sum(dot) * scale_log2;
+        const float mnew = fmaxf(m, logit);
+        const float alpha = exp2f(m - mnew), p = exp2f(logit - mnew);
+        l = l * alpha + p;
+        m = mnew;
+        for (int i = 0, c = lane; c < d; ++i, c += 32) acc[i] = acc[i] * alpha + p * to_f32(vr[c]);
+    }
+    float* dst = part + (((int64_t)b * hq + h) * nsplit + split) * (d + 2);
+    for (int i = 0, c = lane; c < d; ++i, c += 32) dst[c] = acc[i];
+    if (lane == 0) {
+        dst[d] = m;
+        dst[d + 1] = l;
+    }
+}
+
+// ---- host-side planning --------------------------------------------------------
+
+struct AttnPlan {
+    int nsplit;
+    int rows_per_cta;
+};
+
+static AttnPlan plan_split(int64_t units, int total_rows, int min_rows) {
+    // ~3 resident CTAs per SM, one wave
+    const int64_t target = 148 * 3;
+    int64_t ns = (target + units - 1) / units;
+    if (ns < 1) ns = 1;
+    int rpc = (int)ceil_div(total_rows, ns);
+    rpc = (int)ceil_div(rpc, 32) * 32;
+    if (rpc < min_rows) rpc = min_rows;
+    AttnPlan p;
+    p.rows_per_cta = rpc;
+    p.nsplit = (int)ceil_div(total_rows, rpc);
+    if (p.nsplit < 1) p.nsplit = 1;
+    return p;
+}
+
+template <typename T, int D>
+constexpr int attn_nst() {
+    return sizeof(T) == 4 ? 2 : 4;
+}
+
+template <typename T, int D, int HPG, bool GATHER>
+static size_t attn_smem() {
+    using TR = AttnTraits<T, D>;
+    constexpr int NST = attn_nst<T, D>();
+    return (size_t)kAttnWarps * NST * 2 * TR::STAGE_BYTES + (size_t)HPG * 4 * (TR::CH + 4) * 4 +
+           (size_t)kAttnWarps * HPG * (D + 2) * 4 + (size_t)kAttnWarps * NST * 8;
+}
+
+template <typename T, int D, int HPG, bool GATHER>
+static int launch_attn(const fier_shape* s, const void* q, const void* K, const void* V,
+                       const int32_t* sel, int n, int tokens, float scale, float* part,
+                       const AttnPlan& p, cudaStream_t st) {
+    constexpr int NST = attn_nst<T, D>();
+    auto kern = attn_kernel<T, D, HPG, GATHER, NST>;
+    const size_t smem = attn_smem<T, D, HPG, GATHER>();
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return fail(FIER_ECUDA, std::string("attention: ") + cudaGetErrorString(e));
+    dim3 grid(p.nsplit, GATHER ? s->q_heads : s->kv_heads, s->batch);
+    kern<<<grid, kAttnWarps * 32, smem, st>>>(
+        static_cast<const T*>(q), static_cast<const T*>(K), static_cast<const T*>(V), sel, n, tokens,
+        s->capacity, s->kv_heads, s->q_heads, scale * kLog2e, p.rows_per_cta, part, p.nsplit);
+    return check_launch("attention");
+}
+
+template <typename T, bool GATHER>
+static int launch_generic(const fier_shape* s, const void* q, const void* K, const void* V,
+                          const int32_t* sel, int n, int tokens, float scale, float* part,
+                          const AttnPlan& p, cudaStream_t st) {
+    dim3 grid(p.nsplit, s->q_heads, s->batch);
+    attn_generic_kernel<T, GATHER><<<grid, 32, 0, st>>>(
+        static_cast<const T*>(q), static_cast<const T*>(K), static_cast<const T*>(V), sel, n, tokens,
+        s->capacity, s->dim, s->kv_heads, s->q_heads, scale * kLog2e, p.rows_per_cta, part,
+        p.nsplit);
+    return check_launch("attention");
+}
+
+static bool fast_dim(const fier_shape* s) {
+    return s->dim == 128 || s->dim == 64;
+}
+
+AttnPlan sparse_plan(const fier_shape* s, int n) {
+    if (!fast_dim(s)) return plan_split((int64_t)s->batch * s->q_heads, n, 64);
+    return plan_split((int64_t)s->batch * s->q_heads, n, 64);
+}
+
+AttnPlan full_plan(const fier_shape* s, int tokens) {
+    const bool fast = fast_dim(s);
+    const int64_t units = fast ? (int64_t)s->batch * s->kv_heads : (int64_t)s->batch * s->q_heads;
+    return plan_split(units, tokens, 256);
+}
+
+size_t sparse_workspace(const fier_shape* s, int n) {
+    const AttnPlan p = sparse_plan(s, n);
+    return (size_t)s->batch * s->q_heads * p.nsplit * (s->dim + 2) * sizeof(float);
+}
+
+size_t full_workspace(const fier_shape* s, int tokens) {
+    const AttnPlan p = full_plan(s, tokens);
+    return (size_t)s->batch * s->q_heads * p.nsplit * (s->dim + 2) * sizeof(float);
+}
+
+template <typename T>
+static int sparse_typed(const fier_shape* s, const void* q, const void* K, const void* V,
+                        const int32_t* sel, int n, int tokens, float scale, float* part,
+                        const AttnPlan& p, cudaStream_t st) {
+    if (s->dim == 128) return launch_attn<T, 128, 1, true>(s, q, K, V, sel, n, tokens, scale, part, p, st);
+    if (s->dim == 64) return launch_attn<T, 64, 1, true>(s, q, K, V, sel, n, tokens, scale, part, p, st);
+    return launch_generic<T, true>(s, q, K, V, sel, n, tokens, scale, part, p, st);
+}
+
+template <typename T, int D>
+static int full_fast(const fier_shape* s, const void* q, const void* K, const void* V, int tokens,
+                     float scale, float* part, const AttnPlan& p, cudaStream_t st) {
+    switch (s->q_heads / s->kv_heads) {
+        case 1: return launch_attn<T, D, 1, false>(s, q, K, V, nullptr, 0, tokens, scale, part, p, st);
+        case 2: return launch_attn<T, D, 2, false>(s, q, K, V, nullptr, 0, tokens, scale, part, p, st);
+        case 4: return launch_attn<T, D, 4, false>(s, q, K, V, nullptr, 0, tokens, scale, part, p, st);
+        case 8: return launch_attn<T, D, 8, false>(s, q, K, V, nullptr, 0, tokens, scale, part, p, st);
+    }
+    return -1;
+}
+
+template <typename T>
+static int full_typed(const fier_shape* s, const void* q, const void* K, const void* V, int tokens,
+                      float scale, float* part, const AttnPlan& p, cudaStream_t st) {
+    const int hpg = s->q_heads / s->kv_heads;
+    const bool hpg_ok = hpg == 1 || hpg == 2 || hpg == 4 || hpg == 8;
+    if (hpg_ok && s->dim == 128) return full_fast<T, 128>(s, q, K, V, tokens, scale, part, p, st);
+    if (hpg_ok && s->dim == 64) return full_fast<T, 64>(s, q, K, V, tokens, scale, part, p, st);
+    return launch_generic<T, false>(s, q, K, V, nullptr, 0, tokens, scale, part, p, st);
+}
+
+static int merge(const fier_shape* s, const float* part, int nsplit, float* out, cudaStream_t st) {
+    dim3 grid(s->q_heads, s->batch);
+    merge_kernel<<<grid, 128, 0, st>>>(part, nsplit, s->dim, s->q_heads, out);
+    return check_launch("attention merge");
+}
+
+int sparse_dispatch(const fier_shape* s, const void* q, const void* K, const void* V,
+                    const int32_t* sel, int n, int tokens, float scale, float* out, float* part,
+                    cudaStream_t st) {
+    const AttnPlan p = sparse_plan(s, n);
+    int rc = FIER_OK;
+    switch (s->dtype) {
+        case FIER_F32: rc = sparse_typed<float>(s, q, K, V, sel, n, tokens, scale, part, p, st); break;
+        case FIER_F16: rc = sparse_typed<__half>(s, q, K, V, sel, n, tokens, scale, part, p, st); break;
+        case FIER_BF16: rc = sparse_typed<__nv_bfloat16>(s, q, K, V, sel, n, tokens, scale, part, p, st); break;
+        default: return fail(FIER_EINVAL, "fier_sparse_attention: unknown dtype");
+    }
+    if (rc) return rc;
+    return merge(s, part, p.nsplit, out, st);
+}
+
+int full_dispatch(const fier_shape* s, const void* q, const void* K, const void* V, int tokens,
+                  float scale, float* out, float* part, cudaStream_t st) {
+    const AttnPlan p = full_plan(s, tokens);
+    int rc = FIER_OK;
+    switch (s->dtype) {
+        case FIER_F32: rc = full_typed<float>(s, q, K, V, tokens, scale, part, p, st); break;
+        case FIER_F16: rc = full_typed<__half>(s, q, K, V, tokens, scale, part, p, st); break;
+        case FIER_BF16: rc = full_typed<__nv_bfloat16>(s, q, K, V, tokens, scale, part, p, st); break;
+        default: return fail(FIER_EINVAL, "fier_full_attention: unknown dtype");
+    }
+    if (rc) return rc;
+    return merge(s, part, p.nsplit, out, st);
+}
+
+}  // namespace fier_cuda

@@ -1,0 +1,138 @@
+"""The C-ABI library on CPU: it loads, exports every symbol include/fier_cuda.h
+declares, and its host-only logic (FIER format conversion, argument validation
+with the reference's error texts) behaves like the reference.  No kernel is
+launched here."""
+import ctypes as C
+import os
+import re
+
+import numpy as np
+import pytest
+
+from conftest import ROOT, golden_cases, load_golden
+
+HEADER = os.path.join(ROOT, "include", "fier_cuda.h")
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_2508_08256_b200 import _lib
+    return _lib.load()
+
+
+def header_functions():
+    text = open(HEADER).read()
+    return sorted(set(re.findall(r"^\s*FIER_API\s+(?:const\s+)?\w+\*?\s+\**(fier_\w+)\(", text, re.M)))
+
+
+def test_exports_every_declared_symbol(lib):
+    from paper_2508_08256_b200 import _lib
+    names = header_functions()
+    assert len(names) >= 19
+    assert set(names) == set(_lib.EXPORTS)
+    for name in names:
+        assert hasattr(lib, name), name
+
+
+def test_library_is_sm100a(lib):
+    from paper_2508_08256_b200 import _lib
+    blob = open(_lib.LIB_PATH, "rb").read()
+    assert b"sm_100a" in blob
+
+
+def test_payload_bytes_match_reference_accounting(lib):
+    # PackedKeys::payload_bytes (quant1bit.hpp:60-62), acceptance_main.cpp:66-109
+    assert lib.fier_payload_bytes(4096, 128, 32) == 4096 * 128 // 8 + (4096 * 128 // 32) * 4
+    assert lib.fier_payload_bytes(100, 11, 32) == 100 * 2 + 11 * 4 * 4
+    assert lib.fier_payload_bytes(0, 11, 32) == 0
+
+
+@pytest.mark.parametrize("name", golden_cases())
+def test_fier_format_round_trip(lib, name):
+    """Host conversion device-layout <-> FIER bytes is exact on reference fixtures."""
+    c = load_golden(name)
+    for buf in c["fier_list"]:
+        b = np.frombuffer(buf, np.uint8)
+        l, d, g = C.c_int32(), C.c_int32(), C.c_int32()
+        assert lib.fier_fier_to_index(b.ctypes.data, b.size, C.byref(l), C.byref(d), C.byref(g),
+                                      None, 0, None, 0) == 0
+        assert (l.value, d.value, g.value) == (c["l"], c["d"], c["g"])
+        W = (c["d"] + 31) // 32
+        G = (c["l"] + c["g"] - 1) // c["g"]
+        bits = np.zeros(c["l"] * W, np.uint32)
+        par = np.zeros(G * c["d"] * 2, np.uint16)
+        assert lib.fier_fier_to_index(b.ctypes.data, b.size, C.byref(l), C.byref(d), C.byref(g),
+                                      bits.ctypes.data, bits.size, par.ctypes.data, par.size) == 0
+        out = np.zeros(len(buf), np.uint8)
+        assert lib.fier_index_to_fier(bits.ctypes.data, par.ctypes.data, l, d, g, out.ctypes.data,
+                                      out.size) == 0
+        assert out.tobytes() == buf
+
+
+def test_fier_parse_diagnostics(lib):
+    """Rejections name the violated field like parse_packed_keys (test_io.cpp:169-190)."""
+    from paper_2508_08256_b200 import _lib
+    c = load_golden("short_group_d24")
+    good = c["fier_list"][0]
+
+    def parse(buf):
+        b = np.frombuffer(buf, np.uint8)
+        l, d, g = C.c_int32(), C.c_int32(), C.c_int32()
+        rc = lib.fier_fier_to_index(b.ctypes.data, b.size, C.byref(l), C.byref(d), C.byref(g),
+                                    None, 0, None, 0)
+        return rc, _lib.last_error()
+
+    bad = bytearray(good)
+    bad[1] = ord("?")
+    assert parse(bytes(bad)) == (2, "bad magic: expected FIER")
+    assert parse(good[:-1])[0] == 2 and "payload length mismatch" in parse(good[:-1])[1]
+    bad = bytearray(good)
+    bad[14:18] = b"\0\0\0\0"
+    assert parse(bytes(bad)) == (2, "invalid g: must be >= 1")
+    bad = bytearray(good)
+    bad[4] = 9
+    assert parse(bytes(bad)) == (2, "unsupported version: 9")
+
+
+def test_validation_uses_reference_messages(lib):
+    """Precondition failures return FIER_EINVAL before any launch (no GPU needed)."""
+    from paper_2508_08256_b200 import _lib
+    from paper_2508_08256_b200.api import make_shape
+    s = make_shape(1, 2, 2, 64, 128, 32, _lib.FIER_BF16)
+    dummy = C.c_void_p(16)
+    assert lib.fier_topk(dummy, 1, 10, 10, 0, dummy, None, 0, None) == 1
+    assert _lib.last_error() == "topk_oracle: k out of range"
+    assert lib.fier_topk(dummy, 1, 10, 10, 11, dummy, None, 0, None) == 1
+    assert lib.fier_sparse_attention(C.byref(s), dummy, dummy, dummy, dummy, 0, 10, 1.0, dummy,
+                                     dummy, 1 << 20, None) == 1
+    assert _lib.last_error() == "gather_attention: empty selection"
+    assert lib.fier_sparse_attention(C.byref(s), dummy, dummy, dummy, dummy, 11, 10, 1.0, dummy,
+                                     dummy, 1 << 20, None) == 1
+    assert _lib.last_error() == "gather_attention: selection invalid for cache"
+    assert lib.fier_decode_step(C.byref(s), dummy, dummy, dummy, 9, dummy, dummy, dummy, dummy, 11,
+                                1.0, dummy, dummy, None, dummy, 1 << 30, None) == 1
+    assert _lib.last_error() == "fier_select: budget out of range"
+    bad_g = make_shape(1, 2, 2, 64, 128, 0, _lib.FIER_BF16)
+    assert lib.fier_pack_keys(C.byref(bad_g), dummy, 10, dummy, dummy, None, None) == 1
+    assert _lib.last_error() == "quantize: group size must be >= 1"
+    assert lib.fier_pack_keys(C.byref(s), dummy, 0, dummy, dummy, None, None) == 1
+    assert _lib.last_error() == "quantize: empty key cache"
+    gqa_bad = make_shape(1, 3, 2, 64, 128, 32, _lib.FIER_BF16)
+    assert lib.fier_score(C.byref(gqa_bad), dummy, dummy, dummy, 10, dummy, 10, None) == 1
+
+
+def test_python_api_raises_value_error_like_reference():
+    from paper_2508_08256_b200 import _lib
+    with pytest.raises(ValueError, match="topk_oracle: k out of range"):
+        _lib.check(_lib.load().fier_topk(C.c_void_p(16), 1, 4, 4, 5, C.c_void_p(16), None, 0, None))
+
+
+def test_workspace_sizes_are_consistent(lib):
+    from paper_2508_08256_b200 import _lib
+    from paper_2508_08256_b200.api import make_shape
+    s = make_shape(1, 32, 32, 32768, 128, 32, _lib.FIER_BF16)
+    assert lib.fier_bits_bytes(C.byref(s)) == 32 * 32768 * 16
+    assert lib.fier_params_bytes(C.byref(s)) == 32 * 1024 * 128 * 4
+    ws = lib.fier_decode_workspace(C.byref(s), 32768, 3604)
+    assert ws >= 32 * 32768 * 4
+    assert lib.fier_step_scores_ld(33) == 64

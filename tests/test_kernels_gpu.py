@@ -1,0 +1,280 @@
+"""GPU parity of the four kernels against the oracle and the reference's golden vectors.
+
+Bars (BASELINE.json north_star):
+  packed bits + (s, z)          bit-exact (FIER bytes compared byte for byte)
+  scores                        |gpu - ref| <= 1e-3 * max(1, |ref|)  (test_quant1bit.cpp:149 denominator)
+  selection                     bit-exact vs topk_oracle on the GPU's own scores; recall >= 0.999
+                                vs the reference's selection, mismatches only at score-tolerance ties
+  attention output              relative L2 < 1e-2 vs gather_attention on the same selection
+"""
+import numpy as np
+import pytest
+import torch
+
+from conftest import golden_cases, load_golden
+
+pytestmark = pytest.mark.gpu
+
+TDT = {"f32": torch.float32, "f16": torch.float16, "bf16": torch.bfloat16}
+SCORE_TOL = 1e-3
+OUT_TOL = 1e-2
+
+
+def fier():
+    import paper_2508_08256_b200 as F
+    return F
+
+
+def case_tensors(c, dev):
+    dt = TDT[c["dtype"]]
+    K = torch.from_numpy(c["K"]).to(dev, dt).unsqueeze(0)  # [1, Hkv, l, d]
+    V = torch.from_numpy(c["V"]).to(dev, dt).unsqueeze(0)
+    Q = torch.from_numpy(c["Q"]).to(dev, dt).unsqueeze(0)  # [1, Hq, d]
+    return K, V, Q
+
+
+def score_err(gpu, ref):
+    return np.max(np.abs(gpu - ref) / np.maximum(1.0, np.abs(ref)))
+
+
+@pytest.mark.parametrize("name", golden_cases())
+def test_pack_bit_exact(cuda, name):
+    c = load_golden(name)
+    K, V, Q = case_tensors(c, cuda)
+    pk = fier().quantize(K, c["g"])
+    for h in range(c["hkv"]):
+        assert pk.to_fier(0, h) == c["fier_list"][h], f"kv head {h}"
+
+
+@pytest.mark.parametrize("name", golden_cases())
+def test_scores_within_tolerance(cuda, name):
+    c = load_golden(name)
+    K, V, Q = case_tensors(c, cuda)
+    pk = fier().quantize(K, c["g"])
+    s = fier().approx_scores(Q, pk)[0].cpu().numpy().astype(np.float64)
+    assert score_err(s, c["scores"]) <= SCORE_TOL
+
+
+@pytest.mark.parametrize("name", golden_cases())
+def test_selection_and_output(cuda, port, name):
+    c = load_golden(name)
+    K, V, Q = case_tensors(c, cuda)
+    F = fier()
+    pk = F.quantize(K, c["g"])
+    est = F.approx_scores(Q, pk)
+    sel = F.topk_oracle(est, c["n"])
+    out = F.gather_attention(Q, K, V, sel)
+    est_np, sel_np, out_np = est[0].cpu().numpy(), sel[0].cpu().numpy(), out[0].cpu().numpy()
+    group = c["hq"] // c["hkv"]
+    for h in range(c["hq"]):
+        kv = h // group
+        # K3 is exact on the scores it was given
+        np.testing.assert_array_equal(sel_np[h], port.topk(est_np[h].astype(np.float64), c["n"]))
+        # against the reference's selection on its fp64 scores
+        want = c["sel"][h]
+        rec = port.recall(sel_np[h], want)
+        assert rec >= 0.999 or _only_tolerance_ties(sel_np[h], want, c["scores"][h]), (h, rec)
+        q = c["Q"][h].astype(np.float64)
+        ref_out = port.gather_attention(q, c["K"][kv], c["V"][kv], sel_np[h].astype(np.int64))
+        assert port.relative_l2_error(out_np[h], ref_out) < OUT_TOL
+        if np.array_equal(sel_np[h], want):
+            assert port.relative_l2_error(out_np[h], c["out"][h]) < OUT_TOL
+
+
+def _only_tolerance_ties(got, want, ref_scores):
+    """Every index in the symmetric difference scores within tolerance of the threshold."""
+    diff = np.setxor1d(got, want)
+    thr = np.sort(ref_scores)[::-1][len(want) - 1]
+    return all(abs(ref_scores[i] - thr) <= 2 * SCORE_TOL * max(1.0, abs(thr)) for i in diff)
+
+
+@pytest.mark.parametrize("name", golden_cases())
+def test_full_attention_matches_reference(cuda, name):
+    c = load_golden(name)
+    K, V, Q = case_tensors(c, cuda)
+    out = fier().full_attention(Q, K, V)[0].cpu().numpy()
+    group = c["hq"] // c["hkv"]
+    for h in range(c["hq"]):
+        num = np.linalg.norm(out[h] - c["full"][h])
+        assert num / np.linalg.norm(c["full"][h]) < OUT_TOL
+
+
+@pytest.mark.parametrize("name", ["mha_d128", "gqa_d64", "planted_spikes", "score_ties"])
+def test_fier_attend_composition(cuda, name):
+    """fier_attend == topk_oracle(approx_scores) -> gather_attention (test_retrieval.cpp:108-120)."""
+    c = load_golden(name)
+    K, V, Q = case_tensors(c, cuda)
+    F = fier()
+    pk = F.quantize(K, c["g"])
+    r = F.fier_attend(Q, K, V, pk, c["n"])
+    sel = F.fier_select(Q, pk, c["n"])
+    assert torch.equal(r.selection, sel)
+    assert torch.equal(r.output, F.gather_attention(Q, K, V, sel))
+    assert r.bytes_loaded_for_estimation == int(c["bytes_loaded"][0])
+    with pytest.raises(ValueError, match="fier_select: budget out of range"):
+        F.fier_select(Q, pk, c["l"] + 1)
+
+
+def test_planted_spikes_selected(cuda):
+    """Planted keys (workload.hpp:169-191) own the top logits and are always selected."""
+    c = load_golden("planted_spikes")
+    K, V, Q = case_tensors(c, cuda)
+    F = fier()
+    sel = F.fier_select(Q, F.quantize(K, c["g"]), c["n"])[0].cpu().numpy()
+    np.testing.assert_array_equal(sel, c["sel"])
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "f16", "f32"])
+@pytest.mark.parametrize("g", [32, 8, 128])
+def test_append_equals_one_shot(cuda, port, dtype, g):
+    """Incremental decode-time packing == quantize(K[0:l]) bit for bit, across group boundaries."""
+    F = fier()
+    torch.manual_seed(7)
+    B, H, cap, d = 2, 3, 200, 128
+    dt = TDT[dtype]
+    Kfull = (torch.randn(B, H, cap, d, device=cuda) * 3).to(dt)
+    Vfull = torch.randn(B, H, cap, d, device=cuda).to(dt)
+    t0 = 37
+    K = torch.zeros_like(Kfull)
+    V = torch.zeros_like(Vfull)
+    K[:, :, :t0] = Kfull[:, :, :t0]
+    V[:, :, :t0] = Vfull[:, :, :t0]
+    pk = F.quantize(K, g, tokens=t0)
+    for pos in range(t0, 141):
+        F.append_token(K, V, Kfull[:, :, pos].contiguous(), Vfull[:, :, pos].contiguous(), pos, pk,
+                       check_finite=(pos % 50 == 0))
+        if pos in (t0, 63, 64, 95, 127, 128, 140):
+            for b in range(B):
+                for h in range(H):
+                    want = port.quantize_fier(Kfull[b, h, :pos + 1].double().cpu().numpy(), g)
+                    assert pk.to_fier(b, h) == want, (pos, b, h)
+    assert torch.equal(V[:, :, :141], Vfull[:, :, :141])
+
+
+def test_nonfinite_keys_rejected(cuda):
+    F = fier()
+    K = torch.randn(40, 16, device=cuda)
+    K[17, 3] = float("inf")
+    with pytest.raises(ValueError, match="quantize: non-finite key entry"):
+        F.quantize(K, 32)
+
+
+def test_gather_attention_rejects_like_reference(cuda):
+    F = fier()
+    K = torch.randn(10, 128, device=cuda, dtype=torch.bfloat16)
+    q = torch.randn(128, device=cuda, dtype=torch.bfloat16)
+    with pytest.raises(ValueError, match="selection invalid for cache"):
+        F.gather_attention(q, K, K, torch.tensor([3, 2], device=cuda))
+    with pytest.raises(ValueError, match="selection invalid for cache"):
+        F.gather_attention(q, K, K, torch.tensor([3, 10], device=cuda))
+    with pytest.raises(ValueError, match="topk_oracle: k out of range"):
+        F.topk_oracle(torch.randn(5, device=cuda), 6)
+
+
+def test_single_token_returns_value_row(cuda):
+    """test_kvcore.cpp:156-166 / test_retrieval.cpp:100-106."""
+    F = fier()
+    K = torch.randn(8, 128, device=cuda)
+    V = torch.randn(8, 128, device=cuda)
+    q = torch.randn(128, device=cuda)
+    out = F.gather_attention(q, K, V, torch.tensor([5], device=cuda, dtype=torch.int32))
+    torch.testing.assert_close(out, V[5], rtol=0, atol=0)
+
+
+@pytest.mark.parametrize("l,k", [(1, 1), (31, 7), (33, 33), (1000, 1), (4097, 4096), (70000, 7700),
+                                 (300000, 33000)])
+def test_topk_exact_sizes(cuda, port, l, k):
+    F = fier()
+    g = torch.Generator(device="cpu").manual_seed(l)
+    s = torch.randn(3, l, generator=g)
+    s[1] = torch.round(s[1] * 4) / 4  # heavy ties
+    s[2, : l // 2] = 0.0
+    s[2, l // 2:] = -0.0  # signed zeros tie (core.hpp:139-142)
+    sel = F.topk_oracle(s.to(cuda), k).cpu().numpy()
+    for r in range(3):
+        np.testing.assert_array_equal(sel[r], port.topk(s[r].double().numpy(), k))
+
+
+def test_topk_extremes(cuda, port):
+    F = fier()
+    s = torch.tensor([0.0, float("inf"), -float("inf"), 1e38, -1e38, 3.0, 3.0, -0.0, 1e-45, -1e-45])
+    for k in range(1, s.numel() + 1):
+        got = F.topk_oracle(s.to(cuda), k).cpu().numpy()
+        np.testing.assert_array_equal(got, port.topk(s.double().numpy(), k))
+
+
+@pytest.mark.parametrize("B,Hq,Hkv,d,dtype", [(2, 4, 2, 128, "bf16"), (1, 8, 8, 64, "f16"),
+                                              (3, 2, 1, 24, "f32"), (1, 32, 8, 128, "bf16")])
+def test_decode_step_matches_oracle(cuda, port, B, Hq, Hkv, d, dtype):
+    F = fier()
+    torch.manual_seed(11)
+    dt, cap, g = TDT[dtype], 700, 32
+    layer = F.DecodeLayer(B, Hq, Hkv, cap, d, g, dtype=dt, device=cuda)
+    layer.K.copy_(torch.randn(B, Hkv, cap, d, device=cuda).to(dt))
+    layer.V.copy_(torch.randn(B, Hkv, cap, d, device=cuda).to(dt))
+    pos = 613
+    layer.prefill(pos)
+    q = torch.randn(B, Hq, d, device=cuda).to(dt)
+    kn = torch.randn(B, Hkv, d, device=cuda).to(dt)
+    vn = torch.randn(B, Hkv, d, device=cuda).to(dt)
+    n = 77
+    ld = pos + 1 + (-(pos + 1)) % 32
+    scores = torch.empty(B, Hq, ld, device=cuda)
+    out, sel = layer.step(q, kn, vn, pos, n, scores_out=scores)
+    torch.cuda.synchronize()
+    Kc, Vc = layer.K.double().cpu().numpy(), layer.V.double().cpu().numpy()
+    assert np.array_equal(Kc[:, :, pos], kn.double().cpu().numpy())
+    sel_np, out_np, sc = sel.cpu().numpy(), out.cpu().numpy(), scores.cpu().numpy()
+    group = Hq // Hkv
+    for b in range(B):
+        for h in range(Hq):
+            kv = h // group
+            buf = port.quantize_fier(Kc[b, kv, :pos + 1], g)
+            assert layer.pk.to_fier(b, kv) == buf
+            qd = q[b, h].double().cpu().numpy()
+            ref_scores = port.approx_scores_fier(qd, buf)
+            assert score_err(sc[b, h, :pos + 1], ref_scores) <= SCORE_TOL
+            np.testing.assert_array_equal(sel_np[b, h], port.topk(sc[b, h, :pos + 1].astype(np.float64), n))
+            assert port.recall(sel_np[b, h], port.topk(ref_scores, n)) >= 0.97
+            ref_out = port.gather_attention(qd, Kc[b, kv, :pos + 1], Vc[b, kv, :pos + 1],
+                                            sel_np[b, h].astype(np.int64))
+            assert port.relative_l2_error(out_np[b, h], ref_out) < OUT_TOL
+    # K0 on the same cache
+    full = layer.full_step(q, pos + 1).cpu().numpy()
+    for b in range(B):
+        for h in range(0, Hq, max(1, Hq // 4)):
+            kv = h // group
+            qd = q[b, h].double().cpu().numpy()
+            ref = port.gather_attention(qd, Kc[b, kv, :pos + 1], Vc[b, kv, :pos + 1], np.arange(pos + 1))
+            assert port.relative_l2_error(full[b, h], ref) < OUT_TOL
+
+
+def test_c2_shape_step_properties(cuda, port):
+    """Full C2 shape (32 MHA heads, d=128, l=32768, n=3604, bf16): exact selection on the
+    GPU scores, score tolerance and output tolerance on sampled heads, FIER round trip."""
+    F = fier()
+    torch.manual_seed(3)
+    B, H, L, d, n = 1, 32, 32768, 128, 3604
+    layer = F.DecodeLayer(B, H, H, L, d, 32, dtype=torch.bfloat16, device=cuda)
+    layer.K.copy_(torch.randn(B, H, L, d, device=cuda).to(torch.bfloat16))
+    layer.V.copy_(torch.randn(B, H, L, d, device=cuda).to(torch.bfloat16))
+    layer.prefill(L - 1)
+    q = torch.randn(B, H, d, device=cuda).to(torch.bfloat16)
+    kn = torch.randn(B, H, d, device=cuda).to(torch.bfloat16)
+    scores = torch.empty(B, H, L, device=cuda)
+    out, sel = layer.step(q, kn, kn, L - 1, n, scores_out=scores)
+    sel_np = sel[0].cpu().numpy()
+    assert (np.diff(sel_np, axis=1) > 0).all() and sel_np.min() >= 0 and sel_np.max() < L
+    sc = scores[0].cpu().numpy().astype(np.float64)
+    for h in (0, 13, 31):
+        np.testing.assert_array_equal(sel_np[h], port.topk(sc[h], n))
+        Kh = layer.K[0, h].double().cpu().numpy()
+        Vh = layer.V[0, h].double().cpu().numpy()
+        buf = layer.pk.to_fier(0, h)
+        assert buf == port.quantize_fier(Kh, 32)
+        qd = q[0, h].double().cpu().numpy()
+        ref_scores = port.approx_scores_fier(qd, buf)
+        assert score_err(sc[h], ref_scores) <= SCORE_TOL
+        assert port.recall(sel_np[h], port.topk(ref_scores, n)) >= 0.999
+        ref_out = port.gather_attention(qd, Kh, Vh, sel_np[h].astype(np.int64))
+        assert port.relative_l2_error(out[0, h].cpu().numpy(), ref_out) < OUT_TOL
