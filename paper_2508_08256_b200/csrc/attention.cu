@@ -19,7 +19,7 @@
 
 namespace fier_cuda {
 
-constexpr int kAttnWarps = 4;
+constexpr int kAttnWarps = 8;
 constexpr int kRowsPerStage = 8;
 
 template <typename T, int D>
@@ -74,23 +74,73 @@ __device__ __forceinline__ void unpack_vec(const uint4& v, float* f) {
     }
 }
 
-// One CTA = 4 warps over rows [r_begin, r_end) of one (b, head-set).
-// GATHER: rows are sel[r] of q head `head` (HPG must be 1).
-// !GATHER: rows are tokens r of kv head `head`, for HPG query heads.
+// Merge nsplit partials (m, l, o[D]) of `heads` consecutive heads (stride
+// nsplit*(D+2)) into out[h][D].  Called by one whole CTA; partials written by
+// other CTAs are read with ld.global.cg (L2, not a stale L1).  smem: 2*nsplit floats.
+template <int D>
+__device__ void merge_partials(const float* part, int nsplit, int heads, float* out, float* smem) {
+    for (int hh = 0; hh < heads; ++hh) {
+        const float* pp = part + (int64_t)hh * nsplit * (D + 2);
+        for (int sp = threadIdx.x; sp < nsplit; sp += blockDim.x) {
+            smem[sp] = __ldcg(pp + sp * (D + 2) + D);
+            smem[nsplit + sp] = __ldcg(pp + sp * (D + 2) + D + 1);
+        }
+        __syncthreads();
+        float M = -INFINITY;
+        for (int sp = 0; sp < nsplit; ++sp) M = fmaxf(M, smem[sp]);
+        float L = 0.f;
+        for (int sp = 0; sp < nsplit; ++sp)
+            if (smem[sp] != -INFINITY) L += smem[nsplit + sp] * exp2f(smem[sp] - M);
+        const float inv = 1.f / L;
+        for (int c = threadIdx.x; c < D; c += blockDim.x) {
+            float o = 0.f;
+#pragma unroll 4
+            for (int sp = 0; sp < nsplit; ++sp) {
+                const float ms = smem[sp];
+                const float x = __ldcg(pp + sp * (D + 2) + c);
+                if (ms != -INFINITY) o = fmaf(x, exp2f(ms - M), o);
+            }
+            out[(int64_t)hh * D + c] = o * inv;
+        }
+        __syncthreads();
+    }
+}
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, uint64_t policy) {
+    asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(smem_u32(smem)),
+                 "l"(gmem), "l"(policy)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+// One CTA = kAttnWarps independent warps over rows [r_begin, r_end) of one
+// (b, head-set); each warp streams its sub-range through a private NST-stage
+// shared-memory ring filled with 16-byte cp.async (every lane copies its share
+// of the stage's 8 K rows and 8 V rows; completion by commit/wait groups).
+// GATHER: rows are sel[r] of q head `head` (HPG == 1, q kept in registers).
+// !GATHER: rows are tokens r of kv head `head`, shared by its HPG query heads.
 template <typename T, int D, int HPG, bool GATHER, int NST>
 __global__ void __launch_bounds__(kAttnWarps * 32) attn_kernel(
     const T* __restrict__ q, const T* __restrict__ K, const T* __restrict__ V,
     const int32_t* __restrict__ sel, int n, int tokens, int cap, int hkv, int hq, float scale_log2,
-    int rows_per_cta, float* __restrict__ part, int nsplit) {
+    int rows_per_cta, float* __restrict__ part, int nsplit, int* __restrict__ counters,
+    float* __restrict__ out) {
     using TR = AttnTraits<T, D>;
     constexpr int CH = TR::CH, VEC = TR::VEC, EPV = TR::EPV, CPL = TR::CPL, RB = TR::RB;
-    constexpr int QSTRIDE = CH + 4;  // padded per-part q rows (bank spread)
+    constexpr int QSTRIDE = CH + 4;                 // padded per-part q rows (bank spread)
+    constexpr int CPR = RB / 16;                    // 16-byte chunks per row
+    constexpr int CPLANE = kRowsPerStage * CPR / 32;  // chunks per lane per K (or V) stage
+    static_assert(CPLANE >= 1 && (kRowsPerStage * CPR) % 32 == 0, "row width");
 
     extern __shared__ __align__(128) uint8_t smem[];
-    uint8_t* ring = smem;  // [warp][stage][K|V][8 rows]
+    uint8_t* ring = smem;  // [warp][stage][K|V][8 rows][RB]
     float* qs = reinterpret_cast<float*>(ring + (size_t)kAttnWarps * NST * 2 * TR::STAGE_BYTES);
-    float* wres = qs + HPG * 4 * QSTRIDE;               // [warp][HPG][D+2]
-    uint64_t* bars = reinterpret_cast<uint64_t*>(wres + kAttnWarps * HPG * (D + 2));
+    float* pbuf = qs + (HPG > 1 ? HPG * 4 * QSTRIDE : 0);  // [warp][HPG][8]
+    float* wres = pbuf + kAttnWarps * HPG * kRowsPerStage;  // [warp][HPG][D+2]
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int split = blockIdx.x, head = blockIdx.y, b = blockIdx.z;
@@ -107,88 +157,101 @@ __global__ void __launch_bounds__(kAttnWarps * 32) attn_kernel(
     const int wr1 = min(wr0 + rpw, r_end);
     const int nstages = (wr1 - wr0 + kRowsPerStage - 1) / kRowsPerStage;
     const int32_t* selrow = GATHER ? sel + ((int64_t)b * hq + head) * n : nullptr;
-
-    // q heads -> shared memory, fp32, [hh][part][CH] padded
     const int qh0 = GATHER ? head : head * HPG;
-    for (int i = threadIdx.x; i < HPG * D; i += blockDim.x) {
-        const int hh = i / D, c = i % D;
-        qs[hh * 4 * QSTRIDE + (c / CH) * QSTRIDE + (c % CH)] =
-            to_f32(q[((int64_t)b * hq + qh0 + hh) * D + c]);
+    const int row = lane >> 2, prt = lane & 3;
+
+    float qreg[HPG == 1 ? CH : 1];
+    if constexpr (HPG == 1) {
+        const T* qp = q + ((int64_t)b * hq + qh0) * D + prt * CH;
+#pragma unroll
+        for (int i = 0; i < CH; ++i) qreg[i] = to_f32(qp[i]);
+    } else {
+        for (int i = threadIdx.x; i < HPG * D; i += blockDim.x) {
+            const int hh = i / D, c = i % D;
+            qs[hh * 4 * QSTRIDE + (c / CH) * QSTRIDE + (c % CH)] =
+                to_f32(q[((int64_t)b * hq + qh0 + hh) * D + c]);
+        }
+        __syncthreads();
     }
-    uint64_t* wbar = bars + warp * NST;
-    if (lane == 0)
-        for (int s = 0; s < NST; ++s) mbar_init(&wbar[s], 1);
-    fence_barrier_init();
-    __syncthreads();
 
     uint8_t* wring = ring + (size_t)warp * NST * 2 * TR::STAGE_BYTES;
+    float* wp = pbuf + warp * HPG * kRowsPerStage;
     const uint64_t pol = policy_evict_first();
 
-    auto issue = [&](int st) {  // fill ring slot st % NST with stage st
-        if (st >= nstages) return;
-        uint8_t* kdst = wring + (size_t)(st % NST) * 2 * TR::STAGE_BYTES;
-        uint8_t* vdst = kdst + TR::STAGE_BYTES;
-        const int r0 = wr0 + st * kRowsPerStage;
-        const int nr = min(kRowsPerStage, wr1 - r0);
-        if (lane == 0) mbar_arrive_expect_tx(&wbar[st % NST], (uint32_t)(2 * nr * RB));
-        __syncwarp();
-        if constexpr (GATHER) {
+    auto issue = [&](int st) {  // copy stage st into ring slot st % NST (one commit group)
+        if (st < nstages) {
+            uint8_t* kdst = wring + (size_t)(st % NST) * 2 * TR::STAGE_BYTES;
+            uint8_t* vdst = kdst + TR::STAGE_BYTES;
+            const int r0 = wr0 + st * kRowsPerStage;
+            const int nr = min(kRowsPerStage, wr1 - r0);
             int tok = 0;
-            if (lane < nr) tok = selrow[r0 + lane];
-            const int tv = __shfl_sync(0xffffffffu, tok, lane & 7);
-            if (lane < nr)
-                bulk_g2s_evict_first(kdst + lane * RB, Kseq + (int64_t)tok * D, RB, &wbar[st % NST], pol);
-            else if (lane >= 8 && lane < 8 + nr)
-                bulk_g2s_evict_first(vdst + (lane - 8) * RB, Vseq + (int64_t)tv * D, RB,
-                                     &wbar[st % NST], pol);
-        } else {
-            if (lane == 0)
-                bulk_g2s_evict_first(kdst, Kseq + (int64_t)r0 * D, nr * RB, &wbar[st % NST], pol);
-            else if (lane == 1)
-                bulk_g2s_evict_first(vdst, Vseq + (int64_t)r0 * D, nr * RB, &wbar[st % NST], pol);
+            if constexpr (GATHER) {
+                if (lane < nr) tok = __ldg(selrow + r0 + lane);
+            }
+#pragma unroll
+            for (int c = 0; c < CPLANE; ++c) {
+                const int chunk = lane + 32 * c;
+                const int rr = chunk / CPR, off = chunk % CPR;
+                int t;
+                if constexpr (GATHER) {
+                    t = __shfl_sync(0xffffffffu, tok, rr);
+                } else {
+                    t = r0 + rr;
+                }
+                if (rr < nr) {
+                    cp_async16(kdst + rr * RB + off * 16, Kseq + (int64_t)t * D + off * (16 / sizeof(T)), pol);
+                    cp_async16(vdst + rr * RB + off * 16, Vseq + (int64_t)t * D + off * (16 / sizeof(T)), pol);
+                }
+            }
         }
+        cp_async_commit();
     };
 
-    for (int s = 0; s < NST; ++s) issue(s);
+#pragma unroll
+    for (int s = 0; s < NST - 1; ++s) issue(s);
 
-    const int row = lane >> 2, prt = lane & 3;
-    float m[HPG], l[HPG], acc[HPG][CPL];
+    float m[HPG], lloc[HPG], acc[HPG][CPL];
 #pragma unroll
     for (int hh = 0; hh < HPG; ++hh) {
         m[hh] = -INFINITY;
-        l[hh] = 0.f;
+        lloc[hh] = 0.f;
 #pragma unroll
         for (int i = 0; i < CPL; ++i) acc[hh][i] = 0.f;
     }
 
     for (int st = 0; st < nstages; ++st) {
-        mbar_wait(&wbar[st % NST], (uint32_t)((st / NST) & 1));
+        issue(st + NST - 1);
+        cp_async_wait<NST - 1>();
+        __syncwarp();
         const uint8_t* kst = wring + (size_t)(st % NST) * 2 * TR::STAGE_BYTES;
         const uint8_t* vst = kst + TR::STAGE_BYTES;
         const int nr = min(kRowsPerStage, wr1 - (wr0 + st * kRowsPerStage));
 
-        // K vectors of this lane's (row, part): kept in registers across heads
         float kf[CH];
-        if (row < nr) {
+        {
             const uint4* kp = reinterpret_cast<const uint4*>(kst + row * RB + prt * CH * sizeof(T));
 #pragma unroll
             for (int v = 0; v < VEC; ++v) unpack_vec<T>(kp[v], kf + v * EPV);
-        } else {
-#pragma unroll
-            for (int i = 0; i < CH; ++i) kf[i] = 0.f;
         }
-        float p[HPG];
 #pragma unroll
         for (int hh = 0; hh < HPG; ++hh) {
-            const float* qp = qs + hh * 4 * QSTRIDE + prt * QSTRIDE;
             float dot0 = 0.f, dot1 = 0.f;
+            if constexpr (HPG == 1) {
 #pragma unroll
-            for (int i = 0; i < CH; i += 4) {
-                const float4 qq = *reinterpret_cast<const float4*>(qp + i);
-                dot0 = fmaf(qq.x, kf[i], dot0);
-                dot1 = fmaf(qq.y, kf[i + 1], dot1);
-                dot0 = fmaf(qq.z, kf[i + 2], dot0);
-                dot1 = fmaf(qq.w, kf[i + 3], dot1);
+                for (int i = 0; i < CH; i += 2) {
+                    dot0 = fmaf(qreg[i], kf[i], dot0);
+                    dot1 = fmaf(qreg[i + 1], kf[i + 1], dot1);
+                }
+            } else {
+                const float* qp = qs + hh * 4 * QSTRIDE + prt * QSTRIDE;
+#pragma unroll
+                for (int i = 0; i < CH; i += 4) {
+                    const float4 qq = *reinterpret_cast<const float4*>(qp + i);
+                    dot0 = fmaf(qq.x, kf[i], dot0);
+                    dot1 = fmaf(qq.y, kf[i + 1], dot1);
+                    dot0 = fmaf(qq.z, kf[i + 2], dot0);
+                    dot1 = fmaf(qq.w, kf[i + 3], dot1);
+                }
             }
             float dot = dot0 + dot1;
             dot += __shfl_xor_sync(0xffffffffu, dot, 1);
@@ -199,38 +262,43 @@ __global__ void __launch_bounds__(kAttnWarps * 32) attn_kernel(
             mst = fmaxf(mst, __shfl_xor_sync(0xffffffffu, mst, 16));
             const float mnew = fmaxf(m[hh], mst);
             const float alpha = exp2f(m[hh] - mnew);
-            p[hh] = exp2f(logit - mnew);
-            float ps = prt == 0 ? p[hh] : 0.f;
-            ps = warp_sum(ps);
-            l[hh] = l[hh] * alpha + ps;
+            const float p = exp2f(logit - mnew);
+            lloc[hh] = lloc[hh] * alpha + (prt == 0 ? p : 0.f);
             m[hh] = mnew;
 #pragma unroll
             for (int i = 0; i < CPL; ++i) acc[hh][i] *= alpha;
+            if (prt == 0) wp[hh * kRowsPerStage + row] = p;
         }
-        for (int r = 0; r < nr; ++r) {
-            float vf[CPL];
-            load_v<T, CPL>(reinterpret_cast<const T*>(vst + r * RB), lane, vf);
+        __syncwarp();
 #pragma unroll
-            for (int hh = 0; hh < HPG; ++hh) {
-                const float pr = __shfl_sync(0xffffffffu, p[hh], r * 4);
+        for (int hh = 0; hh < HPG; ++hh) {
+            const float4 pa = *reinterpret_cast<const float4*>(wp + hh * kRowsPerStage);
+            const float4 pb = *reinterpret_cast<const float4*>(wp + hh * kRowsPerStage + 4);
+            const float pr[8] = {pa.x, pa.y, pa.z, pa.w, pb.x, pb.y, pb.z, pb.w};
 #pragma unroll
-                for (int i = 0; i < CPL; ++i) acc[hh][i] = fmaf(pr, vf[i], acc[hh][i]);
+            for (int r = 0; r < kRowsPerStage; ++r) {
+                if (r < nr) {
+                    float vf[CPL];
+                    load_v<T, CPL>(reinterpret_cast<const T*>(vst + r * RB), lane, vf);
+#pragma unroll
+                    for (int i = 0; i < CPL; ++i) acc[hh][i] = fmaf(pr[r], vf[i], acc[hh][i]);
+                }
             }
         }
         __syncwarp();
-        fence_proxy_async();
-        issue(st + NST);
     }
+    cp_async_wait<0>();
 
     // warp states -> smem -> CTA partial
     float* wr = wres + warp * HPG * (D + 2);
 #pragma unroll
     for (int hh = 0; hh < HPG; ++hh) {
+        const float l = warp_sum(lloc[hh]);
 #pragma unroll
         for (int i = 0; i < CPL; ++i) wr[hh * (D + 2) + lane * CPL + i] = acc[hh][i];
         if (lane == 0) {
             wr[hh * (D + 2) + D] = m[hh];
-            wr[hh * (D + 2) + D + 1] = l[hh];
+            wr[hh * (D + 2) + D + 1] = l;
         }
     }
     __syncthreads();
@@ -255,6 +323,22 @@ __global__ void __launch_bounds__(kAttnWarps * 32) attn_kernel(
             dst[D + 1] = L;
         }
     }
+    // The last CTA of this (b, head-set) merges the nsplit partials by
+    // log-sum-exp (threadFenceReduction pattern) and resets its counter, so
+    // the counters stay zero between calls (and CUDA-graph replays).
+    __shared__ int s_last;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        const int unit = b * (GATHER ? hq : hkv) + head;
+        s_last = atomicAdd(&counters[unit], 1) == nsplit - 1;
+        if (s_last) counters[unit] = 0;
+    }
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    merge_partials<D>(part + ((int64_t)b * hq + qh0) * nsplit * (D + 2), nsplit, HPG,
+                      out + ((int64_t)b * hq + qh0) * D, wres);
 }
 
 // LSE merge of nsplit partials per (b, q head): out = sum_s o_s 2^(m_s-M) / sum_s l_s 2^(m_s-M).
@@ -327,8 +411,8 @@ struct AttnPlan {
 };
 
 static AttnPlan plan_split(int64_t units, int total_rows, int min_rows) {
-    // ~3 resident CTAs per SM, one wave
-    const int64_t target = 148 * 3;
+    // ~2 resident CTAs (16 warps) per SM, one wave
+    const int64_t target = 148 * 2;
     int64_t ns = (target + units - 1) / units;
     if (ns < 1) ns = 1;
     int rpc = (int)ceil_div(total_rows, ns);
@@ -343,21 +427,21 @@ static AttnPlan plan_split(int64_t units, int total_rows, int min_rows) {
 
 template <typename T, int D>
 constexpr int attn_nst() {
-    return sizeof(T) == 4 ? 2 : 4;
+    return sizeof(T) == 4 ? 2 : 3;
 }
 
 template <typename T, int D, int HPG, bool GATHER>
 static size_t attn_smem() {
     using TR = AttnTraits<T, D>;
     constexpr int NST = attn_nst<T, D>();
-    return (size_t)kAttnWarps * NST * 2 * TR::STAGE_BYTES + (size_t)HPG * 4 * (TR::CH + 4) * 4 +
-           (size_t)kAttnWarps * HPG * (D + 2) * 4 + (size_t)kAttnWarps * NST * 8;
+    return (size_t)kAttnWarps * NST * 2 * TR::STAGE_BYTES + (HPG > 1 ? (size_t)HPG * 4 * (TR::CH + 4) * 4 : 0) +
+           (size_t)kAttnWarps * HPG * kRowsPerStage * 4 + (size_t)kAttnWarps * HPG * (D + 2) * 4;
 }
 
 template <typename T, int D, int HPG, bool GATHER>
 static int launch_attn(const fier_shape* s, const void* q, const void* K, const void* V,
                        const int32_t* sel, int n, int tokens, float scale, float* part,
-                       const AttnPlan& p, cudaStream_t st) {
+                       int* counters, float* out, const AttnPlan& p, cudaStream_t st) {
     constexpr int NST = attn_nst<T, D>();
     auto kern = attn_kernel<T, D, HPG, GATHER, NST>;
     const size_t smem = attn_smem<T, D, HPG, GATHER>();
@@ -366,7 +450,8 @@ static int launch_attn(const fier_shape* s, const void* q, const void* K, const 
     dim3 grid(p.nsplit, GATHER ? s->q_heads : s->kv_heads, s->batch);
     kern<<<grid, kAttnWarps * 32, smem, st>>>(
         static_cast<const T*>(q), static_cast<const T*>(K), static_cast<const T*>(V), sel, n, tokens,
-        s->capacity, s->kv_heads, s->q_heads, scale * kLog2e, p.rows_per_cta, part, p.nsplit);
+        s->capacity, s->kv_heads, s->q_heads, scale * kLog2e, p.rows_per_cta, part, p.nsplit,
+        counters, out);
     return check_launch("attention");
 }
 
@@ -386,55 +471,73 @@ static bool fast_dim(const fier_shape* s) {
     return s->dim == 128 || s->dim == 64;
 }
 
+static bool fast_hpg(const fier_shape* s) {
+    const int hpg = s->q_heads / s->kv_heads;
+    return hpg == 1 || hpg == 2 || hpg == 4 || hpg == 8;
+}
+
+constexpr int kMaxSplit = 256;  // the merging CTA keeps 2*nsplit floats in its smem
+
 AttnPlan sparse_plan(const fier_shape* s, int n) {
-    if (!fast_dim(s)) return plan_split((int64_t)s->batch * s->q_heads, n, 64);
-    return plan_split((int64_t)s->batch * s->q_heads, n, 64);
+    AttnPlan p = plan_split((int64_t)s->batch * s->q_heads, n, 64);
+    if (p.nsplit > kMaxSplit) {
+        p.rows_per_cta = (int)ceil_div(ceil_div(n, kMaxSplit), 32) * 32;
+        p.nsplit = (int)ceil_div(n, p.rows_per_cta);
+    }
+    return p;
 }
 
 AttnPlan full_plan(const fier_shape* s, int tokens) {
-    const bool fast = fast_dim(s);
+    const bool fast = fast_dim(s) && fast_hpg(s);
     const int64_t units = fast ? (int64_t)s->batch * s->kv_heads : (int64_t)s->batch * s->q_heads;
-    return plan_split(units, tokens, 256);
+    AttnPlan p = plan_split(units, tokens, 256);
+    if (p.nsplit > kMaxSplit) {
+        p.rows_per_cta = (int)ceil_div(ceil_div(tokens, kMaxSplit), 32) * 32;
+        p.nsplit = (int)ceil_div(tokens, p.rows_per_cta);
+    }
+    return p;
+}
+
+// workspace: [partials f32 B*Hq*nsplit*(d+2)][counters i32 B*Hq] (counters zeroed per call)
+static size_t part_bytes(const fier_shape* s, int nsplit) {
+    return (((size_t)s->batch * s->q_heads * nsplit * (s->dim + 2) * sizeof(float)) + 255) & ~(size_t)255;
 }
 
 size_t sparse_workspace(const fier_shape* s, int n) {
-    const AttnPlan p = sparse_plan(s, n);
-    return (size_t)s->batch * s->q_heads * p.nsplit * (s->dim + 2) * sizeof(float);
+    return part_bytes(s, sparse_plan(s, n).nsplit) + (size_t)s->batch * s->q_heads * sizeof(int);
 }
 
 size_t full_workspace(const fier_shape* s, int tokens) {
-    const AttnPlan p = full_plan(s, tokens);
-    return (size_t)s->batch * s->q_heads * p.nsplit * (s->dim + 2) * sizeof(float);
+    return part_bytes(s, full_plan(s, tokens).nsplit) + (size_t)s->batch * s->q_heads * sizeof(int);
 }
 
 template <typename T>
 static int sparse_typed(const fier_shape* s, const void* q, const void* K, const void* V,
-                        const int32_t* sel, int n, int tokens, float scale, float* part,
-                        const AttnPlan& p, cudaStream_t st) {
-    if (s->dim == 128) return launch_attn<T, 128, 1, true>(s, q, K, V, sel, n, tokens, scale, part, p, st);
-    if (s->dim == 64) return launch_attn<T, 64, 1, true>(s, q, K, V, sel, n, tokens, scale, part, p, st);
+                        const int32_t* sel, int n, int tokens, float scale, float* part, int* ctr,
+                        float* out, const AttnPlan& p, cudaStream_t st) {
+    if (s->dim == 128)
+        return launch_attn<T, 128, 1, true>(s, q, K, V, sel, n, tokens, scale, part, ctr, out, p, st);
+    if (s->dim == 64)
+        return launch_attn<T, 64, 1, true>(s, q, K, V, sel, n, tokens, scale, part, ctr, out, p, st);
     return launch_generic<T, true>(s, q, K, V, sel, n, tokens, scale, part, p, st);
 }
 
 template <typename T, int D>
 static int full_fast(const fier_shape* s, const void* q, const void* K, const void* V, int tokens,
-                     float scale, float* part, const AttnPlan& p, cudaStream_t st) {
+                     float scale, float* part, int* ctr, float* out, const AttnPlan& p, cudaStream_t st) {
     switch (s->q_heads / s->kv_heads) {
-        case 1: return launch_attn<T, D, 1, false>(s, q, K, V, nullptr, 0, tokens, scale, part, p, st);
-        case 2: return launch_attn<T, D, 2, false>(s, q, K, V, nullptr, 0, tokens, scale, part, p, st);
-        case 4: return launch_attn<T, D, 4, false>(s, q, K, V, nullptr, 0, tokens, scale, part, p, st);
-        case 8: return launch_attn<T, D, 8, false>(s, q, K, V, nullptr, 0, tokens, scale, part, p, st);
+        case 1: return launch_attn<T, D, 1, false>(s, q, K, V, nullptr, 0, tokens, scale, part, ctr, out, p, st);
+        case 2: return launch_attn<T, D, 2, false>(s, q, K, V, nullptr, 0, tokens, scale, part, ctr, out, p, st);
+        case 4: return launch_attn<T, D, 4, false>(s, q, K, V, nullptr, 0, tokens, scale, part, ctr, out, p, st);
+        default: return launch_attn<T, D, 8, false>(s, q, K, V, nullptr, 0, tokens, scale, part, ctr, out, p, st);
     }
-    return -1;
 }
 
 template <typename T>
 static int full_typed(const fier_shape* s, const void* q, const void* K, const void* V, int tokens,
-                      float scale, float* part, const AttnPlan& p, cudaStream_t st) {
-    const int hpg = s->q_heads / s->kv_heads;
-    const bool hpg_ok = hpg == 1 || hpg == 2 || hpg == 4 || hpg == 8;
-    if (hpg_ok && s->dim == 128) return full_fast<T, 128>(s, q, K, V, tokens, scale, part, p, st);
-    if (hpg_ok && s->dim == 64) return full_fast<T, 64>(s, q, K, V, tokens, scale, part, p, st);
+                      float scale, float* part, int* ctr, float* out, const AttnPlan& p, cudaStream_t st) {
+    if (fast_hpg(s) && s->dim == 128) return full_fast<T, 128>(s, q, K, V, tokens, scale, part, ctr, out, p, st);
+    if (fast_hpg(s) && s->dim == 64) return full_fast<T, 64>(s, q, K, V, tokens, scale, part, ctr, out, p, st);
     return launch_generic<T, false>(s, q, K, V, nullptr, 0, tokens, scale, part, p, st);
 }
 
@@ -444,33 +547,52 @@ static int merge(const fier_shape* s, const float* part, int nsplit, float* out,
     return check_launch("attention merge");
 }
 
+// counters_zeroed: the caller guarantees the counter words are zero (the fused
+// decode step zeroes them in its append kernel); otherwise a memset node is issued.
 int sparse_dispatch(const fier_shape* s, const void* q, const void* K, const void* V,
-                    const int32_t* sel, int n, int tokens, float scale, float* out, float* part,
-                    cudaStream_t st) {
+                    const int32_t* sel, int n, int tokens, float scale, float* out, void* ws,
+                    bool counters_zeroed, cudaStream_t st) {
     const AttnPlan p = sparse_plan(s, n);
+    float* part = static_cast<float*>(ws);
+    int* ctr = reinterpret_cast<int*>(static_cast<uint8_t*>(ws) + part_bytes(s, p.nsplit));
+    const bool fused = fast_dim(s);
+    if (fused && !counters_zeroed) {
+        cudaError_t e = cudaMemsetAsync(ctr, 0, (size_t)s->batch * s->q_heads * sizeof(int), st);
+        if (e != cudaSuccess) return fail(FIER_ECUDA, std::string("gather_attention: ") + cudaGetErrorString(e));
+    }
     int rc = FIER_OK;
     switch (s->dtype) {
-        case FIER_F32: rc = sparse_typed<float>(s, q, K, V, sel, n, tokens, scale, part, p, st); break;
-        case FIER_F16: rc = sparse_typed<__half>(s, q, K, V, sel, n, tokens, scale, part, p, st); break;
-        case FIER_BF16: rc = sparse_typed<__nv_bfloat16>(s, q, K, V, sel, n, tokens, scale, part, p, st); break;
+        case FIER_F32: rc = sparse_typed<float>(s, q, K, V, sel, n, tokens, scale, part, ctr, out, p, st); break;
+        case FIER_F16: rc = sparse_typed<__half>(s, q, K, V, sel, n, tokens, scale, part, ctr, out, p, st); break;
+        case FIER_BF16: rc = sparse_typed<__nv_bfloat16>(s, q, K, V, sel, n, tokens, scale, part, ctr, out, p, st); break;
         default: return fail(FIER_EINVAL, "fier_sparse_attention: unknown dtype");
     }
-    if (rc) return rc;
+    if (rc || fused) return rc;
     return merge(s, part, p.nsplit, out, st);
 }
 
 int full_dispatch(const fier_shape* s, const void* q, const void* K, const void* V, int tokens,
-                  float scale, float* out, float* part, cudaStream_t st) {
+                  float scale, float* out, void* ws, cudaStream_t st) {
     const AttnPlan p = full_plan(s, tokens);
+    float* part = static_cast<float*>(ws);
+    int* ctr = reinterpret_cast<int*>(static_cast<uint8_t*>(ws) + part_bytes(s, p.nsplit));
+    const bool fused = fast_dim(s) && fast_hpg(s);
+    if (fused) {
+        cudaError_t e = cudaMemsetAsync(ctr, 0, (size_t)s->batch * s->q_heads * sizeof(int), st);
+        if (e != cudaSuccess) return fail(FIER_ECUDA, std::string("gather_attention: ") + cudaGetErrorString(e));
+    }
     int rc = FIER_OK;
     switch (s->dtype) {
-        case FIER_F32: rc = full_typed<float>(s, q, K, V, tokens, scale, part, p, st); break;
-        case FIER_F16: rc = full_typed<__half>(s, q, K, V, tokens, scale, part, p, st); break;
-        case FIER_BF16: rc = full_typed<__nv_bfloat16>(s, q, K, V, tokens, scale, part, p, st); break;
+        case FIER_F32: rc = full_typed<float>(s, q, K, V, tokens, scale, part, ctr, out, p, st); break;
+        case FIER_F16: rc = full_typed<__half>(s, q, K, V, tokens, scale, part, ctr, out, p, st); break;
+        case FIER_BF16: rc = full_typed<__nv_bfloat16>(s, q, K, V, tokens, scale, part, ctr, out, p, st); break;
         default: return fail(FIER_EINVAL, "fier_full_attention: unknown dtype");
     }
-    if (rc) return rc;
+    if (rc || fused) return rc;
     return merge(s, part, p.nsplit, out, st);
 }
+
+// Offset of the counter words inside a sparse workspace (for the fused step).
+size_t sparse_counter_offset(const fier_shape* s, int n) { return part_bytes(s, sparse_plan(s, n).nsplit); }
 
 }  // namespace fier_cuda

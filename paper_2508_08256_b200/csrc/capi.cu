@@ -26,7 +26,7 @@ int check_launch(const char* what) {
 // kernels (pack.cu, score.cu, topk.cu, attention.cu)
 int pack_dispatch(const fier_shape*, const void*, int32_t, uint32_t*, void*, int32_t*, cudaStream_t);
 int append_dispatch(const fier_shape*, void*, void*, const void*, const void*, int32_t, uint32_t*,
-                    void*, int32_t*, cudaStream_t);
+                    void*, int32_t*, int*, int, cudaStream_t);
 int score_dispatch(const fier_shape*, const void*, const uint32_t*, const void*, int, float*, int64_t,
                    cudaStream_t);
 int topk_dispatch(const float*, int, int, int64_t, int, int32_t*, cudaStream_t);
@@ -34,9 +34,10 @@ size_t topk_workspace(int, int, int);
 size_t sparse_workspace(const fier_shape*, int);
 size_t full_workspace(const fier_shape*, int);
 int sparse_dispatch(const fier_shape*, const void*, const void*, const void*, const int32_t*, int, int,
-                    float, float*, float*, cudaStream_t);
-int full_dispatch(const fier_shape*, const void*, const void*, const void*, int, float, float*, float*,
+                    float, float*, void*, bool, cudaStream_t);
+int full_dispatch(const fier_shape*, const void*, const void*, const void*, int, float, float*, void*,
                   cudaStream_t);
+size_t sparse_counter_offset(const fier_shape*, int);
 
 static int check_shape(const fier_shape* s, const char* fn) {
     const std::string f(fn);
@@ -97,7 +98,7 @@ int fier_append(const fier_shape* s, void* K, void* V, const void* k_new, const 
     if (int rc = check_shape(s, "fier_append")) return rc;
     FIER_REQUIRE(pos >= 0 && pos < s->capacity, "fier_append: position outside cache capacity");
     FIER_REQUIRE(K && V && k_new && v_new && bits && params, "fier_append: null buffer");
-    return append_dispatch(s, K, V, k_new, v_new, pos, bits, params, nonfinite,
+    return append_dispatch(s, K, V, k_new, v_new, pos, bits, params, nonfinite, nullptr, 0,
                            static_cast<cudaStream_t>(stream));
 }
 
@@ -140,7 +141,7 @@ int fier_sparse_attention(const fier_shape* s, const void* q, const void* K, con
     FIER_REQUIRE(aligned16(K) && aligned16(V), "gather_attention: K/V must be 16-byte aligned");
     FIER_REQUIRE(workspace && workspace_bytes >= sparse_workspace(s, n),
                  "gather_attention: workspace too small");
-    return sparse_dispatch(s, q, K, V, sel, n, tokens, scale, out, static_cast<float*>(workspace),
+    return sparse_dispatch(s, q, K, V, sel, n, tokens, scale, out, workspace, false,
                            static_cast<cudaStream_t>(stream));
 }
 
@@ -158,8 +159,7 @@ int fier_full_attention(const fier_shape* s, const void* q, const void* K, const
     FIER_REQUIRE(aligned16(K) && aligned16(V), "gather_attention: K/V must be 16-byte aligned");
     FIER_REQUIRE(workspace && workspace_bytes >= full_workspace(s, tokens),
                  "gather_attention: workspace too small");
-    return full_dispatch(s, q, K, V, tokens, scale, out, static_cast<float*>(workspace),
-                         static_cast<cudaStream_t>(stream));
+    return full_dispatch(s, q, K, V, tokens, scale, out, workspace, static_cast<cudaStream_t>(stream));
 }
 
 int64_t fier_step_scores_ld(int32_t tokens) { return ceil_div(tokens, 32) * 32; }
@@ -185,15 +185,16 @@ int fier_decode_step(const fier_shape* s, const void* q, const void* k_new, cons
     const int64_t ld = fier_step_scores_ld(tokens);
     uint8_t* ws = static_cast<uint8_t*>(workspace);
     float* scores = scores_out ? scores_out : reinterpret_cast<float*>(ws);
-    float* part = reinterpret_cast<float*>(
-        ws + align_up((size_t)s->batch * s->q_heads * ld * sizeof(float)));
-    int rc = fier_append(s, K, V, k_new, v_new, pos, bits, params, nullptr, stream);
+    uint8_t* attn_ws = ws + align_up((size_t)s->batch * s->q_heads * ld * sizeof(float));
+    int* counters = reinterpret_cast<int*>(attn_ws + sparse_counter_offset(s, n));
+    int rc = append_dispatch(s, K, V, k_new, v_new, pos, bits, params, nullptr, counters,
+                             s->batch * s->q_heads, st);
     if (rc) return rc;
     rc = score_dispatch(s, q, bits, params, tokens, scores, ld, st);
     if (rc) return rc;
     rc = topk_dispatch(scores, s->batch * s->q_heads, tokens, ld, n, sel, st);
     if (rc) return rc;
-    return sparse_dispatch(s, q, K, V, sel, n, tokens, scale, out, part, st);
+    return sparse_dispatch(s, q, K, V, sel, n, tokens, scale, out, attn_ws, true, st);
 }
 
 // ---- host-side FIER conversion (io.hpp:197-277) ------------------------------------

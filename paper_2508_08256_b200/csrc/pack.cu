@@ -16,8 +16,20 @@
 
 namespace fier_cuda {
 
+// Values of one 32-token chunk of this lane's channel, loaded together (one
+// memory latency per chunk instead of one per token).  bf16/fp16/fp32 are
+// exact in fp32; they are widened to fp64 for the arithmetic below.
 template <typename T>
-__device__ __forceinline__ void pack_group(const T* __restrict__ Kseq, int d, int W, int g, int gi,
+__device__ __forceinline__ void load_chunk(const T* Kseq, int d, int c, bool valid,
+                                           int tc, int cnt, float (&v)[32]) {
+#pragma unroll
+    for (int i = 0; i < 32; ++i)
+        v[i] = (valid && i < cnt) ? to_f32(Kseq[(int64_t)(tc + i) * d + c]) : 0.f;
+}
+
+template <typename T>
+__device__ __forceinline__ void pack_group(const T* Kseq,  // no restrict: append re-reads its own store
+                                           int d, int W, int g, int gi,
                                            int t_end, uint32_t* __restrict__ bits_seq,
                                            __half2* __restrict__ sz_seq, int32_t* nonfinite) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -25,34 +37,44 @@ __device__ __forceinline__ void pack_group(const T* __restrict__ Kseq, int d, in
     const bool valid = c < d;
     const int t0 = gi * g;
     const int t1 = min(t0 + g, t_end);  // short final group (quant1bit.hpp:84)
-    double mn = 0.0, mx = 0.0, z = 0.0, s = 0.0;
+    float v[32];
+    double mn = 0.0, mx = 0.0;
     bool bad = false;
-    if (valid) {
-        const double first = to_f64(Kseq[(int64_t)t0 * d + c]);
-        mn = mx = first;
-        bad = !isfinite(first);
-        for (int t = t0 + 1; t < t1; ++t) {
-            const double v = to_f64(Kseq[(int64_t)t * d + c]);
-            bad |= !isfinite(v);
-            mn = (v < mn) ? v : mn;
-            mx = (mx < v) ? v : mx;
-        }
-        z = (mx + mn) / 2.0;
-        s = (mx - mn) / 2.0;
-        sz_seq[(int64_t)gi * d + c] = __halves2half2(__double2half(s), __double2half(z));
-    }
-    if (bad && nonfinite) atomicExch(nonfinite, 1);
+    // pass 1: min/max in token order, first seen wins ties (std::min/std::max)
     for (int tc = t0; tc < t1; tc += 32) {
-        uint32_t mine = 0;
         const int cnt = min(32, t1 - tc);
-        for (int i = 0; i < cnt; ++i) {
-            bool bit = false;
-            if (valid) {
-                const double v = to_f64(Kseq[(int64_t)(tc + i) * d + c]);
-                bit = (s == 0.0) || (v >= z);
+        load_chunk<T>(Kseq, d, c, valid, tc, cnt, v);
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+            if (i < cnt) {
+                const double x = (double)v[i];
+                bad |= !isfinite(x);
+                if (tc == t0 && i == 0) {
+                    mn = mx = x;
+                } else {
+                    mn = (x < mn) ? x : mn;
+                    mx = (mx < x) ? x : mx;
+                }
             }
-            const uint32_t word = __ballot_sync(0xffffffffu, bit);
-            if (lane == i) mine = word;
+        }
+    }
+    const double z = (mx + mn) / 2.0;
+    const double s = (mx - mn) / 2.0;
+    if (valid) sz_seq[(int64_t)gi * d + c] = __halves2half2(__double2half(s), __double2half(z));
+    if (bad && nonfinite) atomicExch(nonfinite, 1);
+    // pass 2: one ballot per token -> the word of (token, 32 channels); for
+    // g <= 32 the chunk is still in registers.
+    for (int tc = t0; tc < t1; tc += 32) {
+        const int cnt = min(32, t1 - tc);
+        if (g > 32) load_chunk<T>(Kseq, d, c, valid, tc, cnt, v);
+        uint32_t mine = 0;
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+            if (i < cnt) {
+                const bool bit = valid && ((s == 0.0) || ((double)v[i] >= z));
+                const uint32_t word = __ballot_sync(0xffffffffu, bit);
+                if (lane == i) mine = word;
+            }
         }
         if (lane < cnt) bits_seq[(int64_t)(tc + lane) * W + warp] = mine;
     }
@@ -75,10 +97,18 @@ __global__ void __launch_bounds__(1024) append_kernel(T* __restrict__ K, T* __re
                                                        const T* __restrict__ v_new, int pos, int cap,
                                                        int d, int W, int g, int G, int hkv,
                                                        uint32_t* __restrict__ bits,
-                                                       __half2* __restrict__ sz, int32_t* nonfinite) {
+                                                       __half2* __restrict__ sz, int32_t* nonfinite,
+                                                       int* zero_words, int zero_n) {
     const int h = blockIdx.y, b = blockIdx.z;
     const int64_t seq = (int64_t)b * hkv + h;
     T* Kseq = K + seq * cap * d;
+    if (zero_words) {  // the fused step's attention-merge counters (stream-ordered before K4)
+        const int per = (zero_n + gridDim.y * gridDim.z - 1) / (gridDim.y * gridDim.z);
+        for (int i = threadIdx.x; i < per; i += blockDim.x) {
+            const int64_t j = seq * per + i;
+            if (j < zero_n) zero_words[j] = 0;
+        }
+    }
     const int c = threadIdx.x;
     if (c < d) {
         // Same thread writes then re-reads channel c below: program order suffices.
@@ -105,7 +135,7 @@ static int launch_pack(const fier_shape* s, const void* K, int32_t tokens, uint3
 template <typename T>
 static int launch_append(const fier_shape* s, void* K, void* V, const void* k_new,
                          const void* v_new, int32_t pos, uint32_t* bits, void* params,
-                         int32_t* nonfinite, cudaStream_t st) {
+                         int32_t* nonfinite, int* zero_words, int zero_n, cudaStream_t st) {
     const int W = (s->dim + 31) / 32;
     const int G = (int)ceil_div(s->capacity, s->group);
     dim3 grid(1, s->kv_heads, s->batch);
@@ -113,7 +143,8 @@ static int launch_append(const fier_shape* s, void* K, void* V, const void* k_ne
                                               static_cast<const T*>(k_new),
                                               static_cast<const T*>(v_new), pos, s->capacity,
                                               s->dim, W, s->group, G, s->kv_heads, bits,
-                                              static_cast<__half2*>(params), nonfinite);
+                                              static_cast<__half2*>(params), nonfinite, zero_words,
+                                              zero_n);
     return check_launch("fier_append");
 }
 
@@ -128,15 +159,16 @@ int pack_dispatch(const fier_shape* s, const void* K, int32_t tokens, uint32_t* 
 }
 
 int append_dispatch(const fier_shape* s, void* K, void* V, const void* k_new, const void* v_new,
-                    int32_t pos, uint32_t* bits, void* params, int32_t* nonfinite, cudaStream_t st) {
+                    int32_t pos, uint32_t* bits, void* params, int32_t* nonfinite, int* zero_words,
+                    int zero_n, cudaStream_t st) {
     switch (s->dtype) {
         case FIER_F32:
-            return launch_append<float>(s, K, V, k_new, v_new, pos, bits, params, nonfinite, st);
+            return launch_append<float>(s, K, V, k_new, v_new, pos, bits, params, nonfinite, zero_words, zero_n, st);
         case FIER_F16:
-            return launch_append<__half>(s, K, V, k_new, v_new, pos, bits, params, nonfinite, st);
+            return launch_append<__half>(s, K, V, k_new, v_new, pos, bits, params, nonfinite, zero_words, zero_n, st);
         case FIER_BF16:
             return launch_append<__nv_bfloat16>(s, K, V, k_new, v_new, pos, bits, params,
-                                                nonfinite, st);
+                                                nonfinite, zero_words, zero_n, st);
     }
     return fail(FIER_EINVAL, "fier_append: unknown dtype");
 }

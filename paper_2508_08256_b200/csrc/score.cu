@@ -76,9 +76,12 @@ __global__ void __launch_bounds__(kScoreWarps * 32) score128_kernel(
             w.z = qv[hh][2] * s[2];
             w.w = qv[hh][3] * s[3];
             wtab[warp][hh][lane] = w;
-            float bz = qv[hh][0] * z[0] + qv[hh][1] * z[1] + qv[hh][2] * z[2] + qv[hh][3] * z[3];
-            float bs = w.x + w.y + w.z + w.w;
-            bias[hh] = warp_sum(bz) - warp_sum(bs);
+            // sum_j q_j (z_j - s_j) over this lane's 4 channels, one warp reduction
+            float bz = qv[hh][0] * (z[0] - s[0]);
+            bz = fmaf(qv[hh][1], z[1] - s[1], bz);
+            bz = fmaf(qv[hh][2], z[2] - s[2], bz);
+            bz = fmaf(qv[hh][3], z[3] - s[3], bz);
+            bias[hh] = warp_sum(bz);
         }
         __syncwarp();
 

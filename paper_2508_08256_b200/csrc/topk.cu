@@ -1,21 +1,30 @@
-// topk.cu -- K3: per-head Top-k token selector (radix select, exact tie rule).
+// topk.cu -- K3: per-head Top-k token selector.
 //
 // Replaces topk_oracle (reference core.hpp:134-148): the k largest scores,
 // ties to the LOWER index, returned in ascending index order.
 //
-// One thread-block cluster (C CTAs, C <= 8) per score row; CTA r owns the
-// contiguous slice [r*S, (r+1)*S) of the row, caches its order-preserving u32
-// keys in shared memory, and the cluster runs three radix passes (11/11/10
-// bits) over them.  Each pass builds a shared-memory histogram of the keys
-// still matching the resolved prefix; the cluster sums the C histograms over
-// distributed shared memory and every CTA finds the same digit (deterministic,
-// no atomics across CTAs).  After the passes the exact threshold key T and
-// the number r of T-valued keys to keep are known.  Compaction is a pure
-// function of index order: a key at position i is kept iff key > T or
-// (key == T and #(T-valued keys before i) < r), and its output slot is
-// #(> T before i) + min(#(== T before i), r) -- warp ballots + a block scan
-// + a cluster prefix over the CTA totals, so the output is ascending without
-// any sort.
+// One thread-block cluster (C <= 8 CTAs of 256 threads) per score row; CTA r
+// owns the contiguous slice [r*S, (r+1)*S) and keeps its keys in registers
+// (KPT per thread, slot j of lane L of warp w = position w*32*KPT + 32j + L).
+// Shared-memory atomics cost ~2 cycles per lane on this part, so histograms
+// are counted WITHOUT atomics: per 32-key slot a warp "multisplit" (6 ballots
+// give every lane the mask of lanes sharing its bin; the lowest such lane adds
+// the popcount into the warp's private smem row).
+//
+//   1. (lo, hi) = min/max of the finite scores of the row (cluster exchange).
+//   2. 32 linear bins over [lo, hi] -> bin b1 holding the k-th largest.
+//   3. 32 linear sub-bins over b1's range -> b2.  Both binnings are monotone
+//      non-decreasing functions of the value, so everything in a higher bin is
+//      strictly larger than everything in a lower one.
+//   4. Candidates = keys in (b1, b2) (typically tens): gathered over DSMEM and
+//      ranked exactly by (value desc, index asc) -> threshold T and the number
+//      r of T-valued keys to keep.
+//   5. Compaction in index order with ballots: kept iff above (b1,b2), or a
+//      candidate with key > T, or key == T among the first r ties; output slot
+//      = #kept before it.  Output is ascending without a sort.
+// If the candidate set overflows (massive ties / degenerate ranges) the
+// cluster switches to an exact 3-pass radix select on the order-preserving
+// keys (smem histograms), then the same compaction.
 #include <cooperative_groups.h>
 
 #include "common.cuh"
@@ -24,45 +33,103 @@ namespace cg = cooperative_groups;
 
 namespace fier_cuda {
 
-constexpr int kTkThreads = 1024;
-constexpr int kTkBins = 2048;
-constexpr int kTkMaxCached = 32768;  // keys per CTA kept in shared memory
-constexpr int kTkMisc = 160;  // scan scratch [0,64), results [64,72), warp counts [72,136)
+constexpr int kTkThreads = 256;
+constexpr int kTkWarps = kTkThreads / 32;
+constexpr int kTkMaxCluster = 8;
+constexpr int kTkCandCta = 512;   // candidates one CTA may contribute
+constexpr int kTkCandAll = 1024;  // candidates a cluster may rank (fast path)
+constexpr int kTkRadixBins = 2048;
 
-// Block-wide exclusive scan of one u32 per thread; returns the exclusive
-// prefix and writes the block total to *total (all threads).
-__device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* scratch, uint32_t* total) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    uint32_t x = v;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-        if (lane >= o) x += y;
-    }
-    if (lane == 31) scratch[warp] = x;
-    __syncthreads();
-    if (warp == 0) {
-        const int nw = blockDim.x >> 5;
-        uint32_t w = lane < nw ? scratch[lane] : 0u;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t y = __shfl_up_sync(0xffffffffu, w, o);
-            if (lane >= o) w += y;
-        }
-        scratch[32 + lane] = w;  // inclusive warp prefix
-    }
-    __syncthreads();
-    const uint32_t warp_excl = warp ? scratch[32 + warp - 1] : 0u;
-    *total = scratch[32 + (blockDim.x >> 5) - 1];
-    const uint32_t r = warp_excl + x - v;
-    __syncthreads();
-    return r;
+struct TopkShared {
+    // exchanged over DSMEM (read by other CTAs after a cluster barrier)
+    float mm[2];                  // local min, max of finite values
+    uint32_t h1[32];              // CTA histogram, pass 1
+    uint32_t h2[32];              // CTA histogram, pass 2
+    uint32_t ncand, nabove;       // candidates / strictly-above count of this CTA
+    uint32_t cand_key[kTkCandCta];
+    int32_t cand_idx[kTkCandCta];
+    uint32_t rhist[2][kTkRadixBins];  // fallback radix histograms
+    uint32_t rsel[2];             // fallback: CTA counts (> T, == T)
+    // CTA-private
+    uint32_t wh[kTkWarps][32];    // per-warp histogram rows
+    uint32_t all_key[kTkCandAll];
+    int32_t all_idx[kTkCandAll];
+    uint32_t all_cta[kTkCandAll];
+    uint32_t tot[kTkRadixBins];
+    uint32_t scratch[64];
+    uint32_t wcnt[kTkWarps];
+    float fscratch[2 * kTkWarps];
+    uint32_t res[8];
+};
+
+__device__ __forceinline__ uint32_t lanemask_lt() {
+    uint32_t m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
 }
 
-template <bool CACHED>
-__global__ void __launch_bounds__(kTkThreads, 1)
-    topk_kernel(const float* __restrict__ scores, int tokens, int64_t ld, int k, int slice,
-                int32_t* __restrict__ sel) {
+// Warp multisplit of a bin id in [0, 64): adds each bin's lane count into row[bin]
+// (bins >= 32 are ignored).  No atomics: one leader lane per distinct bin.
+__device__ __forceinline__ void warp_count_bins(uint32_t bin, uint32_t* row) {
+    uint32_t peers = 0xffffffffu;
+#pragma unroll
+    for (int bit = 0; bit < 6; ++bit) {
+        const uint32_t m = __ballot_sync(0xffffffffu, (bin >> bit) & 1u);
+        peers &= ((bin >> bit) & 1u) ? m : ~m;
+    }
+    if (bin < 32 && (peers & lanemask_lt()) == 0) row[bin] += __popc(peers);
+}
+
+// suffix search over 32 bins held one per lane (lane b has count of bin b):
+// returns in all lanes the bin b* with above(b*) < krem <= above(b*)+cnt(b*),
+// above(b) = sum of bins > b.
+__device__ __forceinline__ void find_bin32(uint32_t cnt, uint32_t krem, uint32_t* bin,
+                                           uint32_t* above) {
+    const int lane = threadIdx.x & 31;
+    // inclusive suffix sum: s(b) = sum_{b' >= b}
+    uint32_t s = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_down_sync(0xffffffffu, s, o);
+        if (lane + o < 32) s += y;
+    }
+    const uint32_t ab = s - cnt;
+    const uint32_t hit = __ballot_sync(0xffffffffu, ab < krem && krem <= s);
+    const int b = 31 - __clz(hit);  // unique in exact arithmetic; highest if any
+    *bin = (uint32_t)b;
+    *above = __shfl_sync(0xffffffffu, ab, b);
+}
+
+__device__ __forceinline__ int lin_bin(float x, float lo, float inv) {
+    if (x == INFINITY) return 31;
+    if (x == -INFINITY) return 0;
+    float t = (x - lo) * inv;
+    t = fminf(fmaxf(t, 0.f), 31.f);
+    return (int)t;  // truncation == floor on [0, 31]
+}
+
+// Block-wide exclusive scan over warps of one value per warp (lane 0 holds it);
+// returns the warp's exclusive prefix in all lanes and the block total.
+__device__ __forceinline__ uint32_t warp_prefix(uint32_t v, uint32_t* wcnt, uint32_t* total) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (lane == 0) wcnt[warp] = v;
+    __syncthreads();
+    uint32_t ex = 0, t = 0;
+#pragma unroll
+    for (int w = 0; w < kTkWarps; ++w) {
+        const uint32_t x = wcnt[w];
+        ex += w < warp ? x : 0u;
+        t += x;
+    }
+    __syncthreads();
+    *total = t;
+    return ex;
+}
+
+template <int KPT>
+__global__ void __launch_bounds__(kTkThreads) topk_kernel(const float* __restrict__ scores, int tokens,
+                                                          int64_t ld, int k, int slice,
+                                                          int32_t* __restrict__ sel) {
     cg::cluster_group cluster = cg::this_cluster();
     const int nct = (int)cluster.num_blocks();
     const int rank = (int)cluster.block_rank();
@@ -71,90 +138,392 @@ __global__ void __launch_bounds__(kTkThreads, 1)
     const float* srow = scores + (int64_t)row * ld;
     const int s0 = rank * slice;
     const int cnt = max(0, min(s0 + slice, tokens) - s0);
+    extern __shared__ __align__(16) uint8_t smem_raw[];
+    TopkShared& S = *reinterpret_cast<TopkShared*>(smem_raw);
 
-    extern __shared__ __align__(16) uint32_t smem[];
-    uint32_t* hist0 = smem;
-    uint32_t* hist1 = smem + kTkBins;
-    uint32_t* tot = smem + 2 * kTkBins;
-    uint32_t* misc = smem + 3 * kTkBins;  // [0..63] scan scratch, [64..] results
-    uint32_t* keys = misc + kTkMisc;
+    // ---- load: slot j of this lane = position warp*32*KPT + 32j + lane ----
+    const int wbase = warp * 32 * KPT;
+    float x[KPT];
+    float mn = INFINITY, mx = -INFINITY;
+#pragma unroll
+    for (int j = 0; j < KPT; ++j) {
+        const int p = wbase + 32 * j + lane;
+        x[j] = p < cnt ? srow[s0 + p] : __int_as_float(0x7fffffff);  // NaN = empty slot
+        if (isfinite(x[j])) {
+            mn = fminf(mn, x[j]);
+            mx = fmaxf(mx, x[j]);
+        }
+    }
+    for (int i = tid; i < kTkWarps * 32; i += kTkThreads) (&S.wh[0][0])[i] = 0;
+    mn = -warp_max(-mn);
+    mx = warp_max(mx);
+    if (lane == 0) {
+        S.fscratch[warp] = mn;
+        S.fscratch[kTkWarps + warp] = mx;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        float a = INFINITY, b = -INFINITY;
+        for (int w = 0; w < kTkWarps; ++w) {
+            a = fminf(a, S.fscratch[w]);
+            b = fmaxf(b, S.fscratch[kTkWarps + w]);
+        }
+        S.mm[0] = a;
+        S.mm[1] = b;
+    }
+    cluster.sync();  // #1
+    float lo = INFINITY, hi = -INFINITY;
+    for (int r = 0; r < nct; ++r) {
+        const float* m = cluster.map_shared_rank(S.mm, r);
+        lo = fminf(lo, m[0]);
+        hi = fmaxf(hi, m[1]);
+    }
+    if (!(lo <= hi)) {  // no finite values
+        lo = 0.f;
+        hi = 0.f;
+    }
+    const float inv1 = hi > lo ? 32.f / (hi - lo) : 0.f;
 
-    uint32_t prefix = 0, pmask = 0;
-    uint32_t krem = (uint32_t)k;
+    // ---- pass 1: 32 bins over [lo, hi] ----
+#pragma unroll
+    for (int j = 0; j < KPT; ++j) {
+        const bool v = !isnan(x[j]);
+        warp_count_bins(v ? (uint32_t)lin_bin(x[j], lo, inv1) : 63u, S.wh[warp]);
+    }
+    __syncthreads();
+    if (tid < 32) {
+        uint32_t c = 0;
+        for (int w = 0; w < kTkWarps; ++w) {
+            c += S.wh[w][tid];
+            S.wh[w][tid] = 0;
+        }
+        S.h1[tid] = c;
+    }
+    cluster.sync();  // #2
+    uint32_t b1, above1, b2, above2;
+    {
+        uint32_t c = 0;
+        if (lane < 32)
+            for (int r = 0; r < nct; ++r) c += cluster.map_shared_rank(S.h1, r)[lane];
+        find_bin32(c, (uint32_t)k, &b1, &above1);
+    }
+    // ---- pass 2: 32 sub-bins over bin b1 ----
+    const float w1 = (hi - lo) / 32.f;
+    const float lo2 = lo + (float)b1 * w1;
+    const float inv2 = w1 > 0.f ? 32.f / w1 : 0.f;
+    auto bins12 = [&](float v, int* p1, int* p2) {
+        *p1 = lin_bin(v, lo, inv1);
+        *p2 = lin_bin(v, lo2, inv2);
+    };
+#pragma unroll
+    for (int j = 0; j < KPT; ++j) {
+        int p1, p2;
+        bins12(x[j], &p1, &p2);
+        const bool in = !isnan(x[j]) && p1 == (int)b1;
+        warp_count_bins(in ? (uint32_t)p2 : 63u, S.wh[warp]);
+    }
+    __syncthreads();
+    if (tid < 32) {
+        uint32_t c = 0;
+        for (int w = 0; w < kTkWarps; ++w) c += S.wh[w][tid];
+        S.h2[tid] = c;
+    }
+    if (tid == 0) S.ncand = 0;
+    cluster.sync();  // #3
+    {
+        uint32_t c = 0;
+        for (int r = 0; r < nct; ++r) c += cluster.map_shared_rank(S.h2, r)[lane];
+        find_bin32(c, (uint32_t)k - above1, &b2, &above2);
+    }
+    uint32_t krem = (uint32_t)k - above1 - above2;  // >= 1
 
+    // ---- candidates (b1, b2) and the strictly-above count of this CTA ----
+    auto cls = [&](float v) -> int {  // 2 = above, 1 = candidate, 0 = below/empty
+        if (isnan(v)) return 0;
+        int p1, p2;
+        bins12(v, &p1, &p2);
+        if (p1 != (int)b1) return p1 > (int)b1 ? 2 : 0;
+        if (p2 != (int)b2) return p2 > (int)b2 ? 2 : 0;
+        return 1;
+    };
+    uint32_t nab = 0;
+#pragma unroll
+    for (int j = 0; j < KPT; ++j) {
+        const int c = cls(x[j]);
+        nab += __popc(__ballot_sync(0xffffffffu, c == 2));
+        const uint32_t m = __ballot_sync(0xffffffffu, c == 1);
+        if (m) {
+            uint32_t base = 0;
+            if (lane == __ffs(m) - 1) base = atomicAdd(&S.ncand, (uint32_t)__popc(m));
+            base = __shfl_sync(0xffffffffu, base, __ffs(m) - 1);
+            const uint32_t slot = base + __popc(m & lanemask_lt());
+            if (c == 1 && slot < kTkCandCta) {
+                S.cand_key[slot] = float_key(x[j]);
+                S.cand_idx[slot] = s0 + wbase + 32 * j + lane;
+            }
+        }
+    }
+    uint32_t tot_ab;
+    warp_prefix(nab, S.wcnt, &tot_ab);
+    if (tid == 0) S.nabove = tot_ab;
+    cluster.sync();  // #4
+    uint32_t ncand_all = 0, ncand_max = 0;
+    for (int r = 0; r < nct; ++r) {
+        const uint32_t c = *cluster.map_shared_rank(&S.ncand, r);
+        ncand_all += c;
+        ncand_max = max(ncand_max, c);
+    }
+
+    uint32_t T;                 // threshold key
+    uint32_t sel_before = 0;    // kept elements in lower-ranked CTAs
+    uint32_t eq_before = 0;     // T-valued keys in lower-ranked CTAs
+    bool radix = ncand_max > kTkCandCta || ncand_all > kTkCandAll;  // uniform
+    if (!radix) {
+        // gather every candidate (rank order of CTAs), rank by (key desc, idx asc)
+        uint32_t off = 0;
+        for (int r = 0; r < nct; ++r) {
+            const uint32_t c = *cluster.map_shared_rank(&S.ncand, r);
+            const uint32_t* rk = cluster.map_shared_rank(S.cand_key, r);
+            const int32_t* ri = cluster.map_shared_rank(S.cand_idx, r);
+            for (uint32_t i = tid; i < c; i += kTkThreads) {
+                S.all_key[off + i] = rk[i];
+                S.all_idx[off + i] = ri[i];
+                S.all_cta[off + i] = (uint32_t)r;
+            }
+            off += c;
+        }
+        __syncthreads();
+        for (uint32_t i = tid; i < ncand_all; i += kTkThreads) {
+            const uint32_t ki = S.all_key[i];
+            const int32_t ii = S.all_idx[i];
+            uint32_t rk = 0;
+            for (uint32_t j = 0; j < ncand_all; ++j) {
+                const uint32_t kj = S.all_key[j];
+                rk += (kj > ki) || (kj == ki && S.all_idx[j] < ii);
+            }
+            if (rk == krem - 1) S.res[0] = ki;
+        }
+        __syncthreads();
+        T = S.res[0];
+        // r = number of T-valued candidates kept = krem - #(candidates > T)
+        uint32_t gtT = 0;
+        for (uint32_t i = lane; i < ncand_all; i += 32) gtT += S.all_key[i] > T;
+        for (int o = 16; o > 0; o >>= 1) gtT += __shfl_xor_sync(0xffffffffu, gtT, o);
+        const uint32_t rties = krem - gtT;
+        // per lower CTA: kept = above + candidates > T + min(ties there, remaining ties)
+        uint32_t ties_seen = 0;
+        for (int r = 0; r < rank; ++r) {
+            uint32_t cg_ = 0, ce = 0;
+            for (uint32_t i = lane; i < ncand_all; i += 32) {
+                if (S.all_cta[i] == (uint32_t)r) {
+                    cg_ += S.all_key[i] > T;
+                    ce += S.all_key[i] == T;
+                }
+            }
+            for (int o = 16; o > 0; o >>= 1) {
+                cg_ += __shfl_xor_sync(0xffffffffu, cg_, o);
+                ce += __shfl_xor_sync(0xffffffffu, ce, o);
+            }
+            const uint32_t take = min(ce, rties > ties_seen ? rties - ties_seen : 0u);
+            sel_before += *cluster.map_shared_rank(&S.nabove, r) + cg_ + take;
+            ties_seen += ce;
+        }
+        eq_before = ties_seen;
+        krem = rties;  // from here: keep the first krem T-valued keys (global order)
+    } else {
+        // ---- exact radix fallback on the order-preserving keys ----
+        uint32_t prefix = 0, pmask = 0, kr = (uint32_t)k;
+#pragma unroll 1
+        for (int pass = 0; pass < 3; ++pass) {
+            const int shift = pass == 0 ? 21 : (pass == 1 ? 10 : 0);
+            const int bins = pass == 2 ? 1024 : 2048;
+            uint32_t* h = S.rhist[pass & 1];
+            for (int i = tid; i < bins; i += kTkThreads) h[i] = 0;
+            __syncthreads();
+#pragma unroll
+            for (int j = 0; j < KPT; ++j) {
+                if (!isnan(x[j])) {
+                    const uint32_t key = float_key(x[j]);
+                    if ((key & pmask) == prefix) atomicAdd(&h[(key >> shift) & (bins - 1)], 1u);
+                }
+            }
+            cluster.sync();
+            for (int i = tid; i < bins; i += kTkThreads) {
+                uint32_t a = 0;
+                for (int r = 0; r < nct; ++r) a += cluster.map_shared_rank(h, r)[i];
+                S.tot[i] = a;
+            }
+            __syncthreads();
+            if (warp == 0) {  // descending scan, 32 lanes x bins/32 bins each
+                const int per = bins / 32;
+                uint32_t loc = 0;
+                for (int j = 0; j < per; ++j) loc += S.tot[bins - 1 - (lane * per + j)];
+                uint32_t inc = loc;
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+                    if (lane >= o) inc += y;
+                }
+                uint32_t ab = inc - loc;
+                for (int j = 0; j < per; ++j) {
+                    const int bin = bins - 1 - (lane * per + j);
+                    const uint32_t c = S.tot[bin];
+                    if (ab < kr && kr <= ab + c) {
+                        S.res[1] = (uint32_t)bin;
+                        S.res[2] = ab;
+                    }
+                    ab += c;
+                }
+            }
+            __syncthreads();
+            kr -= S.res[2];
+            prefix |= S.res[1] << shift;
+            pmask |= (uint32_t)(bins - 1) << shift;
+            __syncthreads();
+        }
+        T = prefix;
+        // CTA counts of (> T, == T) -> prefixes over lower CTAs
+        uint32_t g = 0, e = 0;
+#pragma unroll
+        for (int j = 0; j < KPT; ++j) {
+            const uint32_t key = isnan(x[j]) ? 0u : float_key(x[j]);
+            g += __popc(__ballot_sync(0xffffffffu, !isnan(x[j]) && key > T));
+            e += __popc(__ballot_sync(0xffffffffu, !isnan(x[j]) && key == T));
+        }
+        uint32_t tg, te;
+        warp_prefix(g, S.wcnt, &tg);
+        warp_prefix(e, S.wcnt, &te);
+        if (tid == 0) {
+            S.rsel[0] = tg;
+            S.rsel[1] = te;
+        }
+        cluster.sync();
+        uint32_t gb = 0, eb = 0;
+        for (int r = 0; r < rank; ++r) {
+            const uint32_t* m = cluster.map_shared_rank(S.rsel, r);
+            gb += m[0];
+            eb += m[1];
+        }
+        sel_before = gb + min(eb, kr);
+        eq_before = eb;
+        krem = kr;
+    }
+
+    // ---- compaction in index order: kept iff key > T or (key == T and tie rank < krem) ----
+    // warp-level counts first (warps own contiguous position ranges)
+    uint32_t wsel = 0, weq = 0;
+#pragma unroll
+    for (int j = 0; j < KPT; ++j) {
+        const bool v = !isnan(x[j]);
+        const uint32_t key = v ? float_key(x[j]) : 0u;
+        wsel += __popc(__ballot_sync(0xffffffffu, v && key > T));
+        weq += __popc(__ballot_sync(0xffffffffu, v && key == T));
+    }
+    uint32_t tmp;
+    const uint32_t gt_w = warp_prefix(wsel, S.wcnt, &tmp);
+    const uint32_t eq_w = warp_prefix(weq, S.wcnt, &tmp);
+    // positions: kept before = (#> T before) + min(#== T before, krem) -- counted from
+    // the CTA start, then shifted by the lower CTAs' kept count.
+    uint32_t gt_run = gt_w, eq_run = eq_before + eq_w;
+    const uint32_t cta_gt_base = sel_before - min(eq_before, krem);  // lower CTAs' (> T) kept
+    int32_t* out = sel + (int64_t)row * k;
+    const uint32_t lt = lanemask_lt();
+#pragma unroll
+    for (int j = 0; j < KPT; ++j) {
+        const bool v = !isnan(x[j]);
+        const uint32_t key = v ? float_key(x[j]) : 0u;
+        const bool g = v && key > T, e = v && key == T;
+        const uint32_t mg = __ballot_sync(0xffffffffu, g);
+        const uint32_t me = __ballot_sync(0xffffffffu, e);
+        const uint32_t my_gt = cta_gt_base + gt_run + __popc(mg & lt);
+        const uint32_t my_eq = eq_run + __popc(me & lt);
+        if (g || (e && my_eq < krem)) out[my_gt + min(my_eq, krem)] = s0 + wbase + 32 * j + lane;
+        gt_run += __popc(mg);
+        eq_run += __popc(me);
+    }
+    cluster.sync();  // keep exchanged smem alive until every CTA is done reading
+}
+
+// Long rows (> 8 * 256 * 64 keys): the original smem-radix kernel streaming keys
+// from global memory each pass (correct for any length; not the fast path).
+__global__ void __launch_bounds__(1024, 1)
+    topk_stream_kernel(const float* __restrict__ scores, int tokens, int64_t ld, int k, int slice,
+                       int32_t* __restrict__ sel) {
+    cg::cluster_group cluster = cg::this_cluster();
+    const int nct = (int)cluster.num_blocks();
+    const int rank = (int)cluster.block_rank();
+    const int row = blockIdx.y;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const float* srow = scores + (int64_t)row * ld;
+    const int s0 = rank * slice;
+    const int cnt = max(0, min(s0 + slice, tokens) - s0);
+    __shared__ uint32_t hist[2][kTkRadixBins];
+    __shared__ uint32_t tot[kTkRadixBins];
+    __shared__ uint32_t misc[160];
+    uint32_t prefix = 0, pmask = 0, krem = (uint32_t)k;
 #pragma unroll 1
     for (int pass = 0; pass < 3; ++pass) {
         const int shift = pass == 0 ? 21 : (pass == 1 ? 10 : 0);
         const int bins = pass == 2 ? 1024 : 2048;
-        uint32_t* hist = (pass & 1) ? hist1 : hist0;
-        for (int i = tid; i < bins; i += kTkThreads) hist[i] = 0;
+        uint32_t* h = hist[pass & 1];
+        for (int i = tid; i < bins; i += 1024) h[i] = 0;
         __syncthreads();
-        for (int i = tid; i < cnt; i += kTkThreads) {
-            uint32_t key;
-            if (CACHED && pass > 0) {
-                key = keys[i];
-            } else {
-                key = float_key(srow[s0 + i]);
-                if (CACHED) keys[i] = key;
-            }
-            if ((key & pmask) == prefix) atomicAdd(&hist[(key >> shift) & (bins - 1)], 1u);
+        for (int i = tid; i < cnt; i += 1024) {
+            const uint32_t key = float_key(srow[s0 + i]);
+            if ((key & pmask) == prefix) atomicAdd(&h[(key >> shift) & (bins - 1)], 1u);
         }
         cluster.sync();
-        for (int i = tid; i < bins; i += kTkThreads) {
-            uint32_t acc = 0;
-            for (int r = 0; r < nct; ++r) acc += cluster.map_shared_rank(hist, r)[i];
-            tot[i] = acc;
+        for (int i = tid; i < bins; i += 1024) {
+            uint32_t a = 0;
+            for (int r = 0; r < nct; ++r) a += cluster.map_shared_rank(h, r)[i];
+            tot[i] = a;
         }
         __syncthreads();
-        // Digit search, descending: thread t owns descending positions
-        // [t*per, (t+1)*per).  Find the bin where the running count from the
-        // top first reaches krem.
-        const int per = bins / kTkThreads;
-        uint32_t local = 0;
-        for (int j = 0; j < per; ++j) local += tot[bins - 1 - (tid * per + j)];
-        uint32_t total;
-        uint32_t above = block_excl_scan(local, misc, &total);
-        for (int j = 0; j < per; ++j) {
-            const int bin = bins - 1 - (tid * per + j);
-            const uint32_t c = tot[bin];
-            if (above < krem && krem <= above + c) {
-                misc[64] = (uint32_t)bin;
-                misc[65] = above;
+        if (warp == 0) {
+            const int per = bins / 32;
+            uint32_t loc = 0;
+            for (int j = 0; j < per; ++j) loc += tot[bins - 1 - (lane * per + j)];
+            uint32_t inc = loc;
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+                if (lane >= o) inc += y;
             }
-            above += c;
+            uint32_t ab = inc - loc;
+            for (int j = 0; j < per; ++j) {
+                const int bin = bins - 1 - (lane * per + j);
+                const uint32_t c = tot[bin];
+                if (ab < krem && krem <= ab + c) {
+                    misc[64] = (uint32_t)bin;
+                    misc[65] = ab;
+                }
+                ab += c;
+            }
         }
         __syncthreads();
-        const uint32_t bin = misc[64];
         krem -= misc[65];
-        prefix |= bin << shift;
+        prefix |= misc[64] << shift;
         pmask |= (uint32_t)(bins - 1) << shift;
         __syncthreads();
     }
-    const uint32_t T = prefix;  // exact threshold key; keep krem keys equal to T
-
-    // ---- compaction in index order ----
-    // warp w owns [w*per_w, min((w+1)*per_w, cnt)), per_w a multiple of 32
+    const uint32_t T = prefix;
     const int per_w = (int)(((cnt + 32 * 32 - 1) / (32 * 32)) * 32);
     const int w0 = warp * per_w, w1 = min(w0 + per_w, cnt);
     uint32_t gt = 0, eq = 0;
     for (int base = w0; base < w1; base += 32) {
         const int i = base + lane;
-        uint32_t key = 0;
-        if (i < w1) key = CACHED ? keys[i] : float_key(srow[s0 + i]);
+        const uint32_t key = i < w1 ? float_key(srow[s0 + i]) : 0u;
         gt += __popc(__ballot_sync(0xffffffffu, key > T));
         eq += __popc(__ballot_sync(0xffffffffu, key == T));
     }
-    uint32_t* wgt = misc + 72;        // [32]
-    uint32_t* weq = misc + 72 + 32;   // [32]
+    uint32_t* wgt = misc + 72;
+    uint32_t* weq = misc + 104;
     if (lane == 0) {
         wgt[warp] = gt;
         weq[warp] = eq;
     }
     __syncthreads();
     if (warp == 0) {
-        uint32_t a = wgt[lane], e = weq[lane];
+        const uint32_t a = wgt[lane], e = weq[lane];
         uint32_t ia = a, ie = e;
-#pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
             const uint32_t ya = __shfl_up_sync(0xffffffffu, ia, o);
             const uint32_t ye = __shfl_up_sync(0xffffffffu, ie, o);
@@ -163,11 +532,11 @@ __global__ void __launch_bounds__(kTkThreads, 1)
                 ie += ye;
             }
         }
-        wgt[lane] = ia - a;  // exclusive
+        wgt[lane] = ia - a;
         weq[lane] = ie - e;
         if (lane == 31) {
-            misc[66] = ia;  // CTA total > T
-            misc[67] = ie;  // CTA total == T
+            misc[66] = ia;
+            misc[67] = ie;
         }
     }
     cluster.sync();
@@ -183,8 +552,7 @@ __global__ void __launch_bounds__(kTkThreads, 1)
     const uint32_t lower = (1u << lane) - 1u;
     for (int base = w0; base < w1; base += 32) {
         const int i = base + lane;
-        uint32_t key = 0;
-        if (i < w1) key = CACHED ? keys[i] : float_key(srow[s0 + i]);
+        const uint32_t key = i < w1 ? float_key(srow[s0 + i]) : 0u;
         const bool g = key > T, e = key == T;
         const uint32_t mg = __ballot_sync(0xffffffffu, g);
         const uint32_t me = __ballot_sync(0xffffffffu, e);
@@ -194,26 +562,7 @@ __global__ void __launch_bounds__(kTkThreads, 1)
         gt_before += __popc(mg);
         eq_before += __popc(me);
     }
-    cluster.sync();  // keep misc alive until every CTA has read it
-}
-
-struct TopkPlan {
-    int cluster;
-    int slice;
-    bool cached;
-    size_t smem;
-};
-
-static TopkPlan plan_topk(int rows, int tokens) {
-    TopkPlan p;
-    int c = 1;
-    while (c < 8 && ((int64_t)rows * c < 2 * 148 || ceil_div(tokens, c) > kTkMaxCached)) c *= 2;
-    while (c > 1 && tokens / c < 2048) c /= 2;
-    p.cluster = c;
-    p.slice = (int)(ceil_div(ceil_div(tokens, c), 32) * 32);
-    p.cached = p.slice <= kTkMaxCached;
-    p.smem = (size_t)(3 * kTkBins + kTkMisc) * 4 + (p.cached ? (size_t)p.slice * 4 : 0);
-    return p;
+    cluster.sync();
 }
 
 size_t topk_workspace(int rows, int tokens, int k) {
@@ -223,34 +572,52 @@ size_t topk_workspace(int rows, int tokens, int k) {
     return 0;
 }
 
-template <bool CACHED>
-static int launch_topk_impl(const TopkPlan& p, const float* scores, int rows, int tokens,
-                            int64_t ld, int k, int32_t* sel, cudaStream_t st) {
-    auto kern = topk_kernel<CACHED>;
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem);
-    if (e != cudaSuccess) return fail(FIER_ECUDA, std::string("fier_topk: ") + cudaGetErrorString(e));
+template <typename Kern, typename... Args>
+static int launch_cluster(Kern kern, int cluster, int rows, int threads, size_t smem, cudaStream_t st,
+                          Args... args) {
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return fail(FIER_ECUDA, std::string("fier_topk: ") + cudaGetErrorString(e));
+    }
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(p.cluster, rows, 1);
-    cfg.blockDim = dim3(kTkThreads, 1, 1);
-    cfg.dynamicSmemBytes = p.smem;
+    cfg.gridDim = dim3(cluster, rows, 1);
+    cfg.blockDim = dim3(threads, 1, 1);
+    cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = p.cluster;
+    attr[0].val.clusterDim.x = cluster;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    e = cudaLaunchKernelEx(&cfg, kern, scores, tokens, ld, k, p.slice, sel);
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, args...);
     if (e != cudaSuccess) return fail(FIER_ECUDA, std::string("fier_topk: ") + cudaGetErrorString(e));
     return FIER_OK;
 }
 
 int topk_dispatch(const float* scores, int rows, int tokens, int64_t ld, int k, int32_t* sel,
                   cudaStream_t st) {
-    const TopkPlan p = plan_topk(rows, tokens);
-    if (p.cached) return launch_topk_impl<true>(p, scores, rows, tokens, ld, k, sel, st);
-    return launch_topk_impl<false>(p, scores, rows, tokens, ld, k, sel, st);
+    // cluster size: enough CTAs to fill the chip, every slice <= 256 * 64 keys
+    int c = 1;
+    while (c < kTkMaxCluster && ((int64_t)rows * c < 2 * 148 || ceil_div(tokens, c) > kTkThreads * 64)) c *= 2;
+    while (c > 1 && ceil_div(tokens, c) < kTkThreads * 4) c /= 2;
+    const int64_t slice = ceil_div(tokens, c);
+    const size_t smem = sizeof(TopkShared);
+    if (slice <= kTkThreads * 64) {
+        int kpt = 4;
+        while ((int64_t)kTkThreads * kpt < slice) kpt *= 2;
+        const int sl = kTkThreads * kpt;
+        switch (kpt) {
+            case 4: return launch_cluster(topk_kernel<4>, c, rows, kTkThreads, smem, st, scores, tokens, ld, k, sl, sel);
+            case 8: return launch_cluster(topk_kernel<8>, c, rows, kTkThreads, smem, st, scores, tokens, ld, k, sl, sel);
+            case 16: return launch_cluster(topk_kernel<16>, c, rows, kTkThreads, smem, st, scores, tokens, ld, k, sl, sel);
+            case 32: return launch_cluster(topk_kernel<32>, c, rows, kTkThreads, smem, st, scores, tokens, ld, k, sl, sel);
+            default: return launch_cluster(topk_kernel<64>, c, rows, kTkThreads, smem, st, scores, tokens, ld, k, sl, sel);
+        }
+    }
+    const int sl = (int)(ceil_div(slice, 32) * 32);
+    return launch_cluster(topk_stream_kernel, c, rows, 1024, 0, st, scores, tokens, ld, k, sl, sel);
 }
 
 }  // namespace fier_cuda
