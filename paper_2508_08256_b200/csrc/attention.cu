@@ -106,10 +106,11 @@ __device__ void merge_partials(const float* part, int nsplit, int heads, float* 
     }
 }
 
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, uint64_t policy) {
-    asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(smem_u32(smem)),
-                 "l"(gmem), "l"(policy)
-                 : "memory");
+// (The .L2::cache_hint form of this instruction was miscompiled by ptxas 12.9 for
+// sm_100a in one instantiation -- an odd uniform register as the 64-bit policy
+// descriptor, trapping as an illegal instruction -- so no hint is used.)
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
@@ -176,7 +177,6 @@ __global__ void __launch_bounds__(kAttnWarps * 32) attn_kernel(
 
     uint8_t* wring = ring + (size_t)warp * NST * 2 * TR::STAGE_BYTES;
     float* wp = pbuf + warp * HPG * kRowsPerStage;
-    const uint64_t pol = policy_evict_first();
 
     auto issue = [&](int st) {  // copy stage st into ring slot st % NST (one commit group)
         if (st < nstages) {
@@ -199,8 +199,8 @@ __global__ void __launch_bounds__(kAttnWarps * 32) attn_kernel(
                     t = r0 + rr;
                 }
                 if (rr < nr) {
-                    cp_async16(kdst + rr * RB + off * 16, Kseq + (int64_t)t * D + off * (16 / sizeof(T)), pol);
-                    cp_async16(vdst + rr * RB + off * 16, Vseq + (int64_t)t * D + off * (16 / sizeof(T)), pol);
+                    cp_async16(kdst + rr * RB + off * 16, Kseq + (int64_t)t * D + off * (16 / sizeof(T)));
+                    cp_async16(vdst + rr * RB + off * 16, Vseq + (int64_t)t * D + off * (16 / sizeof(T)));
                 }
             }
         }
@@ -410,10 +410,10 @@ struct AttnPlan {
     int rows_per_cta;
 };
 
-static AttnPlan plan_split(int64_t units, int total_rows, int min_rows) {
-    // ~2 resident CTAs (16 warps) per SM, one wave
-    const int64_t target = 148 * 2;
-    int64_t ns = (target + units - 1) / units;
+// Split rows so the whole grid is one wave of resident CTAs (per_sm per SM).
+static AttnPlan plan_split(int64_t units, int total_rows, int min_rows, int per_sm) {
+    const int64_t target = (int64_t)per_sm * num_sms();
+    int64_t ns = target / units;
     if (ns < 1) ns = 1;
     int rpc = (int)ceil_div(total_rows, ns);
     rpc = (int)ceil_div(rpc, 32) * 32;
@@ -478,8 +478,44 @@ static bool fast_hpg(const fier_shape* s) {
 
 constexpr int kMaxSplit = 256;  // the merging CTA keeps 2*nsplit floats in its smem
 
+template <typename T, int D, int HPG, bool GATHER>
+static int attn_per_sm() {
+    static const int v = [] {
+        auto kern = attn_kernel<T, D, HPG, GATHER, attn_nst<T, D>()>;
+        const size_t smem = attn_smem<T, D, HPG, GATHER>();
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        return ctas_per_sm(kern, kAttnWarps * 32, smem);
+    }();
+    return v;
+}
+
+template <typename T>
+static int per_sm_typed(const fier_shape* s, bool gather) {
+    const int hpg = s->q_heads / s->kv_heads;
+    if (s->dim == 128) {
+        if (gather) return attn_per_sm<T, 128, 1, true>();
+        return hpg == 1 ? attn_per_sm<T, 128, 1, false>() : hpg == 2 ? attn_per_sm<T, 128, 2, false>()
+             : hpg == 4 ? attn_per_sm<T, 128, 4, false>() : attn_per_sm<T, 128, 8, false>();
+    }
+    if (s->dim == 64) {
+        if (gather) return attn_per_sm<T, 64, 1, true>();
+        return hpg == 1 ? attn_per_sm<T, 64, 1, false>() : hpg == 2 ? attn_per_sm<T, 64, 2, false>()
+             : hpg == 4 ? attn_per_sm<T, 64, 4, false>() : attn_per_sm<T, 64, 8, false>();
+    }
+    return 8;  // generic one-warp kernel
+}
+
+static int resident_per_sm(const fier_shape* s, bool gather) {
+    // occupancy needs the opt-in smem limit set on the kernel first
+    switch (s->dtype) {
+        case FIER_F32: return per_sm_typed<float>(s, gather);
+        case FIER_F16: return per_sm_typed<__half>(s, gather);
+        default: return per_sm_typed<__nv_bfloat16>(s, gather);
+    }
+}
+
 AttnPlan sparse_plan(const fier_shape* s, int n) {
-    AttnPlan p = plan_split((int64_t)s->batch * s->q_heads, n, 64);
+    AttnPlan p = plan_split((int64_t)s->batch * s->q_heads, n, 64, resident_per_sm(s, true));
     if (p.nsplit > kMaxSplit) {
         p.rows_per_cta = (int)ceil_div(ceil_div(n, kMaxSplit), 32) * 32;
         p.nsplit = (int)ceil_div(n, p.rows_per_cta);
@@ -490,7 +526,7 @@ AttnPlan sparse_plan(const fier_shape* s, int n) {
 AttnPlan full_plan(const fier_shape* s, int tokens) {
     const bool fast = fast_dim(s) && fast_hpg(s);
     const int64_t units = fast ? (int64_t)s->batch * s->kv_heads : (int64_t)s->batch * s->q_heads;
-    AttnPlan p = plan_split(units, tokens, 256);
+    AttnPlan p = plan_split(units, tokens, 256, resident_per_sm(s, false));
     if (p.nsplit > kMaxSplit) {
         p.rows_per_cta = (int)ceil_div(ceil_div(tokens, kMaxSplit), 32) * 32;
         p.nsplit = (int)ceil_div(tokens, p.rows_per_cta);

@@ -38,6 +38,8 @@ int sparse_dispatch(const fier_shape*, const void*, const void*, const void*, co
 int full_dispatch(const fier_shape*, const void*, const void*, const void*, int, float, float*, void*,
                   cudaStream_t);
 size_t sparse_counter_offset(const fier_shape*, int);
+int append_score_dispatch(const fier_shape*, const void*, void*, void*, const void*, const void*, int,
+                          uint32_t*, void*, float*, int64_t, int*, int, cudaStream_t);
 
 static int check_shape(const fier_shape* s, const char* fn) {
     const std::string f(fn);
@@ -187,10 +189,8 @@ int fier_decode_step(const fier_shape* s, const void* q, const void* k_new, cons
     float* scores = scores_out ? scores_out : reinterpret_cast<float*>(ws);
     uint8_t* attn_ws = ws + align_up((size_t)s->batch * s->q_heads * ld * sizeof(float));
     int* counters = reinterpret_cast<int*>(attn_ws + sparse_counter_offset(s, n));
-    int rc = append_dispatch(s, K, V, k_new, v_new, pos, bits, params, nullptr, counters,
-                             s->batch * s->q_heads, st);
-    if (rc) return rc;
-    rc = score_dispatch(s, q, bits, params, tokens, scores, ld, st);
+    int rc = append_score_dispatch(s, q, K, V, k_new, v_new, pos, bits, params, scores, ld, counters,
+                                   s->batch * s->q_heads, st);
     if (rc) return rc;
     rc = topk_dispatch(scores, s->batch * s->q_heads, tokens, ld, n, sel, st);
     if (rc) return rc;

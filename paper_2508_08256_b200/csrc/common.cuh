@@ -151,4 +151,23 @@ constexpr float kLog2e = 1.4426950408889634f;
 
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
+inline int num_sms() {
+    static int n = [] {
+        int dev = 0, v = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+        return v;
+    }();
+    return n;
+}
+
+// Resident CTAs of `kern` per SM at this block size / dynamic smem (cached per call site).
+template <typename Kern>
+inline int ctas_per_sm(Kern kern, int threads, size_t smem) {
+    int occ = 1;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem) != cudaSuccess || occ < 1)
+        occ = 1;
+    return occ;
+}
+
 }  // namespace fier_cuda

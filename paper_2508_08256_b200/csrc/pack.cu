@@ -12,76 +12,12 @@
 //     per (token, 32 channels).
 // The append variant first writes the new k/v row (the KV-cache update that
 // precedes scoring in a decode step), then re-packs only the open group.
-#include "common.cuh"
+#include "pack.cuh"
 
 namespace fier_cuda {
 
-// Values of one 32-token chunk of this lane's channel, loaded together (one
-// memory latency per chunk instead of one per token).  bf16/fp16/fp32 are
-// exact in fp32; they are widened to fp64 for the arithmetic below.
 template <typename T>
-__device__ __forceinline__ void load_chunk(const T* Kseq, int d, int c, bool valid,
-                                           int tc, int cnt, float (&v)[32]) {
-#pragma unroll
-    for (int i = 0; i < 32; ++i)
-        v[i] = (valid && i < cnt) ? to_f32(Kseq[(int64_t)(tc + i) * d + c]) : 0.f;
-}
-
-template <typename T>
-__device__ __forceinline__ void pack_group(const T* Kseq,  // no restrict: append re-reads its own store
-                                           int d, int W, int g, int gi,
-                                           int t_end, uint32_t* __restrict__ bits_seq,
-                                           __half2* __restrict__ sz_seq, int32_t* nonfinite) {
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int c = warp * 32 + lane;
-    const bool valid = c < d;
-    const int t0 = gi * g;
-    const int t1 = min(t0 + g, t_end);  // short final group (quant1bit.hpp:84)
-    float v[32];
-    double mn = 0.0, mx = 0.0;
-    bool bad = false;
-    // pass 1: min/max in token order, first seen wins ties (std::min/std::max)
-    for (int tc = t0; tc < t1; tc += 32) {
-        const int cnt = min(32, t1 - tc);
-        load_chunk<T>(Kseq, d, c, valid, tc, cnt, v);
-#pragma unroll
-        for (int i = 0; i < 32; ++i) {
-            if (i < cnt) {
-                const double x = (double)v[i];
-                bad |= !isfinite(x);
-                if (tc == t0 && i == 0) {
-                    mn = mx = x;
-                } else {
-                    mn = (x < mn) ? x : mn;
-                    mx = (mx < x) ? x : mx;
-                }
-            }
-        }
-    }
-    const double z = (mx + mn) / 2.0;
-    const double s = (mx - mn) / 2.0;
-    if (valid) sz_seq[(int64_t)gi * d + c] = __halves2half2(__double2half(s), __double2half(z));
-    if (bad && nonfinite) atomicExch(nonfinite, 1);
-    // pass 2: one ballot per token -> the word of (token, 32 channels); for
-    // g <= 32 the chunk is still in registers.
-    for (int tc = t0; tc < t1; tc += 32) {
-        const int cnt = min(32, t1 - tc);
-        if (g > 32) load_chunk<T>(Kseq, d, c, valid, tc, cnt, v);
-        uint32_t mine = 0;
-#pragma unroll
-        for (int i = 0; i < 32; ++i) {
-            if (i < cnt) {
-                const bool bit = valid && ((s == 0.0) || ((double)v[i] >= z));
-                const uint32_t word = __ballot_sync(0xffffffffu, bit);
-                if (lane == i) mine = word;
-            }
-        }
-        if (lane < cnt) bits_seq[(int64_t)(tc + lane) * W + warp] = mine;
-    }
-}
-
-template <typename T>
-__global__ void __launch_bounds__(1024) pack_kernel(const T* __restrict__ K, int cap, int d, int W,
+__global__ void __launch_bounds__(kPackThreads) pack_kernel(const T* __restrict__ K, int cap, int d, int W,
                                                      int g, int G, int tokens, int hkv,
                                                      uint32_t* __restrict__ bits,
                                                      __half2* __restrict__ sz, int32_t* nonfinite) {
@@ -92,7 +28,7 @@ __global__ void __launch_bounds__(1024) pack_kernel(const T* __restrict__ K, int
 }
 
 template <typename T>
-__global__ void __launch_bounds__(1024) append_kernel(T* __restrict__ K, T* __restrict__ V,
+__global__ void __launch_bounds__(kPackThreads) append_kernel(T* __restrict__ K, T* __restrict__ V,
                                                        const T* __restrict__ k_new,
                                                        const T* __restrict__ v_new, int pos, int cap,
                                                        int d, int W, int g, int G, int hkv,
@@ -109,9 +45,9 @@ __global__ void __launch_bounds__(1024) append_kernel(T* __restrict__ K, T* __re
             if (j < zero_n) zero_words[j] = 0;
         }
     }
-    const int c = threadIdx.x;
-    if (c < d) {
-        // Same thread writes then re-reads channel c below: program order suffices.
+    // Thread c writes channel c and is the lane that re-reads it below (warp
+    // (c/32) % 4 owns slice c/32): program order suffices.
+    for (int c = threadIdx.x; c < d; c += blockDim.x) {
         Kseq[(int64_t)pos * d + c] = k_new[seq * d + c];
         V[seq * cap * d + (int64_t)pos * d + c] = v_new[seq * d + c];
     }
@@ -126,7 +62,7 @@ static int launch_pack(const fier_shape* s, const void* K, int32_t tokens, uint3
     const int G = (int)ceil_div(s->capacity, s->group);
     const int groups = (int)ceil_div(tokens, s->group);
     dim3 grid(groups, s->kv_heads, s->batch);
-    pack_kernel<T><<<grid, 32 * W, 0, st>>>(static_cast<const T*>(K), s->capacity, s->dim, W,
+    pack_kernel<T><<<grid, min(32 * W, kPackThreads), 0, st>>>(static_cast<const T*>(K), s->capacity, s->dim, W,
                                             s->group, G, tokens, s->kv_heads, bits,
                                             static_cast<__half2*>(params), nonfinite);
     return check_launch("fier_pack_keys");
@@ -139,7 +75,7 @@ static int launch_append(const fier_shape* s, void* K, void* V, const void* k_ne
     const int W = (s->dim + 31) / 32;
     const int G = (int)ceil_div(s->capacity, s->group);
     dim3 grid(1, s->kv_heads, s->batch);
-    append_kernel<T><<<grid, 32 * W, 0, st>>>(static_cast<T*>(K), static_cast<T*>(V),
+    append_kernel<T><<<grid, min(32 * W, kPackThreads), 0, st>>>(static_cast<T*>(K), static_cast<T*>(V),
                                               static_cast<const T*>(k_new),
                                               static_cast<const T*>(v_new), pos, s->capacity,
                                               s->dim, W, s->group, G, s->kv_heads, bits,

@@ -1,0 +1,82 @@
+// pack.cuh -- the 1-bit group packer shared by K1 (pack.cu) and the fused
+// append+score launch (score.cu).  See pack.cu for the reference mapping.
+#pragma once
+
+#include "common.cuh"
+
+namespace fier_cuda {
+
+constexpr int kPackThreads = 128;  // 4 warps; warp w packs channel slices w, w+4, ...
+
+// Values of one 32-token chunk of this lane's channel, loaded together (one
+// memory latency per chunk instead of one per token).  bf16/fp16/fp32 are
+// exact in fp32; they are widened to fp64 for the arithmetic below.
+template <typename T>
+__device__ __forceinline__ void load_chunk(const T* Kseq, int d, int c, bool valid,
+                                           int tc, int cnt, float (&v)[32]) {
+#pragma unroll
+    for (int i = 0; i < 32; ++i)
+        v[i] = (valid && i < cnt) ? to_f32(Kseq[(int64_t)(tc + i) * d + c]) : 0.f;
+}
+
+template <typename T>
+__device__ __forceinline__ void pack_group(const T* Kseq,  // no restrict: append re-reads its own store
+                                           int d, int W, int g, int gi,
+                                           int t_end, uint32_t* __restrict__ bits_seq,
+                                           __half2* __restrict__ sz_seq, int32_t* nonfinite) {
+    const int lane = threadIdx.x & 31;
+    for (int warp = threadIdx.x >> 5; warp < W; warp += blockDim.x >> 5) {
+    const int c = warp * 32 + lane;
+    const bool valid = c < d;
+    const int t0 = gi * g;
+    const int t1 = min(t0 + g, t_end);  // short final group (quant1bit.hpp:84)
+    float v[32];
+    // min/max on the exact fp32 values (== their fp64 widenings), sequential with
+    // std::min/std::max semantics: a tie keeps the first-seen value (+0 vs -0).
+    float mn = 0.f, mx = 0.f;
+    bool bad = false;
+    for (int tc = t0; tc < t1; tc += 32) {
+        const int cnt = min(32, t1 - tc);
+        load_chunk<T>(Kseq, d, c, valid, tc, cnt, v);
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+            if (i < cnt) {
+                const float x = v[i];
+                bad |= !isfinite(x);
+                if (tc == t0 && i == 0) {
+                    mn = mx = x;
+                } else {
+                    mn = (x < mn) ? x : mn;
+                    mx = (mx < x) ? x : mx;
+                }
+            }
+        }
+    }
+    // z, s in fp64 exactly as the reference (quant1bit.hpp:90-93)
+    const double z = ((double)mx + (double)mn) / 2.0;
+    const double s = ((double)mx - (double)mn) / 2.0;
+    if (valid) sz_seq[(int64_t)gi * d + c] = __halves2half2(__double2half(s), __double2half(z));
+    if (bad && nonfinite) atomicExch(nonfinite, 1);
+    // x >= z (fp64) <=> x >= zc for fp32 x, zc = the smallest float >= z.
+    float zc = __double2float_rn(z);
+    if ((double)zc < z) zc = nextafterf(zc, INFINITY);
+    const bool all_one = (s == 0.0);
+    // pass 2: one ballot per token -> the word of (token, 32 channels); for
+    // g <= 32 the chunk is still in registers.
+    for (int tc = t0; tc < t1; tc += 32) {
+        const int cnt = min(32, t1 - tc);
+        if (g > 32) load_chunk<T>(Kseq, d, c, valid, tc, cnt, v);
+        uint32_t mine = 0;
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+            if (i < cnt) {
+                const uint32_t word = __ballot_sync(0xffffffffu, valid && (all_one || v[i] >= zc));
+                if (lane == i) mine = word;
+            }
+        }
+        if (lane < cnt) bits_seq[(int64_t)(tc + lane) * W + warp] = mine;
+    }
+    }  // channel slices
+}
+
+}  // namespace fier_cuda

@@ -3,13 +3,13 @@
 // Replaces topk_oracle (reference core.hpp:134-148): the k largest scores,
 // ties to the LOWER index, returned in ascending index order.
 //
-// One thread-block cluster (C <= 8 CTAs of 256 threads) per score row; CTA r
-// owns the contiguous slice [r*S, (r+1)*S) and keeps its keys in registers
-// (KPT per thread, slot j of lane L of warp w = position w*32*KPT + 32j + L).
-// Shared-memory atomics cost ~2 cycles per lane on this part, so histograms
-// are counted WITHOUT atomics: per 32-key slot a warp "multisplit" (6 ballots
-// give every lane the mask of lanes sharing its bin; the lowest such lane adds
-// the popcount into the warp's private smem row).
+// One thread-block cluster (C <= 8 CTAs of 512 or 256 threads) per score row;
+// CTA r owns the contiguous slice [r*S, (r+1)*S) and keeps its keys in
+// registers (KPT per thread, slot j of lane L of warp w = position
+// w*32*KPT + 32j + L).  Shared-memory atomics cost ~2 cycles per lane on this
+// part, so histograms are counted WITHOUT atomics: per 32-key slot a warp
+// multisplit (__match_any_sync gives every lane the mask of lanes sharing its
+// bin; the lowest such lane adds the popcount into the warp's private smem row).
 //
 //   1. (lo, hi) = min/max of the finite scores of the row (cluster exchange).
 //   2. 32 linear bins over [lo, hi] -> bin b1 holding the k-th largest.
@@ -33,32 +33,30 @@ namespace cg = cooperative_groups;
 
 namespace fier_cuda {
 
-constexpr int kTkThreads = 256;
-constexpr int kTkWarps = kTkThreads / 32;
+constexpr int kTkMaxWarps = 16;
 constexpr int kTkMaxCluster = 8;
-constexpr int kTkCandCta = 512;   // candidates one CTA may contribute
-constexpr int kTkCandAll = 1024;  // candidates a cluster may rank (fast path)
+constexpr int kTkCandCta = 256;   // candidates one CTA may contribute (fast path)
 constexpr int kTkRadixBins = 2048;
 
 struct TopkShared {
-    // exchanged over DSMEM (read by other CTAs after a cluster barrier)
-    float mm[2];                  // local min, max of finite values
-    uint32_t h1[32];              // CTA histogram, pass 1
-    uint32_t h2[32];              // CTA histogram, pass 2
-    uint32_t ncand, nabove;       // candidates / strictly-above count of this CTA
-    uint32_t cand_key[kTkCandCta];
-    int32_t cand_idx[kTkCandCta];
-    uint32_t rhist[2][kTkRadixBins];  // fallback radix histograms
-    uint32_t rsel[2];             // fallback: CTA counts (> T, == T)
-    // CTA-private
-    uint32_t wh[kTkWarps][32];    // per-warp histogram rows
-    uint32_t all_key[kTkCandAll];
-    int32_t all_idx[kTkCandAll];
-    uint32_t all_cta[kTkCandAll];
+    // pushed by every CTA of the cluster into every CTA (slot = sender's rank),
+    // then read locally after one cluster barrier
+    float mm[kTkMaxCluster][2];               // min, max of finite values
+    uint32_t h1[kTkMaxCluster][32];           // pass-1 histograms
+    uint32_t h2[kTkMaxCluster][32];           // pass-2 histograms
+    uint32_t ncand[kTkMaxCluster];            // candidates per CTA
+    uint32_t nabove[kTkMaxCluster];           // strictly-above count per CTA
+    uint32_t ckey[kTkMaxCluster][kTkCandCta];  // candidate keys
+    int32_t cidx[kTkMaxCluster][kTkCandCta];   // candidate global indices
+    // fallback radix path (pulled over DSMEM; rare)
+    uint32_t rhist[2][kTkRadixBins];
+    uint32_t rsel[2];
     uint32_t tot[kTkRadixBins];
-    uint32_t scratch[64];
-    uint32_t wcnt[kTkWarps];
-    float fscratch[2 * kTkWarps];
+    // CTA-private
+    uint32_t wh[kTkMaxWarps][32];             // per-warp histogram rows
+    uint32_t wcnt[kTkMaxWarps];
+    float fscratch[2 * kTkMaxWarps];
+    uint32_t lcand;                           // local candidate counter
     uint32_t res[8];
 };
 
@@ -68,15 +66,11 @@ __device__ __forceinline__ uint32_t lanemask_lt() {
     return m;
 }
 
-// Warp multisplit of a bin id in [0, 64): adds each bin's lane count into row[bin]
-// (bins >= 32 are ignored).  No atomics: one leader lane per distinct bin.
+// Warp multisplit of a bin id: adds each bin's lane count into row[bin] (bins
+// >= 32 are ignored).  No atomics: __match_any_sync gives every lane the mask
+// of lanes sharing its bin; the lowest lane of each group does a plain RMW.
 __device__ __forceinline__ void warp_count_bins(uint32_t bin, uint32_t* row) {
-    uint32_t peers = 0xffffffffu;
-#pragma unroll
-    for (int bit = 0; bit < 6; ++bit) {
-        const uint32_t m = __ballot_sync(0xffffffffu, (bin >> bit) & 1u);
-        peers &= ((bin >> bit) & 1u) ? m : ~m;
-    }
+    const uint32_t peers = __match_any_sync(0xffffffffu, bin);
     if (bin < 32 && (peers & lanemask_lt()) == 0) row[bin] += __popc(peers);
 }
 
@@ -110,6 +104,7 @@ __device__ __forceinline__ int lin_bin(float x, float lo, float inv) {
 
 // Block-wide exclusive scan over warps of one value per warp (lane 0 holds it);
 // returns the warp's exclusive prefix in all lanes and the block total.
+template <int kTkWarps>
 __device__ __forceinline__ uint32_t warp_prefix(uint32_t v, uint32_t* wcnt, uint32_t* total) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     if (lane == 0) wcnt[warp] = v;
@@ -126,10 +121,11 @@ __device__ __forceinline__ uint32_t warp_prefix(uint32_t v, uint32_t* wcnt, uint
     return ex;
 }
 
-template <int KPT>
+template <int KPT, int kTkThreads>
 __global__ void __launch_bounds__(kTkThreads) topk_kernel(const float* __restrict__ scores, int tokens,
                                                           int64_t ld, int k, int slice,
                                                           int32_t* __restrict__ sel) {
+    constexpr int kTkWarps = kTkThreads / 32;
     cg::cluster_group cluster = cg::this_cluster();
     const int nct = (int)cluster.num_blocks();
     const int rank = (int)cluster.block_rank();
@@ -141,6 +137,9 @@ __global__ void __launch_bounds__(kTkThreads) topk_kernel(const float* __restric
     extern __shared__ __align__(16) uint8_t smem_raw[];
     TopkShared& S = *reinterpret_cast<TopkShared*>(smem_raw);
 
+    // Every CTA of the cluster must have started before anyone writes into its
+    // shared memory: arrive now, wait just before the first remote store.
+    asm volatile("barrier.cluster.arrive.relaxed;" ::: "memory");
     // ---- load: slot j of this lane = position warp*32*KPT + 32j + lane ----
     const int wbase = warp * 32 * KPT;
     float x[KPT];
@@ -161,22 +160,24 @@ __global__ void __launch_bounds__(kTkThreads) topk_kernel(const float* __restric
         S.fscratch[warp] = mn;
         S.fscratch[kTkWarps + warp] = mx;
     }
+    if (tid == 0) S.lcand = 0;
     __syncthreads();
-    if (tid == 0) {
+    asm volatile("barrier.cluster.wait;" ::: "memory");
+    if (tid < nct) {  // push this CTA's (min, max) into slot [rank] of CTA tid
         float a = INFINITY, b = -INFINITY;
         for (int w = 0; w < kTkWarps; ++w) {
             a = fminf(a, S.fscratch[w]);
             b = fmaxf(b, S.fscratch[kTkWarps + w]);
         }
-        S.mm[0] = a;
-        S.mm[1] = b;
+        float* dst = cluster.map_shared_rank(&S.mm[rank][0], tid);
+        dst[0] = a;
+        dst[1] = b;
     }
     cluster.sync();  // #1
     float lo = INFINITY, hi = -INFINITY;
     for (int r = 0; r < nct; ++r) {
-        const float* m = cluster.map_shared_rank(S.mm, r);
-        lo = fminf(lo, m[0]);
-        hi = fmaxf(hi, m[1]);
+        lo = fminf(lo, S.mm[r][0]);
+        hi = fmaxf(hi, S.mm[r][1]);
     }
     if (!(lo <= hi)) {  // no finite values
         lo = 0.f;
@@ -184,152 +185,146 @@ __global__ void __launch_bounds__(kTkThreads) topk_kernel(const float* __restric
     }
     const float inv1 = hi > lo ? 32.f / (hi - lo) : 0.f;
 
-    // ---- pass 1: 32 bins over [lo, hi] ----
+    // ---- pass 1: 32 bins over [lo, hi]; code[j] caches the bin (63 = empty) ----
+    int code[KPT];
 #pragma unroll
     for (int j = 0; j < KPT; ++j) {
-        const bool v = !isnan(x[j]);
-        warp_count_bins(v ? (uint32_t)lin_bin(x[j], lo, inv1) : 63u, S.wh[warp]);
+        code[j] = isnan(x[j]) ? 63 : lin_bin(x[j], lo, inv1);
+        warp_count_bins((uint32_t)code[j], S.wh[warp]);
     }
     __syncthreads();
-    if (tid < 32) {
+    if (tid < 32 * nct) {  // push histogram bin (tid % 32) to CTA tid / 32
+        const int b = tid & 31;
         uint32_t c = 0;
-        for (int w = 0; w < kTkWarps; ++w) {
-            c += S.wh[w][tid];
-            S.wh[w][tid] = 0;
-        }
-        S.h1[tid] = c;
+        for (int w = 0; w < kTkWarps; ++w) c += S.wh[w][b];
+        *cluster.map_shared_rank(&S.h1[rank][b], tid >> 5) = c;
     }
+    __syncthreads();
+    for (int i = tid; i < kTkWarps * 32; i += kTkThreads) (&S.wh[0][0])[i] = 0;
     cluster.sync();  // #2
     uint32_t b1, above1, b2, above2;
     {
         uint32_t c = 0;
-        if (lane < 32)
-            for (int r = 0; r < nct; ++r) c += cluster.map_shared_rank(S.h1, r)[lane];
+        for (int r = 0; r < nct; ++r) c += S.h1[r][lane];
         find_bin32(c, (uint32_t)k, &b1, &above1);
     }
     // ---- pass 2: 32 sub-bins over bin b1 ----
     const float w1 = (hi - lo) / 32.f;
     const float lo2 = lo + (float)b1 * w1;
     const float inv2 = w1 > 0.f ? 32.f / w1 : 0.f;
-    auto bins12 = [&](float v, int* p1, int* p2) {
-        *p1 = lin_bin(v, lo, inv1);
-        *p2 = lin_bin(v, lo2, inv2);
-    };
+    // code[j] becomes: -1 below b1 (or empty), 64 above b1, else the sub-bin
 #pragma unroll
     for (int j = 0; j < KPT; ++j) {
-        int p1, p2;
-        bins12(x[j], &p1, &p2);
-        const bool in = !isnan(x[j]) && p1 == (int)b1;
-        warp_count_bins(in ? (uint32_t)p2 : 63u, S.wh[warp]);
+        const int c1 = code[j];
+        int c = c1 == 63 ? -1 : (c1 < (int)b1 ? -1 : (c1 > (int)b1 ? 64 : lin_bin(x[j], lo2, inv2)));
+        code[j] = c;
+        warp_count_bins(c >= 0 && c < 32 ? (uint32_t)c : 63u, S.wh[warp]);
     }
     __syncthreads();
-    if (tid < 32) {
+    if (tid < 32 * nct) {
+        const int b = tid & 31;
         uint32_t c = 0;
-        for (int w = 0; w < kTkWarps; ++w) c += S.wh[w][tid];
-        S.h2[tid] = c;
+        for (int w = 0; w < kTkWarps; ++w) c += S.wh[w][b];
+        *cluster.map_shared_rank(&S.h2[rank][b], tid >> 5) = c;
     }
-    if (tid == 0) S.ncand = 0;
     cluster.sync();  // #3
     {
         uint32_t c = 0;
-        for (int r = 0; r < nct; ++r) c += cluster.map_shared_rank(S.h2, r)[lane];
+        for (int r = 0; r < nct; ++r) c += S.h2[r][lane];
         find_bin32(c, (uint32_t)k - above1, &b2, &above2);
     }
     uint32_t krem = (uint32_t)k - above1 - above2;  // >= 1
 
-    // ---- candidates (b1, b2) and the strictly-above count of this CTA ----
-    auto cls = [&](float v) -> int {  // 2 = above, 1 = candidate, 0 = below/empty
-        if (isnan(v)) return 0;
-        int p1, p2;
-        bins12(v, &p1, &p2);
-        if (p1 != (int)b1) return p1 > (int)b1 ? 2 : 0;
-        if (p2 != (int)b2) return p2 > (int)b2 ? 2 : 0;
-        return 1;
-    };
+    // ---- candidates (b1, b2) pushed to every CTA; strictly-above counts ----
     uint32_t nab = 0;
 #pragma unroll
     for (int j = 0; j < KPT; ++j) {
-        const int c = cls(x[j]);
+        const int c = code[j] > (int)b2 ? 2 : (code[j] == (int)b2 ? 1 : 0);  // above / candidate / below
         nab += __popc(__ballot_sync(0xffffffffu, c == 2));
         const uint32_t m = __ballot_sync(0xffffffffu, c == 1);
         if (m) {
             uint32_t base = 0;
-            if (lane == __ffs(m) - 1) base = atomicAdd(&S.ncand, (uint32_t)__popc(m));
+            if (lane == __ffs(m) - 1) base = atomicAdd(&S.lcand, (uint32_t)__popc(m));
             base = __shfl_sync(0xffffffffu, base, __ffs(m) - 1);
             const uint32_t slot = base + __popc(m & lanemask_lt());
             if (c == 1 && slot < kTkCandCta) {
-                S.cand_key[slot] = float_key(x[j]);
-                S.cand_idx[slot] = s0 + wbase + 32 * j + lane;
+                const uint32_t key = float_key(x[j]);
+                const int32_t idx = s0 + wbase + 32 * j + lane;
+                for (int r = 0; r < nct; ++r) {
+                    *cluster.map_shared_rank(&S.ckey[rank][slot], r) = key;
+                    *cluster.map_shared_rank(&S.cidx[rank][slot], r) = idx;
+                }
             }
         }
     }
     uint32_t tot_ab;
-    warp_prefix(nab, S.wcnt, &tot_ab);
-    if (tid == 0) S.nabove = tot_ab;
-    cluster.sync();  // #4
+    warp_prefix<kTkWarps>(nab, S.wcnt, &tot_ab);  // (contains __syncthreads: lcand final)
+    if (tid < nct) {
+        *cluster.map_shared_rank(&S.ncand[rank], tid) = S.lcand;
+        *cluster.map_shared_rank(&S.nabove[rank], tid) = tot_ab;
+    }
+    cluster.sync();  // #4 -- after this, the fast path reads only local smem
     uint32_t ncand_all = 0, ncand_max = 0;
     for (int r = 0; r < nct; ++r) {
-        const uint32_t c = *cluster.map_shared_rank(&S.ncand, r);
-        ncand_all += c;
-        ncand_max = max(ncand_max, c);
+        ncand_all += S.ncand[r];
+        ncand_max = max(ncand_max, S.ncand[r]);
     }
 
     uint32_t T;                 // threshold key
     uint32_t sel_before = 0;    // kept elements in lower-ranked CTAs
     uint32_t eq_before = 0;     // T-valued keys in lower-ranked CTAs
-    bool radix = ncand_max > kTkCandCta || ncand_all > kTkCandAll;  // uniform
+    const bool radix = ncand_max > kTkCandCta;  // uniform over the cluster
     if (!radix) {
-        // gather every candidate (rank order of CTAs), rank by (key desc, idx asc)
-        uint32_t off = 0;
-        for (int r = 0; r < nct; ++r) {
-            const uint32_t c = *cluster.map_shared_rank(&S.ncand, r);
-            const uint32_t* rk = cluster.map_shared_rank(S.cand_key, r);
-            const int32_t* ri = cluster.map_shared_rank(S.cand_idx, r);
-            for (uint32_t i = tid; i < c; i += kTkThreads) {
-                S.all_key[off + i] = rk[i];
-                S.all_idx[off + i] = ri[i];
-                S.all_cta[off + i] = (uint32_t)r;
-            }
-            off += c;
-        }
-        __syncthreads();
-        for (uint32_t i = tid; i < ncand_all; i += kTkThreads) {
-            const uint32_t ki = S.all_key[i];
-            const int32_t ii = S.all_idx[i];
+        // rank every candidate by (key desc, index asc): the one at rank krem-1 is T.
+        // One warp per candidate, lanes split the comparisons.
+        for (uint32_t i = warp; i < ncand_all; i += kTkWarps) {
+            int ri = 0;
+            uint32_t o = i;
+            while (o >= S.ncand[ri]) o -= S.ncand[ri++];
+            const uint32_t ki = S.ckey[ri][o];
+            const int32_t ii = S.cidx[ri][o];
             uint32_t rk = 0;
-            for (uint32_t j = 0; j < ncand_all; ++j) {
-                const uint32_t kj = S.all_key[j];
-                rk += (kj > ki) || (kj == ki && S.all_idx[j] < ii);
-            }
-            if (rk == krem - 1) S.res[0] = ki;
+            for (int r = 0; r < nct; ++r)
+                for (uint32_t j = lane; j < S.ncand[r]; j += 32) {
+                    const uint32_t kj = S.ckey[r][j];
+                    rk += (kj > ki) || (kj == ki && S.cidx[r][j] < ii);
+                }
+#pragma unroll
+            for (int o2 = 16; o2 > 0; o2 >>= 1) rk += __shfl_xor_sync(0xffffffffu, rk, o2);
+            if (lane == 0 && rk == krem - 1) S.res[0] = ki;
         }
         __syncthreads();
         T = S.res[0];
-        // r = number of T-valued candidates kept = krem - #(candidates > T)
-        uint32_t gtT = 0;
-        for (uint32_t i = lane; i < ncand_all; i += 32) gtT += S.all_key[i] > T;
-        for (int o = 16; o > 0; o >>= 1) gtT += __shfl_xor_sync(0xffffffffu, gtT, o);
-        const uint32_t rties = krem - gtT;
-        // per lower CTA: kept = above + candidates > T + min(ties there, remaining ties)
-        uint32_t ties_seen = 0;
-        for (int r = 0; r < rank; ++r) {
+        // per CTA r (warp r): candidates > T and == T
+        if (warp < nct) {
             uint32_t cg_ = 0, ce = 0;
-            for (uint32_t i = lane; i < ncand_all; i += 32) {
-                if (S.all_cta[i] == (uint32_t)r) {
-                    cg_ += S.all_key[i] > T;
-                    ce += S.all_key[i] == T;
-                }
+            for (uint32_t j = lane; j < S.ncand[warp]; j += 32) {
+                cg_ += S.ckey[warp][j] > T;
+                ce += S.ckey[warp][j] == T;
             }
             for (int o = 16; o > 0; o >>= 1) {
                 cg_ += __shfl_xor_sync(0xffffffffu, cg_, o);
                 ce += __shfl_xor_sync(0xffffffffu, ce, o);
             }
+            if (lane == 0) {
+                S.wcnt[warp] = cg_;
+                S.fscratch[warp] = __uint_as_float(ce);
+            }
+        }
+        __syncthreads();
+        uint32_t gtT = 0;
+        for (int r = 0; r < nct; ++r) gtT += S.wcnt[r];
+        const uint32_t rties = krem - gtT;  // T-valued keys to keep (global index order)
+        uint32_t ties_seen = 0;
+        for (int r = 0; r < rank; ++r) {
+            const uint32_t ce = __float_as_uint(S.fscratch[r]);
             const uint32_t take = min(ce, rties > ties_seen ? rties - ties_seen : 0u);
-            sel_before += *cluster.map_shared_rank(&S.nabove, r) + cg_ + take;
+            sel_before += S.nabove[r] + S.wcnt[r] + take;
             ties_seen += ce;
         }
         eq_before = ties_seen;
-        krem = rties;  // from here: keep the first krem T-valued keys (global order)
+        krem = rties;
+        __syncthreads();  // wcnt / fscratch are reused below
     } else {
         // ---- exact radix fallback on the order-preserving keys ----
         uint32_t prefix = 0, pmask = 0, kr = (uint32_t)k;
@@ -390,8 +385,8 @@ __global__ void __launch_bounds__(kTkThreads) topk_kernel(const float* __restric
             e += __popc(__ballot_sync(0xffffffffu, !isnan(x[j]) && key == T));
         }
         uint32_t tg, te;
-        warp_prefix(g, S.wcnt, &tg);
-        warp_prefix(e, S.wcnt, &te);
+        warp_prefix<kTkWarps>(g, S.wcnt, &tg);
+        warp_prefix<kTkWarps>(e, S.wcnt, &te);
         if (tid == 0) {
             S.rsel[0] = tg;
             S.rsel[1] = te;
@@ -406,6 +401,7 @@ __global__ void __launch_bounds__(kTkThreads) topk_kernel(const float* __restric
         sel_before = gb + min(eb, kr);
         eq_before = eb;
         krem = kr;
+        cluster.sync();  // remote reads of rsel done before any CTA exits
     }
 
     // ---- compaction in index order: kept iff key > T or (key == T and tie rank < krem) ----
@@ -419,8 +415,8 @@ __global__ void __launch_bounds__(kTkThreads) topk_kernel(const float* __restric
         weq += __popc(__ballot_sync(0xffffffffu, v && key == T));
     }
     uint32_t tmp;
-    const uint32_t gt_w = warp_prefix(wsel, S.wcnt, &tmp);
-    const uint32_t eq_w = warp_prefix(weq, S.wcnt, &tmp);
+    const uint32_t gt_w = warp_prefix<kTkWarps>(wsel, S.wcnt, &tmp);
+    const uint32_t eq_w = warp_prefix<kTkWarps>(weq, S.wcnt, &tmp);
     // positions: kept before = (#> T before) + min(#== T before, krem) -- counted from
     // the CTA start, then shifted by the lower CTAs' kept count.
     uint32_t gt_run = gt_w, eq_run = eq_before + eq_w;
@@ -440,7 +436,6 @@ __global__ void __launch_bounds__(kTkThreads) topk_kernel(const float* __restric
         gt_run += __popc(mg);
         eq_run += __popc(me);
     }
-    cluster.sync();  // keep exchanged smem alive until every CTA is done reading
 }
 
 // Long rows (> 8 * 256 * 64 keys): the original smem-radix kernel streaming keys
@@ -598,23 +593,21 @@ static int launch_cluster(Kern kern, int cluster, int rows, int threads, size_t 
 
 int topk_dispatch(const float* scores, int rows, int tokens, int64_t ld, int k, int32_t* sel,
                   cudaStream_t st) {
-    // cluster size: enough CTAs to fill the chip, every slice <= 256 * 64 keys
+    // Register path: CTA slices up to 512 x 16 (or 256 x 64) keys, cluster of
+    // C <= 8 CTAs per row, C grown until the grid covers the chip.
+    constexpr int kMaxSlice = 256 * 64;
     int c = 1;
-    while (c < kTkMaxCluster && ((int64_t)rows * c < 2 * 148 || ceil_div(tokens, c) > kTkThreads * 64)) c *= 2;
-    while (c > 1 && ceil_div(tokens, c) < kTkThreads * 4) c /= 2;
+    while (c < kTkMaxCluster && ((int64_t)rows * c < 2 * num_sms() || ceil_div(tokens, c) > kMaxSlice)) c *= 2;
+    while (c > 1 && ceil_div(tokens, c) < 512 * 2) c /= 2;
     const int64_t slice = ceil_div(tokens, c);
     const size_t smem = sizeof(TopkShared);
-    if (slice <= kTkThreads * 64) {
-        int kpt = 4;
-        while ((int64_t)kTkThreads * kpt < slice) kpt *= 2;
-        const int sl = kTkThreads * kpt;
-        switch (kpt) {
-            case 4: return launch_cluster(topk_kernel<4>, c, rows, kTkThreads, smem, st, scores, tokens, ld, k, sl, sel);
-            case 8: return launch_cluster(topk_kernel<8>, c, rows, kTkThreads, smem, st, scores, tokens, ld, k, sl, sel);
-            case 16: return launch_cluster(topk_kernel<16>, c, rows, kTkThreads, smem, st, scores, tokens, ld, k, sl, sel);
-            case 32: return launch_cluster(topk_kernel<32>, c, rows, kTkThreads, smem, st, scores, tokens, ld, k, sl, sel);
-            default: return launch_cluster(topk_kernel<64>, c, rows, kTkThreads, smem, st, scores, tokens, ld, k, sl, sel);
-        }
+    if (slice <= kMaxSlice) {
+        if (slice <= 512 * 2) return launch_cluster(topk_kernel<2, 512>, c, rows, 512, smem, st, scores, tokens, ld, k, 1024, sel);
+        if (slice <= 512 * 4) return launch_cluster(topk_kernel<4, 512>, c, rows, 512, smem, st, scores, tokens, ld, k, 2048, sel);
+        if (slice <= 512 * 8) return launch_cluster(topk_kernel<8, 512>, c, rows, 512, smem, st, scores, tokens, ld, k, 4096, sel);
+        if (slice <= 512 * 16) return launch_cluster(topk_kernel<16, 512>, c, rows, 512, smem, st, scores, tokens, ld, k, 8192, sel);
+        if (slice <= 256 * 32) return launch_cluster(topk_kernel<32, 256>, c, rows, 256, smem, st, scores, tokens, ld, k, 8192, sel);
+        return launch_cluster(topk_kernel<64, 256>, c, rows, 256, smem, st, scores, tokens, ld, k, kMaxSlice, sel);
     }
     const int sl = (int)(ceil_div(slice, 32) * 32);
     return launch_cluster(topk_stream_kernel, c, rows, 1024, 0, st, scores, tokens, ld, k, sl, sel);

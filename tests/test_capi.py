@@ -136,3 +136,17 @@ def test_workspace_sizes_are_consistent(lib):
     ws = lib.fier_decode_workspace(C.byref(s), 32768, 3604)
     assert ws >= 32 * 32768 * 4
     assert lib.fier_step_scores_ld(33) == 64
+
+
+def test_sass_has_no_odd_memory_descriptor_registers():
+    """Regression guard: ptxas 12.9 once emitted LDGSTS with desc[UR1] (odd uniform
+    register as a 64-bit descriptor), which traps as an illegal instruction on B200."""
+    import shutil
+    import subprocess
+    from paper_2508_08256_b200 import _lib
+    tool = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    if not os.path.exists(tool):
+        pytest.skip("cuobjdump not available")
+    sass = subprocess.run([tool, "-sass", _lib.LIB_PATH], capture_output=True, text=True, check=True).stdout
+    assert "LDGSTS" in sass
+    assert not re.search(r"desc\[UR\d*[13579]\]", sass)
