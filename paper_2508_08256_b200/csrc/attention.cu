@@ -505,7 +505,13 @@ static int per_sm_typed(const fier_shape* s, bool gather) {
     return 8;  // generic one-warp kernel
 }
 
+int tc_resident(const fier_shape* s, bool gather);
+int tc_dispatch(const fier_shape* s, bool gather, const void* q, const void* K, const void* V,
+                const int32_t* sel, int n, int tokens, float scale, float* part, int* counters, float* out,
+                int nsplit, int rows_per_cta, cudaStream_t st);
+
 static int resident_per_sm(const fier_shape* s, bool gather) {
+    if (const int tc = tc_resident(s, gather)) return tc;
     // occupancy needs the opt-in smem limit set on the kernel first
     switch (s->dtype) {
         case FIER_F32: return per_sm_typed<float>(s, gather);
@@ -596,6 +602,8 @@ int sparse_dispatch(const fier_shape* s, const void* q, const void* K, const voi
         cudaError_t e = cudaMemsetAsync(ctr, 0, (size_t)s->batch * s->q_heads * sizeof(int), st);
         if (e != cudaSuccess) return fail(FIER_ECUDA, std::string("gather_attention: ") + cudaGetErrorString(e));
     }
+    if (tc_resident(s, true) > 0)
+        return tc_dispatch(s, true, q, K, V, sel, n, tokens, scale, part, ctr, out, p.nsplit, p.rows_per_cta, st);
     int rc = FIER_OK;
     switch (s->dtype) {
         case FIER_F32: rc = sparse_typed<float>(s, q, K, V, sel, n, tokens, scale, part, ctr, out, p, st); break;
@@ -617,6 +625,9 @@ int full_dispatch(const fier_shape* s, const void* q, const void* K, const void*
         cudaError_t e = cudaMemsetAsync(ctr, 0, (size_t)s->batch * s->q_heads * sizeof(int), st);
         if (e != cudaSuccess) return fail(FIER_ECUDA, std::string("gather_attention: ") + cudaGetErrorString(e));
     }
+    if (tc_resident(s, false) > 0)
+        return tc_dispatch(s, false, q, K, V, nullptr, 0, tokens, scale, part, ctr, out, p.nsplit, p.rows_per_cta,
+                           st);
     int rc = FIER_OK;
     switch (s->dtype) {
         case FIER_F32: rc = full_typed<float>(s, q, K, V, tokens, scale, part, ctr, out, p, st); break;

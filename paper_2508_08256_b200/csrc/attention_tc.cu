@@ -1,0 +1,425 @@
+// attention_tc.cu -- tensor-core decode attention (bf16 / fp16 K, V; d = 64 or 128).
+//
+// K4 (gather_attention on the Top-k selection, reference core.hpp:152-179) and
+// K0 (gather_attention over every index, retrieval.hpp:159-166) for 16-bit
+// caches.  Decode attention moves bytes, not flops; the tensor cores are used
+// to cut the instruction count per gathered row (~11 vs ~54 on CUDA cores) so
+// the SMs keep enough loads in flight.
+//
+// Each warp owns a sub-range of rows and streams it through a private NST-stage
+// ring of 16-row stages (cp.async 16-byte chunks, XOR-swizzled by row so
+// ldmatrix is conflict-free).  Per stage:
+//   S[m][n]  = sum_k Q[m][k] K[n][k]     16 x mma.m16n8k16 (A = q rows, B = K
+//                                         via ldmatrix), m = query heads of the
+//                                         GQA group (rows >= HPG are zero)
+//   online softmax per query row in fp32 (log2 domain)
+//   O[m][c] += sum_n P[m][n] V[n][c]     P split into bf16 hi + lo parts (two
+//                                         mma per tile, ~2^-16 relative error),
+//                                         B = V via ldmatrix.trans
+// Warp states are merged per CTA, CTA partials by log-sum-exp (the last CTA of
+// each head merges), exactly like attention.cu.
+#include "common.cuh"
+
+namespace fier_cuda {
+
+constexpr int kTcWarps = 4;
+constexpr int kTcRows = 16;  // rows per stage
+
+template <typename T>
+struct MmaType;
+template <>
+struct MmaType<__nv_bfloat16> {
+    static constexpr const char* name = "bf16";
+};
+template <>
+struct MmaType<__half> {
+    static constexpr const char* name = "f16";
+};
+
+__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+                 : "r"(addr));
+}
+__device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+                 : "r"(addr));
+}
+
+template <typename T>
+__device__ __forceinline__ void mma16816(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
+                                         uint32_t b0, uint32_t b1) {
+    if constexpr (std::is_same<T, __nv_bfloat16>::value) {
+        asm volatile(
+            "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+            "{%0,%1,%2,%3};"
+            : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+            : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+    } else {
+        asm volatile(
+            "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+            "{%0,%1,%2,%3};"
+            : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+            : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+    }
+}
+
+// two floats -> packed 16-bit pair (lo in the low half), RNE
+template <typename T>
+__device__ __forceinline__ uint32_t pack2(float lo, float hi) {
+    if constexpr (std::is_same<T, __nv_bfloat16>::value) {
+        __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+        return *reinterpret_cast<uint32_t*>(&v);
+    } else {
+        __half2 v = __floats2half2_rn(lo, hi);
+        return *reinterpret_cast<uint32_t*>(&v);
+    }
+}
+template <typename T>
+__device__ __forceinline__ float2 unpack2(uint32_t w) {
+    if constexpr (std::is_same<T, __nv_bfloat16>::value) {
+        return make_float2(__uint_as_float(w << 16), __uint_as_float(w & 0xFFFF0000u));
+    } else {
+        return __half22float2(*reinterpret_cast<const __half2*>(&w));
+    }
+}
+
+__device__ __forceinline__ void cp_async16_tc(uint32_t smem, const void* gmem) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem), "l"(gmem) : "memory");
+}
+
+// byte offset of 16-byte chunk c of row r inside a stage buffer (rows of RB bytes)
+template <int RB>
+__device__ __forceinline__ uint32_t swz(int r, int c) {
+    return (uint32_t)(r * RB + ((c ^ (r & 7)) << 4));
+}
+
+template <typename T, int D, int HPG, bool GATHER, int NST>
+__global__ void __launch_bounds__(kTcWarps * 32) attn_tc_kernel(
+    const T* __restrict__ q, const T* __restrict__ K, const T* __restrict__ V,
+    const int32_t* __restrict__ sel, int n, int tokens, int cap, int hkv, int hq, float scale_log2,
+    int rows_per_cta, float* __restrict__ part, int nsplit, int* __restrict__ counters,
+    float* __restrict__ out) {
+    static_assert(HPG <= 8, "query rows live in mma rows 0..7");
+    constexpr int RB = D * 2;              // bytes per row
+    constexpr int CPR = RB / 16;           // 16-byte chunks per row
+    constexpr int KSTEPS = D / 16;         // mma k-steps over channels
+    constexpr int NT = D / 8;              // n-tiles over channels (PV)
+    constexpr int STAGE = kTcRows * RB;    // bytes per K (or V) stage
+    constexpr int CPL = kTcRows * CPR / 32;  // chunks per lane per K (or V) stage
+
+    extern __shared__ __align__(128) uint8_t smem[];
+    float* wres = reinterpret_cast<float*>(smem + (size_t)kTcWarps * NST * 2 * STAGE);  // [warp][HPG][D+2]
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int g = lane >> 2, t = lane & 3;
+    const int split = blockIdx.x, head = blockIdx.y, b = blockIdx.z;
+    const int kvh = GATHER ? head / (hq / hkv) : head;
+    const int64_t seq = (int64_t)b * hkv + kvh;
+    const T* Kseq = K + seq * cap * D;
+    const T* Vseq = V + seq * cap * D;
+    const int total = GATHER ? n : tokens;
+    const int r_begin = split * rows_per_cta;
+    const int r_end = min(r_begin + rows_per_cta, total);
+    const int rpw = (int)((((r_end - r_begin) + kTcWarps - 1) / kTcWarps + kTcRows - 1) / kTcRows * kTcRows);
+    const int wr0 = min(r_begin + warp * rpw, r_end);
+    const int wr1 = min(wr0 + rpw, r_end);
+    const int nstages = (wr1 - wr0 + kTcRows - 1) / kTcRows;
+    const int32_t* selrow = GATHER ? sel + ((int64_t)b * hq + head) * n : nullptr;
+    const int qh0 = GATHER ? head : head * HPG;
+
+    // A fragments of Q (row m = query head m of the group; rows >= HPG zero)
+    uint32_t qa[KSTEPS][2];
+#pragma unroll
+    for (int ks = 0; ks < KSTEPS; ++ks) {
+        qa[ks][0] = qa[ks][1] = 0u;
+        if (g < HPG) {
+            const T* qp = q + ((int64_t)b * hq + qh0 + g) * D + ks * 16 + 2 * t;
+            qa[ks][0] = *reinterpret_cast<const uint32_t*>(qp);
+            qa[ks][1] = *reinterpret_cast<const uint32_t*>(qp + 8);
+        }
+    }
+
+    const uint32_t ring = smem_u32(smem) + (uint32_t)warp * NST * 2 * STAGE;
+
+    auto issue = [&](int st) {
+        if (st < nstages) {
+            const uint32_t kdst = ring + (uint32_t)(st % NST) * 2 * STAGE;
+            const uint32_t vdst = kdst + STAGE;
+            const int r0 = wr0 + st * kTcRows;
+            const int nr = min(kTcRows, wr1 - r0);
+            int tok = 0;
+            if constexpr (GATHER) {
+                if (lane < nr) tok = __ldg(selrow + r0 + lane);
+            }
+#pragma unroll
+            for (int i = 0; i < CPL; ++i) {
+                const int chunk = lane + 32 * i;
+                const int rr = chunk / CPR, c = chunk % CPR;
+                int tk;
+                if constexpr (GATHER) {
+                    tk = __shfl_sync(0xffffffffu, tok, rr);
+                } else {
+                    tk = r0 + rr;
+                }
+                const uint32_t o = swz<RB>(rr, c);
+                if (rr < nr) {
+                    cp_async16_tc(kdst + o, Kseq + (int64_t)tk * D + c * 8);
+                    cp_async16_tc(vdst + o, Vseq + (int64_t)tk * D + c * 8);
+                } else {  // rows past the end: V must be finite zeros (p = 0 there)
+                    asm volatile("st.shared.v4.u32 [%0], {%1,%1,%1,%1};" ::"r"(vdst + o), "r"(0u) : "memory");
+                    asm volatile("st.shared.v4.u32 [%0], {%1,%1,%1,%1};" ::"r"(kdst + o), "r"(0u) : "memory");
+                }
+            }
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+
+#pragma unroll
+    for (int s = 0; s < NST - 1; ++s) issue(s);
+
+    float o[NT][2];  // O[g][nt*8 + 2t + {0,1}]
+#pragma unroll
+    for (int i = 0; i < NT; ++i) o[i][0] = o[i][1] = 0.f;
+    float mrow = -INFINITY, lrow = 0.f;  // row g's running max / partial sum (this lane's tokens)
+
+    for (int st = 0; st < nstages; ++st) {
+        issue(st + NST - 1);
+        asm volatile("cp.async.wait_group %0;" ::"n"(NST - 1) : "memory");
+        __syncwarp();
+        const uint32_t kst = ring + (uint32_t)(st % NST) * 2 * STAGE;
+        const uint32_t vst = kst + STAGE;
+        const int nr = min(kTcRows, wr1 - (wr0 + st * kTcRows));
+
+        // ---- S = Q K^T for 16 rows: two n-tiles of 8 rows ----
+        float s[2][4];
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt) {
+            s[nt][0] = s[nt][1] = s[nt][2] = s[nt][3] = 0.f;
+#pragma unroll
+            for (int kp = 0; kp < KSTEPS / 2; ++kp) {  // pairs of k-steps = 4 chunks
+                uint32_t b0, b1, b2, b3;
+                const int row = nt * 8 + (lane & 7);
+                ldsm_x4(kst + swz<RB>(row, 4 * kp + (lane >> 3)), b0, b1, b2, b3);
+                mma16816<T>(s[nt], qa[2 * kp][0], 0u, qa[2 * kp][1], 0u, b0, b1);
+                mma16816<T>(s[nt], qa[2 * kp + 1][0], 0u, qa[2 * kp + 1][1], 0u, b2, b3);
+            }
+        }
+        // this lane's 4 logits of query row g: tokens nt*8 + 2t + {0,1}
+        float x[4];
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int tkn = nt * 8 + 2 * t + e;
+                x[nt * 2 + e] = tkn < nr ? s[nt][e] * scale_log2 : -INFINITY;
+            }
+        float mst = fmaxf(fmaxf(x[0], x[1]), fmaxf(x[2], x[3]));
+        mst = fmaxf(mst, __shfl_xor_sync(0xffffffffu, mst, 1));
+        mst = fmaxf(mst, __shfl_xor_sync(0xffffffffu, mst, 2));
+        const float mnew = fmaxf(mrow, mst);
+        const float alpha = exp2f(mrow - mnew);
+        float p[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) p[i] = exp2f(x[i] - mnew);
+        lrow = lrow * alpha + (p[0] + p[1]) + (p[2] + p[3]);
+        mrow = mnew;
+        if (__any_sync(0xffffffffu, alpha != 1.f)) {
+#pragma unroll
+            for (int i = 0; i < NT; ++i) {
+                o[i][0] *= alpha;
+                o[i][1] *= alpha;
+            }
+        }
+        // P as A fragments (row g): hi + lo 16-bit parts
+        const uint32_t ph0 = pack2<T>(p[0], p[1]), ph2 = pack2<T>(p[2], p[3]);
+        const float2 q0 = unpack2<T>(ph0), q2 = unpack2<T>(ph2);
+        const uint32_t pl0 = pack2<T>(p[0] - q0.x, p[1] - q0.y), pl2 = pack2<T>(p[2] - q2.x, p[3] - q2.y);
+        // ---- O += P V: n-tile pairs of 16 channels ----
+#pragma unroll
+        for (int np = 0; np < NT / 2; ++np) {
+            uint32_t b0, b1, b2, b3;
+            const int row = (lane & 7) + 8 * ((lane >> 3) & 1);
+            ldsm_x4_t(vst + swz<RB>(row, 2 * np + (lane >> 4)), b0, b1, b2, b3);
+            float d0[4] = {o[2 * np][0], o[2 * np][1], 0.f, 0.f};
+            float d1[4] = {o[2 * np + 1][0], o[2 * np + 1][1], 0.f, 0.f};
+            mma16816<T>(d0, ph0, 0u, ph2, 0u, b0, b1);
+            mma16816<T>(d0, pl0, 0u, pl2, 0u, b0, b1);
+            mma16816<T>(d1, ph0, 0u, ph2, 0u, b2, b3);
+            mma16816<T>(d1, pl0, 0u, pl2, 0u, b2, b3);
+            o[2 * np][0] = d0[0];
+            o[2 * np][1] = d0[1];
+            o[2 * np + 1][0] = d1[0];
+            o[2 * np + 1][1] = d1[1];
+        }
+        __syncwarp();
+    }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+
+    // ---- warp states -> smem -> CTA partial -> last-CTA merge ----
+    lrow += __shfl_xor_sync(0xffffffffu, lrow, 1);
+    lrow += __shfl_xor_sync(0xffffffffu, lrow, 2);
+    float* wr = wres + warp * HPG * (D + 2);
+    if (g < HPG) {
+#pragma unroll
+        for (int i = 0; i < NT; ++i) {
+            wr[g * (D + 2) + i * 8 + 2 * t] = o[i][0];
+            wr[g * (D + 2) + i * 8 + 2 * t + 1] = o[i][1];
+        }
+        if (t == 0) {
+            wr[g * (D + 2) + D] = mrow;
+            wr[g * (D + 2) + D + 1] = lrow;
+        }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < HPG * D; i += blockDim.x) {
+        const int hh = i / D, c = i % D;
+        float M = -INFINITY;
+#pragma unroll
+        for (int w = 0; w < kTcWarps; ++w) M = fmaxf(M, wres[(w * HPG + hh) * (D + 2) + D]);
+        float oo = 0.f, L = 0.f;
+#pragma unroll
+        for (int w = 0; w < kTcWarps; ++w) {
+            const float* xx = wres + (w * HPG + hh) * (D + 2);
+            const float mw = xx[D];
+            const float sc = mw == -INFINITY ? 0.f : exp2f(mw - M);
+            oo = fmaf(xx[c], sc, oo);
+            L = fmaf(xx[D + 1], sc, L);
+        }
+        float* dst = part + (((int64_t)b * hq + qh0 + hh) * nsplit + split) * (D + 2);
+        dst[c] = oo;
+        if (c == 0) {
+            dst[D] = M;
+            dst[D + 1] = L;
+        }
+    }
+    __shared__ int s_last;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        const int unit = b * (GATHER ? hq : hkv) + head;
+        s_last = atomicAdd(&counters[unit], 1) == nsplit - 1;
+        if (s_last) counters[unit] = 0;
+    }
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    // merge nsplit partials of the HPG heads (smem: 2*nsplit floats in wres)
+    for (int hh = 0; hh < HPG; ++hh) {
+        const float* pp = part + ((int64_t)b * hq + qh0 + hh) * nsplit * (D + 2);
+        for (int sp = threadIdx.x; sp < nsplit; sp += blockDim.x) {
+            wres[sp] = __ldcg(pp + sp * (D + 2) + D);
+            wres[nsplit + sp] = __ldcg(pp + sp * (D + 2) + D + 1);
+        }
+        __syncthreads();
+        float M = -INFINITY;
+        for (int sp = 0; sp < nsplit; ++sp) M = fmaxf(M, wres[sp]);
+        float L = 0.f;
+        for (int sp = 0; sp < nsplit; ++sp)
+            if (wres[sp] != -INFINITY) L += wres[nsplit + sp] * exp2f(wres[sp] - M);
+        const float inv = 1.f / L;
+        for (int c = threadIdx.x; c < D; c += blockDim.x) {
+            float oo = 0.f;
+#pragma unroll 4
+            for (int sp = 0; sp < nsplit; ++sp) {
+                const float ms = wres[sp];
+                const float xv = __ldcg(pp + sp * (D + 2) + c);
+                if (ms != -INFINITY) oo = fmaf(xv, exp2f(ms - M), oo);
+            }
+            out[((int64_t)b * hq + qh0 + hh) * D + c] = oo * inv;
+        }
+        __syncthreads();
+    }
+}
+
+// ---- host side -------------------------------------------------------------------
+
+template <int D, int HPG>
+constexpr size_t tc_smem(int nst) {
+    // wres must also hold the 2 * nsplit (<= 2 * 256) merge weights
+    return (size_t)kTcWarps * nst * 2 * kTcRows * D * 2 +
+           (size_t)(kTcWarps * HPG * (D + 2) > 512 ? kTcWarps * HPG * (D + 2) : 512) * 4;
+}
+
+constexpr int kTcNst = 3;
+
+template <typename T, int D, int HPG, bool GATHER>
+int tc_per_sm() {
+    static const int v = [] {
+        auto kern = attn_tc_kernel<T, D, HPG, GATHER, kTcNst>;
+        const size_t smem = tc_smem<D, HPG>(kTcNst);
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        return ctas_per_sm(kern, kTcWarps * 32, smem);
+    }();
+    return v;
+}
+
+template <typename T, int D, int HPG, bool GATHER>
+int launch_attn_tc(const fier_shape* s, const void* q, const void* K, const void* V, const int32_t* sel,
+                   int n, int tokens, float scale, float* part, int* counters, float* out, int nsplit,
+                   int rows_per_cta, cudaStream_t st) {
+    auto kern = attn_tc_kernel<T, D, HPG, GATHER, kTcNst>;
+    const size_t smem = tc_smem<D, HPG>(kTcNst);
+    (void)tc_per_sm<T, D, HPG, GATHER>();  // sets the smem attribute once
+    dim3 grid(nsplit, GATHER ? s->q_heads : s->kv_heads, s->batch);
+    kern<<<grid, kTcWarps * 32, smem, st>>>(static_cast<const T*>(q), static_cast<const T*>(K),
+                                            static_cast<const T*>(V), sel, n, tokens, s->capacity,
+                                            s->kv_heads, s->q_heads, scale * kLog2e, rows_per_cta, part,
+                                            nsplit, counters, out);
+    return check_launch("attention (tensor core)");
+}
+
+// resident CTAs per SM for the tensor-core path of this shape (0: not applicable)
+int tc_resident(const fier_shape* s, bool gather) {
+    const int hpg = gather ? 1 : s->q_heads / s->kv_heads;
+    if (s->dtype != FIER_BF16 && s->dtype != FIER_F16) return 0;
+    if (s->dim != 128 && s->dim != 64) return 0;
+    if (!(hpg == 1 || hpg == 2 || hpg == 4 || hpg == 8)) return 0;
+#define TC_CASE(TT, DD)                                                                          \
+    switch (hpg) {                                                                               \
+        case 1: return gather ? tc_per_sm<TT, DD, 1, true>() : tc_per_sm<TT, DD, 1, false>();    \
+        case 2: return tc_per_sm<TT, DD, 2, false>();                                            \
+        case 4: return tc_per_sm<TT, DD, 4, false>();                                            \
+        default: return tc_per_sm<TT, DD, 8, false>();                                           \
+    }
+    if (s->dtype == FIER_BF16) {
+        if (s->dim == 128) { TC_CASE(__nv_bfloat16, 128) }
+        TC_CASE(__nv_bfloat16, 64)
+    }
+    if (s->dim == 128) { TC_CASE(__half, 128) }
+    TC_CASE(__half, 64)
+#undef TC_CASE
+}
+
+int tc_dispatch(const fier_shape* s, bool gather, const void* q, const void* K, const void* V,
+                const int32_t* sel, int n, int tokens, float scale, float* part, int* counters, float* out,
+                int nsplit, int rows_per_cta, cudaStream_t st) {
+    const int hpg = gather ? 1 : s->q_heads / s->kv_heads;
+#define TC_LAUNCH(TT, DD)                                                                               \
+    switch (hpg) {                                                                                      \
+        case 1:                                                                                         \
+            return gather ? launch_attn_tc<TT, DD, 1, true>(s, q, K, V, sel, n, tokens, scale, part,    \
+                                                            counters, out, nsplit, rows_per_cta, st)    \
+                          : launch_attn_tc<TT, DD, 1, false>(s, q, K, V, sel, n, tokens, scale, part,   \
+                                                             counters, out, nsplit, rows_per_cta, st);  \
+        case 2:                                                                                         \
+            return launch_attn_tc<TT, DD, 2, false>(s, q, K, V, sel, n, tokens, scale, part, counters, \
+                                                    out, nsplit, rows_per_cta, st);                     \
+        case 4:                                                                                         \
+            return launch_attn_tc<TT, DD, 4, false>(s, q, K, V, sel, n, tokens, scale, part, counters, \
+                                                    out, nsplit, rows_per_cta, st);                     \
+        default:                                                                                        \
+            return launch_attn_tc<TT, DD, 8, false>(s, q, K, V, sel, n, tokens, scale, part, counters, \
+                                                    out, nsplit, rows_per_cta, st);                     \
+    }
+    if (s->dtype == FIER_BF16) {
+        if (s->dim == 128) { TC_LAUNCH(__nv_bfloat16, 128) }
+        TC_LAUNCH(__nv_bfloat16, 64)
+    }
+    if (s->dim == 128) { TC_LAUNCH(__half, 128) }
+    TC_LAUNCH(__half, 64)
+#undef TC_LAUNCH
+}
+
+}  // namespace fier_cuda

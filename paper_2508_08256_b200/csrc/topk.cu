@@ -36,6 +36,7 @@ namespace fier_cuda {
 constexpr int kTkMaxWarps = 16;
 constexpr int kTkMaxCluster = 8;
 constexpr int kTkCandCta = 256;   // candidates one CTA may contribute (fast path)
+constexpr int kTkFlat = 1024;     // candidates a cluster may rank (fast path)
 constexpr int kTkRadixBins = 2048;
 
 struct TopkShared {
@@ -58,6 +59,12 @@ struct TopkShared {
     float fscratch[2 * kTkMaxWarps];
     uint32_t lcand;                           // local candidate counter
     uint32_t res[8];
+    uint32_t wnab[kTkMaxWarps];               // strictly-above keys per warp (this CTA)
+    uint32_t wg[kTkMaxWarps], we[kTkMaxWarps];  // candidates > T / == T per warp
+    uint32_t cg[kTkMaxCluster], ce[kTkMaxCluster];  // candidates > T / == T per CTA
+    uint32_t fkey[kTkFlat];                   // flattened candidates (CTA-rank order)
+    int32_t fidx[kTkFlat];
+    uint8_t fcta[kTkFlat];
 };
 
 __device__ __forceinline__ uint32_t lanemask_lt() {
@@ -95,8 +102,7 @@ __device__ __forceinline__ void find_bin32(uint32_t cnt, uint32_t krem, uint32_t
 }
 
 __device__ __forceinline__ int lin_bin(float x, float lo, float inv) {
-    if (x == INFINITY) return 31;
-    if (x == -INFINITY) return 0;
+    // +-inf clamp to bins 31 / 0 (inv > 0 on the fast path)
     float t = (x - lo) * inv;
     t = fminf(fmaxf(t, 0.f), 31.f);
     return (int)t;  // truncation == floor on [0, 31]
@@ -257,6 +263,7 @@ __global__ void __launch_bounds__(kTkThreads) topk_kernel(const float* __restric
             }
         }
     }
+    if (lane == 0) S.wnab[warp] = nab;
     uint32_t tot_ab;
     warp_prefix<kTkWarps>(nab, S.wcnt, &tot_ab);  // (contains __syncthreads: lcand final)
     if (tid < nct) {
@@ -264,67 +271,88 @@ __global__ void __launch_bounds__(kTkThreads) topk_kernel(const float* __restric
         *cluster.map_shared_rank(&S.nabove[rank], tid) = tot_ab;
     }
     cluster.sync();  // #4 -- after this, the fast path reads only local smem
-    uint32_t ncand_all = 0, ncand_max = 0;
-    for (int r = 0; r < nct; ++r) {
-        ncand_all += S.ncand[r];
-        ncand_max = max(ncand_max, S.ncand[r]);
+    uint32_t off[kTkMaxCluster + 1];
+    off[0] = 0;
+    uint32_t ncand_max = 0;
+#pragma unroll
+    for (int r = 0; r < kTkMaxCluster; ++r) {
+        const uint32_t c = r < nct ? S.ncand[r] : 0u;
+        off[r + 1] = off[r] + c;
+        ncand_max = max(ncand_max, c);
     }
+    const uint32_t ncand_all = off[kTkMaxCluster];
 
     uint32_t T;                 // threshold key
     uint32_t sel_before = 0;    // kept elements in lower-ranked CTAs
     uint32_t eq_before = 0;     // T-valued keys in lower-ranked CTAs
-    const bool radix = ncand_max > kTkCandCta;  // uniform over the cluster
+    uint32_t gt_w = 0, eq_w = 0;  // (> T) / (== T) keys of this CTA in lower warps
+    // uniform over the cluster: overflow, or a degenerate range (hi == lo: the
+    // linear bins cannot order +inf against the finite values)
+    const bool radix = ncand_max > kTkCandCta || ncand_all > kTkFlat || !(inv1 > 0.f);
     if (!radix) {
-        // rank every candidate by (key desc, index asc): the one at rank krem-1 is T.
-        // One warp per candidate, lanes split the comparisons.
-        for (uint32_t i = warp; i < ncand_all; i += kTkWarps) {
-            int ri = 0;
-            uint32_t o = i;
-            while (o >= S.ncand[ri]) o -= S.ncand[ri++];
-            const uint32_t ki = S.ckey[ri][o];
-            const int32_t ii = S.cidx[ri][o];
-            uint32_t rk = 0;
-            for (int r = 0; r < nct; ++r)
-                for (uint32_t j = lane; j < S.ncand[r]; j += 32) {
-                    const uint32_t kj = S.ckey[r][j];
-                    rk += (kj > ki) || (kj == ki && S.cidx[r][j] < ii);
-                }
+        // flatten the candidates (CTA-rank order), classify after T is known
+        for (uint32_t i = tid; i < ncand_all; i += kTkThreads) {
+            int r = 0;
 #pragma unroll
-            for (int o2 = 16; o2 > 0; o2 >>= 1) rk += __shfl_xor_sync(0xffffffffu, rk, o2);
+            for (int rr = 1; rr < kTkMaxCluster; ++rr) r += i >= off[rr];
+            S.fkey[i] = S.ckey[r][i - off[r]];
+            S.fidx[i] = S.cidx[r][i - off[r]];
+            S.fcta[i] = (uint8_t)r;
+        }
+        if (tid < kTkMaxCluster) {
+            S.cg[tid] = 0;
+            S.ce[tid] = 0;
+        }
+        if (tid < kTkWarps) {
+            S.wg[tid] = 0;
+            S.we[tid] = 0;
+        }
+        __syncthreads();
+        // rank by (key desc, index asc), one warp per candidate, lanes split j;
+        // the candidate of rank krem-1 is the threshold T
+        for (uint32_t i = warp; i < ncand_all; i += kTkWarps) {
+            const uint32_t ki = S.fkey[i];
+            const int32_t ii = S.fidx[i];
+            uint32_t rk = 0;
+            for (uint32_t j = lane; j < ncand_all; j += 32) {
+                const uint32_t kj = S.fkey[j];
+                rk += (kj > ki) || (kj == ki && S.fidx[j] < ii);
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) rk += __shfl_xor_sync(0xffffffffu, rk, o);
             if (lane == 0 && rk == krem - 1) S.res[0] = ki;
         }
         __syncthreads();
         T = S.res[0];
-        // per CTA r (warp r): candidates > T and == T
-        if (warp < nct) {
-            uint32_t cg_ = 0, ce = 0;
-            for (uint32_t j = lane; j < S.ncand[warp]; j += 32) {
-                cg_ += S.ckey[warp][j] > T;
-                ce += S.ckey[warp][j] == T;
-            }
-            for (int o = 16; o > 0; o >>= 1) {
-                cg_ += __shfl_xor_sync(0xffffffffu, cg_, o);
-                ce += __shfl_xor_sync(0xffffffffu, ce, o);
-            }
-            if (lane == 0) {
-                S.wcnt[warp] = cg_;
-                S.fscratch[warp] = __uint_as_float(ce);
+        // per-CTA and (this CTA) per-warp counts of candidates > T and == T
+        for (uint32_t i = tid; i < ncand_all; i += kTkThreads) {
+            const uint32_t key = S.fkey[i];
+            const int r = S.fcta[i];
+            const bool g = key > T, e = key == T;
+            if (g) atomicAdd(&S.cg[r], 1u);
+            if (e) atomicAdd(&S.ce[r], 1u);
+            if (r == rank) {
+                const int w = (S.fidx[i] - s0) / (32 * KPT);
+                if (g) atomicAdd(&S.wg[w], 1u);
+                if (e) atomicAdd(&S.we[w], 1u);
             }
         }
         __syncthreads();
         uint32_t gtT = 0;
-        for (int r = 0; r < nct; ++r) gtT += S.wcnt[r];
+        for (int r = 0; r < nct; ++r) gtT += S.cg[r];
         const uint32_t rties = krem - gtT;  // T-valued keys to keep (global index order)
         uint32_t ties_seen = 0;
         for (int r = 0; r < rank; ++r) {
-            const uint32_t ce = __float_as_uint(S.fscratch[r]);
-            const uint32_t take = min(ce, rties > ties_seen ? rties - ties_seen : 0u);
-            sel_before += S.nabove[r] + S.wcnt[r] + take;
+            const uint32_t ce = S.ce[r];
+            sel_before += S.nabove[r] + S.cg[r] + min(ce, rties > ties_seen ? rties - ties_seen : 0u);
             ties_seen += ce;
         }
         eq_before = ties_seen;
         krem = rties;
-        __syncthreads();  // wcnt / fscratch are reused below
+        for (int w = 0; w < warp; ++w) {
+            gt_w += S.wnab[w] + S.wg[w];
+            eq_w += S.we[w];
+        }
     } else {
         // ---- exact radix fallback on the order-preserving keys ----
         uint32_t prefix = 0, pmask = 0, kr = (uint32_t)k;
@@ -376,7 +404,7 @@ __global__ void __launch_bounds__(kTkThreads) topk_kernel(const float* __restric
             __syncthreads();
         }
         T = prefix;
-        // CTA counts of (> T, == T) -> prefixes over lower CTAs
+        // CTA counts of (> T, == T) -> prefixes over lower CTAs and lower warps
         uint32_t g = 0, e = 0;
 #pragma unroll
         for (int j = 0; j < KPT; ++j) {
@@ -385,8 +413,8 @@ __global__ void __launch_bounds__(kTkThreads) topk_kernel(const float* __restric
             e += __popc(__ballot_sync(0xffffffffu, !isnan(x[j]) && key == T));
         }
         uint32_t tg, te;
-        warp_prefix<kTkWarps>(g, S.wcnt, &tg);
-        warp_prefix<kTkWarps>(e, S.wcnt, &te);
+        gt_w = warp_prefix<kTkWarps>(g, S.wcnt, &tg);
+        eq_w = warp_prefix<kTkWarps>(e, S.wcnt, &te);
         if (tid == 0) {
             S.rsel[0] = tg;
             S.rsel[1] = te;
@@ -404,23 +432,11 @@ __global__ void __launch_bounds__(kTkThreads) topk_kernel(const float* __restric
         cluster.sync();  // remote reads of rsel done before any CTA exits
     }
 
-    // ---- compaction in index order: kept iff key > T or (key == T and tie rank < krem) ----
-    // warp-level counts first (warps own contiguous position ranges)
-    uint32_t wsel = 0, weq = 0;
-#pragma unroll
-    for (int j = 0; j < KPT; ++j) {
-        const bool v = !isnan(x[j]);
-        const uint32_t key = v ? float_key(x[j]) : 0u;
-        wsel += __popc(__ballot_sync(0xffffffffu, v && key > T));
-        weq += __popc(__ballot_sync(0xffffffffu, v && key == T));
-    }
-    uint32_t tmp;
-    const uint32_t gt_w = warp_prefix<kTkWarps>(wsel, S.wcnt, &tmp);
-    const uint32_t eq_w = warp_prefix<kTkWarps>(weq, S.wcnt, &tmp);
-    // positions: kept before = (#> T before) + min(#== T before, krem) -- counted from
-    // the CTA start, then shifted by the lower CTAs' kept count.
-    uint32_t gt_run = gt_w, eq_run = eq_before + eq_w;
-    const uint32_t cta_gt_base = sel_before - min(eq_before, krem);  // lower CTAs' (> T) kept
+    // ---- single compaction pass in index order ----
+    // kept iff key > T or (key == T and tie rank < krem); slot = #(> T before) +
+    // min(#(== T before), krem), counted from the row start.
+    uint32_t gt_run = (sel_before - min(eq_before, krem)) + gt_w;
+    uint32_t eq_run = eq_before + eq_w;
     int32_t* out = sel + (int64_t)row * k;
     const uint32_t lt = lanemask_lt();
 #pragma unroll
@@ -430,7 +446,7 @@ __global__ void __launch_bounds__(kTkThreads) topk_kernel(const float* __restric
         const bool g = v && key > T, e = v && key == T;
         const uint32_t mg = __ballot_sync(0xffffffffu, g);
         const uint32_t me = __ballot_sync(0xffffffffu, e);
-        const uint32_t my_gt = cta_gt_base + gt_run + __popc(mg & lt);
+        const uint32_t my_gt = gt_run + __popc(mg & lt);
         const uint32_t my_eq = eq_run + __popc(me & lt);
         if (g || (e && my_eq < krem)) out[my_gt + min(my_eq, krem)] = s0 + wbase + 32 * j + lane;
         gt_run += __popc(mg);
