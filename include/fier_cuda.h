@@ -109,6 +109,16 @@ FIER_API int fier_sparse_attention(const fier_shape* s, const void* q, const voi
                           const int32_t* sel, int32_t n, int32_t tokens, float scale, float* out,
                           void* workspace, size_t workspace_bytes, void* stream);
 
+/* Ragged variant for the sequence-sharded step: row (b, h) attends over the
+ * first min(n, counts[b][h]) indices of sel[b][h][0..n) (row stride n).  Also
+ * writes lse[b][h] = log2 sum_i exp2(scale*log2(e)*q.k_i) (the log-sum-exp of
+ * this shard's logits in the log2 domain; -inf and out = 0 for an empty row),
+ * the weight fier_lse_merge needs. */
+FIER_API int fier_sparse_attention_ragged(const fier_shape* s, const void* q, const void* K, const void* V,
+                                 const int32_t* sel, const int32_t* counts, int32_t n, int32_t tokens,
+                                 float scale, float* out, float* lse, void* workspace,
+                                 size_t workspace_bytes, void* stream);
+
 /* ---- K0: full-KV decode attention (the in-house baseline) --------------------- */
 /* gather_attention over all indices (the `full` policy, retrieval.hpp:159-166). */
 FIER_API size_t fier_full_attention_workspace(const fier_shape* s, int32_t tokens);
@@ -127,6 +137,31 @@ FIER_API int fier_decode_step(const fier_shape* s, const void* q, const void* k_
                      int32_t pos, void* K, void* V, uint32_t* bits, void* params, int32_t n,
                      float scale, float* out, int32_t* sel, float* scores_out, void* workspace,
                      size_t workspace_bytes, void* stream);
+
+/* ---- X1: sequence-sharded step -------------------------------- */
+/* The whole-group token range [start, end) of shard `rank` of `shards` over a
+ * context of `tokens` (boundaries multiples of g: each shard's index equals the
+ * matching slice of quantize(), quant1bit.hpp:5-9).  Host-only. */
+FIER_API int fier_shard_bounds(int64_t tokens, int32_t shards, int32_t group, int32_t rank, int64_t* start,
+                      int64_t* end);
+/* Candidate list of one shard: (scores[row][sel[row][i]], start + sel[row][i])
+ * for i < k, padded to nc entries with (-inf, -1).  sel = the shard's local
+ * Top-k (ascending), k = min(n, local tokens). */
+FIER_API int fier_shard_candidates(const float* scores, int32_t rows, int64_t ld, const int32_t* sel, int32_t k,
+                          int32_t nc, int32_t start, float* cand_scores, int32_t* cand_idx, void* stream);
+/* Global Top-n (topk_oracle tie rule) from the all-gathered candidate lists
+ * cand_*[shards][rows][nc]: sel_global[rows][n] (ascending global indices),
+ * and this rank's run as local indices sel_local[rows][0..counts[row]) (each
+ * output may be NULL). */
+FIER_API size_t fier_shard_merge_workspace(int32_t shards, int32_t rows, int32_t nc, int32_t n);
+FIER_API int fier_shard_merge(const float* cand_scores, const int32_t* cand_idx, int32_t shards, int32_t rows,
+                     int32_t nc, int32_t n, int32_t rank, int32_t start, int32_t* sel_global,
+                     int32_t* sel_local, int32_t* counts, void* workspace, size_t workspace_bytes,
+                     void* stream);
+/* Log-sum-exp merge of per-shard partials outs[shards][rows][dim], lses[shards][rows]
+ * (from fier_sparse_attention_ragged) into out[rows][dim] (and lse[rows], may be NULL). */
+FIER_API int fier_lse_merge(const float* outs, const float* lses, int32_t shards, int32_t rows, int32_t dim,
+                   float* out, float* lse, void* stream);
 
 /* ---- host-side format conversion (no GPU) -------------------------------------- */
 /* serialize_packed_keys (io.hpp:197-225) of one (b, kv head) index copied to

@@ -78,7 +78,8 @@ __device__ __forceinline__ void unpack_vec(const uint4& v, float* f) {
 // nsplit*(D+2)) into out[h][D].  Called by one whole CTA; partials written by
 // other CTAs are read with ld.global.cg (L2, not a stale L1).  smem: 2*nsplit floats.
 template <int D>
-__device__ void merge_partials(const float* part, int nsplit, int heads, float* out, float* smem) {
+__device__ void merge_partials(const float* part, int nsplit, int heads, float* out, float* smem,
+                               float* lse) {
     for (int hh = 0; hh < heads; ++hh) {
         const float* pp = part + (int64_t)hh * nsplit * (D + 2);
         for (int sp = threadIdx.x; sp < nsplit; sp += blockDim.x) {
@@ -91,7 +92,9 @@ __device__ void merge_partials(const float* part, int nsplit, int heads, float* 
         float L = 0.f;
         for (int sp = 0; sp < nsplit; ++sp)
             if (smem[sp] != -INFINITY) L += smem[nsplit + sp] * exp2f(smem[sp] - M);
-        const float inv = 1.f / L;
+        // an empty (ragged) selection gives o = 0 and lse = -inf
+        const float inv = L > 0.f ? 1.f / L : 0.f;
+        if (lse && threadIdx.x == 0) lse[hh] = L > 0.f ? M + __log2f(L) : -INFINITY;
         for (int c = threadIdx.x; c < D; c += blockDim.x) {
             float o = 0.f;
 #pragma unroll 4
@@ -129,7 +132,7 @@ __global__ void __launch_bounds__(kAttnWarps * 32) attn_kernel(
     const T* __restrict__ q, const T* __restrict__ K, const T* __restrict__ V,
     const int32_t* __restrict__ sel, int n, int tokens, int cap, int hkv, int hq, float scale_log2,
     int rows_per_cta, float* __restrict__ part, int nsplit, int* __restrict__ counters,
-    float* __restrict__ out) {
+    float* __restrict__ out, const int32_t* __restrict__ counts, float* __restrict__ lse) {
     using TR = AttnTraits<T, D>;
     constexpr int CH = TR::CH, VEC = TR::VEC, EPV = TR::EPV, CPL = TR::CPL, RB = TR::RB;
     constexpr int QSTRIDE = CH + 4;                 // padded per-part q rows (bank spread)
@@ -149,9 +152,9 @@ __global__ void __launch_bounds__(kAttnWarps * 32) attn_kernel(
     const int64_t seq = (int64_t)b * hkv + kvh;
     const T* Kseq = K + seq * cap * D;
     const T* Vseq = V + seq * cap * D;
-    const int total = GATHER ? n : tokens;
+    const int total = GATHER ? (counts ? min(n, counts[(int64_t)b * hq + head]) : n) : tokens;
     const int r_begin = split * rows_per_cta;
-    const int r_end = min(r_begin + rows_per_cta, total);
+    const int r_end = max(r_begin, min(r_begin + rows_per_cta, total));
     const int rpw = (int)((((r_end - r_begin) + kAttnWarps - 1) / kAttnWarps + kRowsPerStage - 1) /
                           kRowsPerStage * kRowsPerStage);
     const int wr0 = min(r_begin + warp * rpw, r_end);
@@ -338,12 +341,12 @@ __global__ void __launch_bounds__(kAttnWarps * 32) attn_kernel(
     if (!s_last) return;
     __threadfence();
     merge_partials<D>(part + ((int64_t)b * hq + qh0) * nsplit * (D + 2), nsplit, HPG,
-                      out + ((int64_t)b * hq + qh0) * D, wres);
+                      out + ((int64_t)b * hq + qh0) * D, wres, lse ? lse + (int64_t)b * hq + qh0 : nullptr);
 }
 
 // LSE merge of nsplit partials per (b, q head): out = sum_s o_s 2^(m_s-M) / sum_s l_s 2^(m_s-M).
 __global__ void merge_kernel(const float* __restrict__ part, int nsplit, int d, int hq,
-                             float* __restrict__ out) {
+                             float* __restrict__ out, float* __restrict__ lse) {
     const int h = blockIdx.x, b = blockIdx.y;
     const float* p = part + ((int64_t)b * hq + h) * nsplit * (d + 2);
     float M = -INFINITY;
@@ -353,7 +356,8 @@ __global__ void merge_kernel(const float* __restrict__ part, int nsplit, int d, 
         const float ms = p[s * (d + 2) + d];
         if (ms != -INFINITY) L += p[s * (d + 2) + d + 1] * exp2f(ms - M);
     }
-    const float inv = 1.f / L;
+    const float inv = L > 0.f ? 1.f / L : 0.f;
+    if (lse && threadIdx.x == 0) lse[(int64_t)b * hq + h] = L > 0.f ? M + __log2f(L) : -INFINITY;
     for (int c = threadIdx.x; c < d; c += blockDim.x) {
         float o = 0.f;
         for (int s = 0; s < nsplit; ++s) {
@@ -370,13 +374,14 @@ template <typename T, bool GATHER>
 __global__ void attn_generic_kernel(const T* __restrict__ q, const T* __restrict__ K,
                                     const T* __restrict__ V, const int32_t* __restrict__ sel, int n,
                                     int tokens, int cap, int d, int hkv, int hq, float scale_log2,
-                                    int rows_per_cta, float* __restrict__ part, int nsplit) {
+                                    int rows_per_cta, float* __restrict__ part, int nsplit,
+                                    const int32_t* __restrict__ counts) {
     const int lane = threadIdx.x;
     const int split = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
     const int kvh = h / (hq / hkv);
     const int64_t seq = (int64_t)b * hkv + kvh;
     const T* qp = q + ((int64_t)b * hq + h) * d;
-    const int total = GATHER ? n : tokens;
+    const int total = GATHER ? (counts ? min(n, counts[(int64_t)b * hq + h]) : n) : tokens;
     const int r0 = split * rows_per_cta, r1 = min(r0 + rows_per_cta, total);
     constexpr int MAXC = 32;  // d <= 1024
     float acc[MAXC];
@@ -441,7 +446,8 @@ static size_t attn_smem() {
 template <typename T, int D, int HPG, bool GATHER>
 static int launch_attn(const fier_shape* s, const void* q, const void* K, const void* V,
                        const int32_t* sel, int n, int tokens, float scale, float* part,
-                       int* counters, float* out, const AttnPlan& p, cudaStream_t st) {
+                       int* counters, float* out, const AttnPlan& p, cudaStream_t st,
+                       const int32_t* counts = nullptr, float* lse = nullptr) {
     constexpr int NST = attn_nst<T, D>();
     auto kern = attn_kernel<T, D, HPG, GATHER, NST>;
     const size_t smem = attn_smem<T, D, HPG, GATHER>();
@@ -451,19 +457,19 @@ static int launch_attn(const fier_shape* s, const void* q, const void* K, const 
     kern<<<grid, kAttnWarps * 32, smem, st>>>(
         static_cast<const T*>(q), static_cast<const T*>(K), static_cast<const T*>(V), sel, n, tokens,
         s->capacity, s->kv_heads, s->q_heads, scale * kLog2e, p.rows_per_cta, part, p.nsplit,
-        counters, out);
+        counters, out, counts, lse);
     return check_launch("attention");
 }
 
 template <typename T, bool GATHER>
 static int launch_generic(const fier_shape* s, const void* q, const void* K, const void* V,
                           const int32_t* sel, int n, int tokens, float scale, float* part,
-                          const AttnPlan& p, cudaStream_t st) {
+                          const AttnPlan& p, cudaStream_t st, const int32_t* counts = nullptr) {
     dim3 grid(p.nsplit, s->q_heads, s->batch);
     attn_generic_kernel<T, GATHER><<<grid, 32, 0, st>>>(
         static_cast<const T*>(q), static_cast<const T*>(K), static_cast<const T*>(V), sel, n, tokens,
         s->capacity, s->dim, s->kv_heads, s->q_heads, scale * kLog2e, p.rows_per_cta, part,
-        p.nsplit);
+        p.nsplit, counts);
     return check_launch("attention");
 }
 
@@ -508,7 +514,7 @@ static int per_sm_typed(const fier_shape* s, bool gather) {
 int tc_resident(const fier_shape* s, bool gather);
 int tc_dispatch(const fier_shape* s, bool gather, const void* q, const void* K, const void* V,
                 const int32_t* sel, int n, int tokens, float scale, float* part, int* counters, float* out,
-                int nsplit, int rows_per_cta, cudaStream_t st);
+                int nsplit, int rows_per_cta, const int32_t* counts, float* lse, cudaStream_t st);
 
 static int resident_per_sm(const fier_shape* s, bool gather) {
     if (const int tc = tc_resident(s, gather)) return tc;
@@ -556,12 +562,12 @@ size_t full_workspace(const fier_shape* s, int tokens) {
 template <typename T>
 static int sparse_typed(const fier_shape* s, const void* q, const void* K, const void* V,
                         const int32_t* sel, int n, int tokens, float scale, float* part, int* ctr,
-                        float* out, const AttnPlan& p, cudaStream_t st) {
+                        float* out, const AttnPlan& p, cudaStream_t st, const int32_t* counts, float* lse) {
     if (s->dim == 128)
-        return launch_attn<T, 128, 1, true>(s, q, K, V, sel, n, tokens, scale, part, ctr, out, p, st);
+        return launch_attn<T, 128, 1, true>(s, q, K, V, sel, n, tokens, scale, part, ctr, out, p, st, counts, lse);
     if (s->dim == 64)
-        return launch_attn<T, 64, 1, true>(s, q, K, V, sel, n, tokens, scale, part, ctr, out, p, st);
-    return launch_generic<T, true>(s, q, K, V, sel, n, tokens, scale, part, p, st);
+        return launch_attn<T, 64, 1, true>(s, q, K, V, sel, n, tokens, scale, part, ctr, out, p, st, counts, lse);
+    return launch_generic<T, true>(s, q, K, V, sel, n, tokens, scale, part, p, st, counts);
 }
 
 template <typename T, int D>
@@ -583,9 +589,10 @@ static int full_typed(const fier_shape* s, const void* q, const void* K, const v
     return launch_generic<T, false>(s, q, K, V, nullptr, 0, tokens, scale, part, p, st);
 }
 
-static int merge(const fier_shape* s, const float* part, int nsplit, float* out, cudaStream_t st) {
+static int merge(const fier_shape* s, const float* part, int nsplit, float* out, cudaStream_t st,
+                 float* lse = nullptr) {
     dim3 grid(s->q_heads, s->batch);
-    merge_kernel<<<grid, 128, 0, st>>>(part, nsplit, s->dim, s->q_heads, out);
+    merge_kernel<<<grid, 128, 0, st>>>(part, nsplit, s->dim, s->q_heads, out, lse);
     return check_launch("attention merge");
 }
 
@@ -593,7 +600,7 @@ static int merge(const fier_shape* s, const float* part, int nsplit, float* out,
 // decode step zeroes them in its append kernel); otherwise a memset node is issued.
 int sparse_dispatch(const fier_shape* s, const void* q, const void* K, const void* V,
                     const int32_t* sel, int n, int tokens, float scale, float* out, void* ws,
-                    bool counters_zeroed, cudaStream_t st) {
+                    bool counters_zeroed, cudaStream_t st, const int32_t* counts, float* lse) {
     const AttnPlan p = sparse_plan(s, n);
     float* part = static_cast<float*>(ws);
     int* ctr = reinterpret_cast<int*>(static_cast<uint8_t*>(ws) + part_bytes(s, p.nsplit));
@@ -603,16 +610,17 @@ int sparse_dispatch(const fier_shape* s, const void* q, const void* K, const voi
         if (e != cudaSuccess) return fail(FIER_ECUDA, std::string("gather_attention: ") + cudaGetErrorString(e));
     }
     if (tc_resident(s, true) > 0)
-        return tc_dispatch(s, true, q, K, V, sel, n, tokens, scale, part, ctr, out, p.nsplit, p.rows_per_cta, st);
+        return tc_dispatch(s, true, q, K, V, sel, n, tokens, scale, part, ctr, out, p.nsplit, p.rows_per_cta,
+                           counts, lse, st);
     int rc = FIER_OK;
     switch (s->dtype) {
-        case FIER_F32: rc = sparse_typed<float>(s, q, K, V, sel, n, tokens, scale, part, ctr, out, p, st); break;
-        case FIER_F16: rc = sparse_typed<__half>(s, q, K, V, sel, n, tokens, scale, part, ctr, out, p, st); break;
-        case FIER_BF16: rc = sparse_typed<__nv_bfloat16>(s, q, K, V, sel, n, tokens, scale, part, ctr, out, p, st); break;
+        case FIER_F32: rc = sparse_typed<float>(s, q, K, V, sel, n, tokens, scale, part, ctr, out, p, st, counts, lse); break;
+        case FIER_F16: rc = sparse_typed<__half>(s, q, K, V, sel, n, tokens, scale, part, ctr, out, p, st, counts, lse); break;
+        case FIER_BF16: rc = sparse_typed<__nv_bfloat16>(s, q, K, V, sel, n, tokens, scale, part, ctr, out, p, st, counts, lse); break;
         default: return fail(FIER_EINVAL, "fier_sparse_attention: unknown dtype");
     }
     if (rc || fused) return rc;
-    return merge(s, part, p.nsplit, out, st);
+    return merge(s, part, p.nsplit, out, st, lse);
 }
 
 int full_dispatch(const fier_shape* s, const void* q, const void* K, const void* V, int tokens,
@@ -627,7 +635,7 @@ int full_dispatch(const fier_shape* s, const void* q, const void* K, const void*
     }
     if (tc_resident(s, false) > 0)
         return tc_dispatch(s, false, q, K, V, nullptr, 0, tokens, scale, part, ctr, out, p.nsplit, p.rows_per_cta,
-                           st);
+                           nullptr, nullptr, st);
     int rc = FIER_OK;
     switch (s->dtype) {
         case FIER_F32: rc = full_typed<float>(s, q, K, V, tokens, scale, part, ctr, out, p, st); break;

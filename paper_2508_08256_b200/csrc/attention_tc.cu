@@ -100,7 +100,7 @@ __global__ void __launch_bounds__(kTcWarps * 32) attn_tc_kernel(
     const T* __restrict__ q, const T* __restrict__ K, const T* __restrict__ V,
     const int32_t* __restrict__ sel, int n, int tokens, int cap, int hkv, int hq, float scale_log2,
     int rows_per_cta, float* __restrict__ part, int nsplit, int* __restrict__ counters,
-    float* __restrict__ out) {
+    float* __restrict__ out, const int32_t* __restrict__ counts, float* __restrict__ lse) {
     static_assert(HPG <= 8, "query rows live in mma rows 0..7");
     constexpr int RB = D * 2;              // bytes per row
     constexpr int CPR = RB / 16;           // 16-byte chunks per row
@@ -119,9 +119,10 @@ __global__ void __launch_bounds__(kTcWarps * 32) attn_tc_kernel(
     const int64_t seq = (int64_t)b * hkv + kvh;
     const T* Kseq = K + seq * cap * D;
     const T* Vseq = V + seq * cap * D;
-    const int total = GATHER ? n : tokens;
+    // ragged selections (sequence-sharded step): row count per (b, q head)
+    const int total = GATHER ? (counts ? min(n, counts[(int64_t)b * hq + head]) : n) : tokens;
     const int r_begin = split * rows_per_cta;
-    const int r_end = min(r_begin + rows_per_cta, total);
+    const int r_end = max(r_begin, min(r_begin + rows_per_cta, total));
     const int rpw = (int)((((r_end - r_begin) + kTcWarps - 1) / kTcWarps + kTcRows - 1) / kTcRows * kTcRows);
     const int wr0 = min(r_begin + warp * rpw, r_end);
     const int wr1 = min(wr0 + rpw, r_end);
@@ -318,7 +319,9 @@ __global__ void __launch_bounds__(kTcWarps * 32) attn_tc_kernel(
         float L = 0.f;
         for (int sp = 0; sp < nsplit; ++sp)
             if (wres[sp] != -INFINITY) L += wres[nsplit + sp] * exp2f(wres[sp] - M);
-        const float inv = 1.f / L;
+        // an empty (ragged) selection gives o = 0 and lse = -inf
+        const float inv = L > 0.f ? 1.f / L : 0.f;
+        if (lse && threadIdx.x == 0) lse[(int64_t)b * hq + qh0 + hh] = L > 0.f ? M + __log2f(L) : -INFINITY;
         for (int c = threadIdx.x; c < D; c += blockDim.x) {
             float oo = 0.f;
 #pragma unroll 4
@@ -358,7 +361,7 @@ int tc_per_sm() {
 template <typename T, int D, int HPG, bool GATHER>
 int launch_attn_tc(const fier_shape* s, const void* q, const void* K, const void* V, const int32_t* sel,
                    int n, int tokens, float scale, float* part, int* counters, float* out, int nsplit,
-                   int rows_per_cta, cudaStream_t st) {
+                   int rows_per_cta, const int32_t* counts, float* lse, cudaStream_t st) {
     auto kern = attn_tc_kernel<T, D, HPG, GATHER, kTcNst>;
     const size_t smem = tc_smem<D, HPG>(kTcNst);
     (void)tc_per_sm<T, D, HPG, GATHER>();  // sets the smem attribute once
@@ -366,7 +369,7 @@ int launch_attn_tc(const fier_shape* s, const void* q, const void* K, const void
     kern<<<grid, kTcWarps * 32, smem, st>>>(static_cast<const T*>(q), static_cast<const T*>(K),
                                             static_cast<const T*>(V), sel, n, tokens, s->capacity,
                                             s->kv_heads, s->q_heads, scale * kLog2e, rows_per_cta, part,
-                                            nsplit, counters, out);
+                                            nsplit, counters, out, counts, lse);
     return check_launch("attention (tensor core)");
 }
 
@@ -394,24 +397,24 @@ int tc_resident(const fier_shape* s, bool gather) {
 
 int tc_dispatch(const fier_shape* s, bool gather, const void* q, const void* K, const void* V,
                 const int32_t* sel, int n, int tokens, float scale, float* part, int* counters, float* out,
-                int nsplit, int rows_per_cta, cudaStream_t st) {
+                int nsplit, int rows_per_cta, const int32_t* counts, float* lse, cudaStream_t st) {
     const int hpg = gather ? 1 : s->q_heads / s->kv_heads;
 #define TC_LAUNCH(TT, DD)                                                                               \
     switch (hpg) {                                                                                      \
         case 1:                                                                                         \
             return gather ? launch_attn_tc<TT, DD, 1, true>(s, q, K, V, sel, n, tokens, scale, part,    \
-                                                            counters, out, nsplit, rows_per_cta, st)    \
+                                                            counters, out, nsplit, rows_per_cta, counts, lse, st)    \
                           : launch_attn_tc<TT, DD, 1, false>(s, q, K, V, sel, n, tokens, scale, part,   \
-                                                             counters, out, nsplit, rows_per_cta, st);  \
+                                                             counters, out, nsplit, rows_per_cta, counts, lse, st);  \
         case 2:                                                                                         \
             return launch_attn_tc<TT, DD, 2, false>(s, q, K, V, sel, n, tokens, scale, part, counters, \
-                                                    out, nsplit, rows_per_cta, st);                     \
+                                                    out, nsplit, rows_per_cta, counts, lse, st);                     \
         case 4:                                                                                         \
             return launch_attn_tc<TT, DD, 4, false>(s, q, K, V, sel, n, tokens, scale, part, counters, \
-                                                    out, nsplit, rows_per_cta, st);                     \
+                                                    out, nsplit, rows_per_cta, counts, lse, st);                     \
         default:                                                                                        \
             return launch_attn_tc<TT, DD, 8, false>(s, q, K, V, sel, n, tokens, scale, part, counters, \
-                                                    out, nsplit, rows_per_cta, st);                     \
+                                                    out, nsplit, rows_per_cta, counts, lse, st);                     \
     }
     if (s->dtype == FIER_BF16) {
         if (s->dim == 128) { TC_LAUNCH(__nv_bfloat16, 128) }

@@ -34,7 +34,7 @@ size_t topk_workspace(int, int, int);
 size_t sparse_workspace(const fier_shape*, int);
 size_t full_workspace(const fier_shape*, int);
 int sparse_dispatch(const fier_shape*, const void*, const void*, const void*, const int32_t*, int, int,
-                    float, float*, void*, bool, cudaStream_t);
+                    float, float*, void*, bool, cudaStream_t, const int32_t*, float*);
 int full_dispatch(const fier_shape*, const void*, const void*, const void*, int, float, float*, void*,
                   cudaStream_t);
 size_t sparse_counter_offset(const fier_shape*, int);
@@ -144,7 +144,22 @@ int fier_sparse_attention(const fier_shape* s, const void* q, const void* K, con
     FIER_REQUIRE(workspace && workspace_bytes >= sparse_workspace(s, n),
                  "gather_attention: workspace too small");
     return sparse_dispatch(s, q, K, V, sel, n, tokens, scale, out, workspace, false,
-                           static_cast<cudaStream_t>(stream));
+                           static_cast<cudaStream_t>(stream), nullptr, nullptr);
+}
+
+int fier_sparse_attention_ragged(const fier_shape* s, const void* q, const void* K, const void* V,
+                                 const int32_t* sel, const int32_t* counts, int32_t n, int32_t tokens,
+                                 float scale, float* out, float* lse, void* workspace,
+                                 size_t workspace_bytes, void* stream) {
+    if (int rc = check_shape(s, "gather_attention")) return rc;
+    FIER_REQUIRE(n >= 1, "gather_attention: empty selection");
+    FIER_REQUIRE(tokens >= 1 && tokens <= s->capacity, "gather_attention: selection invalid for cache");
+    FIER_REQUIRE(q && K && V && sel && counts && out && lse, "gather_attention: null buffer");
+    FIER_REQUIRE(aligned16(K) && aligned16(V), "gather_attention: K/V must be 16-byte aligned");
+    FIER_REQUIRE(workspace && workspace_bytes >= sparse_workspace(s, n),
+                 "gather_attention: workspace too small");
+    return sparse_dispatch(s, q, K, V, sel, n, tokens, scale, out, workspace, false,
+                           static_cast<cudaStream_t>(stream), counts, lse);
 }
 
 size_t fier_full_attention_workspace(const fier_shape* s, int32_t tokens) {
@@ -194,7 +209,7 @@ int fier_decode_step(const fier_shape* s, const void* q, const void* k_new, cons
     if (rc) return rc;
     rc = topk_dispatch(scores, s->batch * s->q_heads, tokens, ld, n, sel, st);
     if (rc) return rc;
-    return sparse_dispatch(s, q, K, V, sel, n, tokens, scale, out, attn_ws, true, st);
+    return sparse_dispatch(s, q, K, V, sel, n, tokens, scale, out, attn_ws, true, st, nullptr, nullptr);
 }
 
 // ---- host-side FIER conversion (io.hpp:197-277) ------------------------------------

@@ -1,0 +1,212 @@
+"""Sequence-sharded Fier decode step (X1; BASELINE config C5).
+
+A long context is split into P contiguous token ranges, one per GPU, whose
+boundaries are whole quantization groups (``fier_shard_bounds``), so each
+shard's packed index is bit-identical to the matching slice of the global
+``quantize`` (quant1bit.hpp:5-9, 84).  One decode step:
+
+  1. every shard appends (only the shard that owns ``pos``), scores its tokens
+     and keeps its local Top-min(n, l_r) as (score, global index) candidates
+     (K1b, K2, K3 and ``fier_shard_candidates``);
+  2. exchange #1 -- all-gather of the candidate lists (rows x n x 8 bytes);
+  3. every shard runs the same deterministic merge (``fier_shard_merge``: K3 on
+     the side-by-side lists, which are in global index order, so the reference
+     tie rule of topk_oracle, core.hpp:134-148, holds globally) and keeps its
+     own run of the global selection;
+  4. ragged K4 over that run -> per-row (o_r, lse_r);
+  5. exchange #2 -- all-gather of the partials (rows x (d+1) floats);
+  6. log-sum-exp merge (``fier_lse_merge``) -> the global output, identical on
+     every rank.
+
+Nothing else crosses GPUs.  The protocol (:func:`sharded_step`) is written
+against two small interfaces -- a *shard* (select_local / attend_local /
+combine) and an *exchange* (all_gather) -- so the same code runs over NCCL
+(one process per GPU, :class:`DistExchange`), over gloo in the CPU tests, and
+over P shards held by one process (:func:`virtual_sharded_step`, single-GPU
+parity at 1M tokens).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+from typing import List, Optional, Sequence, Tuple
+
+import torch
+
+from . import _lib
+from ._lib import check
+from .api import DecodeLayer, _p, _stream, make_shape
+
+
+def shard_bounds(tokens: int, shards: int, group: int) -> List[Tuple[int, int]]:
+    """[start, end) of every shard: whole groups, spread evenly (fier_shard_bounds)."""
+    lib = _lib.load()
+    out = []
+    for r in range(shards):
+        a, b = C.c_int64(), C.c_int64()
+        check(lib.fier_shard_bounds(tokens, shards, group, r, C.byref(a), C.byref(b)))
+        out.append((a.value, b.value))
+    return out
+
+
+class DistExchange:
+    """all_gather over a torch.distributed process group (NCCL on GPUs, gloo on CPU)."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        self.dist = dist
+        self.group = group
+        self.world = dist.get_world_size(group)
+
+    def all_gather(self, t: torch.Tensor) -> torch.Tensor:
+        t = t.contiguous()
+        if t.is_cuda:  # NCCL: one fused all-gather into a [P, ...] buffer
+            out = torch.empty((self.world,) + tuple(t.shape), dtype=t.dtype, device=t.device)
+            self.dist.all_gather_into_tensor(out, t, group=self.group)
+            return out
+        parts = [torch.empty_like(t) for _ in range(self.world)]
+        self.dist.all_gather(parts, t, group=self.group)
+        return torch.stack(parts)
+
+
+def _pack_candidates(cs: torch.Tensor, ci: torch.Tensor) -> torch.Tensor:
+    return torch.stack([cs.view(torch.int32), ci])
+
+
+def _unpack_candidates(g: torch.Tensor) -> Tuple[torch.Tensor, torch.Tensor]:
+    # g: [P, 2, rows, n]
+    return g[:, 0].contiguous().view(torch.float32), g[:, 1].contiguous()
+
+
+def _pack_partial(out: torch.Tensor, lse: torch.Tensor) -> torch.Tensor:
+    return torch.cat([out, lse.unsqueeze(-1)], dim=-1)
+
+
+def _unpack_partial(g: torch.Tensor, d: int) -> Tuple[torch.Tensor, torch.Tensor]:
+    # g: [P, rows, d + 1]
+    return g[..., :d].contiguous(), g[..., d].contiguous()
+
+
+def sharded_step(shard, exchange, q, k_new, v_new, pos: int, n: int) -> torch.Tensor:
+    """One decode step of a sequence-sharded layer; returns out [B, Hq, d] (fp32),
+    identical on every rank.  The two all-gathers are the only communication."""
+    cs, ci = shard.select_local(q, k_new, v_new, pos, n)
+    CS, CI = _unpack_candidates(exchange.all_gather(_pack_candidates(cs, ci)))
+    o, lse = shard.attend_local(q, CS, CI, n)
+    O, LSE = _unpack_partial(exchange.all_gather(_pack_partial(o, lse)), o.shape[-1])
+    return shard.combine(O, LSE)
+
+
+def virtual_sharded_step(shards: Sequence, q, k_new, v_new, pos: int, n: int) -> torch.Tensor:
+    """The same protocol with all P shards in one process (the all-gathers become stacks)."""
+    cands = [_pack_candidates(*s.select_local(q, k_new, v_new, pos, n)) for s in shards]
+    CS, CI = _unpack_candidates(torch.stack(cands))
+    parts = [_pack_partial(*s.attend_local(q, CS, CI, n)) for s in shards]
+    O, LSE = _unpack_partial(torch.stack(parts), shards[0].d)
+    return shards[0].combine(O, LSE)
+
+
+class ShardedDecodeLayer:
+    """Shard ``rank`` of ``shards`` of one attention layer over a context of
+    ``context`` tokens, on this process's GPU.  The local KV cache holds global
+    tokens [start, end) as local rows [0, end - start)."""
+
+    def __init__(self, batch, q_heads, kv_heads, context, dim, group=32, rank=0, shards=1,
+                 dtype=torch.bfloat16, device="cuda", K=None, V=None):
+        self.B, self.Hq, self.Hkv, self.d, self.g = batch, q_heads, kv_heads, dim, group
+        self.rank, self.P, self.context = rank, shards, context
+        self.start, self.end = shard_bounds(context, shards, group)[rank]
+        self.cap = max(self.end - self.start, group)
+        self.device = torch.device(device)
+        self.layer = DecodeLayer(batch, q_heads, kv_heads, self.cap, dim, group, dtype=dtype, device=device,
+                                 K=K, V=V)
+        self.rows = batch * q_heads
+        self.local_tokens = 0
+        self.sel_global: Optional[torch.Tensor] = None
+        self._bufs = {}
+
+    # -- helpers ---------------------------------------------------------------
+    def _buf(self, name, shape, dtype):
+        t = self._bufs.get(name)
+        if t is None or tuple(t.shape) != tuple(shape) or t.dtype != dtype:
+            t = torch.empty(shape, dtype=dtype, device=self.device)
+            self._bufs[name] = t
+        return t
+
+    def _local(self, pos: int) -> int:
+        return min(max(pos + 1 - self.start, 0), self.end - self.start)
+
+    @property
+    def K(self):
+        return self.layer.K
+
+    @property
+    def V(self):
+        return self.layer.V
+
+    def prefill(self, tokens: int) -> None:
+        """Pack this shard's part of the prefix [0, tokens)."""
+        lt = min(max(tokens - self.start, 0), self.end - self.start)
+        if lt > 0:
+            self.layer.prefill(lt)
+        self.local_tokens = lt
+
+    # -- protocol steps -----------------------------------------------------------
+    def select_local(self, q, k_new, v_new, pos: int, n: int):
+        lib = _lib.load()
+        sh = C.byref(self.layer.shape)
+        if self.start <= pos < self.end:
+            check(lib.fier_append(sh, _p(self.layer.K), _p(self.layer.V), _p(k_new), _p(v_new),
+                                  pos - self.start, _p(self.layer.pk.bits), _p(self.layer.pk.params), None,
+                                  _stream()))
+            self.layer.pk.tokens = max(self.layer.pk.tokens, pos - self.start + 1)
+        lt = self._local(pos)
+        self.local_tokens = lt
+        cs = self._buf("cs", (self.rows, n), torch.float32)
+        ci = self._buf("ci", (self.rows, n), torch.int32)
+        k = min(n, lt)
+        if k == 0:
+            check(lib.fier_shard_candidates(None, self.rows, 1, None, 0, n, self.start, _p(cs), _p(ci),
+                                            _stream()))
+            return cs, ci
+        ld = lib.fier_step_scores_ld(lt)
+        scores = self._buf("scores", (self.rows, ld), torch.float32)
+        sel = self._buf(f"sel{k}", (self.rows, k), torch.int32)
+        check(lib.fier_score(sh, _p(q), _p(self.layer.pk.bits), _p(self.layer.pk.params), lt, _p(scores), ld,
+                             _stream()))
+        check(lib.fier_topk(_p(scores), self.rows, lt, ld, k, _p(sel), None, 0, _stream()))
+        check(lib.fier_shard_candidates(_p(scores), self.rows, ld, _p(sel), k, n, self.start, _p(cs), _p(ci),
+                                        _stream()))
+        return cs, ci
+
+    def attend_local(self, q, CS, CI, n: int, scale: Optional[float] = None):
+        lib = _lib.load()
+        P = CS.shape[0]
+        ws = self._buf("mws", (lib.fier_shard_merge_workspace(P, self.rows, n, n),), torch.uint8)
+        self.sel_global = self._buf("selg", (self.B, self.Hq, n), torch.int32)
+        sel_local = self._buf("sell", (self.B, self.Hq, n), torch.int32)
+        counts = self._buf("counts", (self.B, self.Hq), torch.int32)
+        check(lib.fier_shard_merge(_p(CS), _p(CI), P, self.rows, n, n, self.rank, self.start,
+                                   _p(self.sel_global), _p(sel_local), _p(counts), _p(ws), ws.numel(),
+                                   _stream()))
+        out = self._buf("o", (self.B, self.Hq, self.d), torch.float32)
+        lse = self._buf("lse", (self.B, self.Hq), torch.float32)
+        if self.local_tokens == 0:
+            out.zero_()
+            lse.fill_(-math.inf)
+            return out, lse
+        scale = 1.0 / math.sqrt(self.d) if scale is None else scale
+        aws = self._buf("aws", (max(4, lib.fier_sparse_attention_workspace(C.byref(self.layer.shape), n)),),
+                        torch.uint8)
+        check(lib.fier_sparse_attention_ragged(C.byref(self.layer.shape), _p(q), _p(self.layer.K),
+                                               _p(self.layer.V), _p(sel_local), _p(counts), n,
+                                               self.local_tokens, scale, _p(out), _p(lse), _p(aws), aws.numel(),
+                                               _stream()))
+        return out, lse
+
+    def combine(self, O, LSE) -> torch.Tensor:
+        lib = _lib.load()
+        P = O.shape[0]
+        out = torch.empty((self.B, self.Hq, self.d), dtype=torch.float32, device=self.device)
+        check(lib.fier_lse_merge(_p(O), _p(LSE), P, self.rows, self.d, _p(out), None, _stream()))
+        return out

@@ -11,7 +11,7 @@ d = collections.defaultdict(list)
 for r in rows[hi + 1:]:
     if len(r) > vi and r[mi] == "gpu__time_duration.sum":
         v = float(r[vi].replace(",", ""))
-        scale = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3}.get(r[ui], 1.0)
+        scale = {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3}.get(r[ui], 1.0)
         d[r[ki].split("(")[0][:70]].append(v * scale)
 for k, v in d.items():
     print(f"{k:70s} n={len(v):3d} mean={sum(v)/len(v):8.2f} us  min={min(v):8.2f}")
