@@ -24,6 +24,8 @@
 //
 // Generic path: any d, any g, one thread per (token, head).
 #include <algorithm>
+#include <cstdlib>
+#include <string>
 
 #include "pack.cuh"
 
@@ -226,10 +228,28 @@ static int launch_fast(const fier_shape* s, const void* q, const uint32_t* bits,
     return check_launch("fier_score");
 }
 
+bool score_mma_ok(const fier_shape* s);
+int score_mma_dispatch(const fier_shape* s, const void* q, const uint32_t* bits, const void* params, int tokens,
+                       float* scores, int64_t ld, void* K, void* V, const void* k_new, const void* v_new, int pos,
+                       int* zero_words, int zero_n, cudaStream_t st);
+
+// FIER_SCORE_KERNEL=cuda_core selects the CUDA-core kernel (A/B measurements only)
+static bool use_cuda_core_scorer() {
+    static const bool v = [] {
+        const char* e = getenv("FIER_SCORE_KERNEL");
+        return e && std::string(e) == "cuda_core";
+    }();
+    return v;
+}
+
 template <typename T>
 static int launch_score(const fier_shape* s, const void* q, const uint32_t* bits, const void* params,
                         int tokens, float* scores, int64_t ld, const AppendArgs& ap, cudaStream_t st) {
     const int hpg = s->q_heads / s->kv_heads;
+    // MHA: the CUDA-core kernel is still ahead of the tensor-core one (ncu, profiles/)
+    if (score_mma_ok(s) && hpg > 1 && !use_cuda_core_scorer())
+        return score_mma_dispatch(s, q, bits, params, tokens, scores, ld, ap.K, ap.V, ap.k_new, ap.v_new, ap.pos,
+                                  ap.zero_words, ap.zero_n, st);
     if (s->dim == 128 && s->group % 32 == 0 && (hpg == 1 || hpg == 2 || hpg == 4 || hpg == 8)) {
         switch (hpg) {
             case 1: return launch_fast<T, 1>(s, q, bits, params, tokens, scores, ld, ap, st);

@@ -278,3 +278,52 @@ def test_c2_shape_step_properties(cuda, port):
         assert port.recall(sel_np[h], port.topk(ref_scores, n)) >= 0.999
         ref_out = port.gather_attention(qd, Kh, Vh, sel_np[h].astype(np.int64))
         assert port.relative_l2_error(out[0, h].cpu().numpy(), ref_out) < OUT_TOL
+
+
+@pytest.mark.parametrize("hpg", [1, 2, 4, 8])
+@pytest.mark.parametrize("g,L,dtype", [(32, 1000, "bf16"), (64, 777, "f16"), (128, 2085, "f32"),
+                                       (32, 31, "bf16"), (32, 8193, "bf16")])
+def test_score_tensor_core_shapes(cuda, port, hpg, g, L, dtype):
+    """K2 (tensor-core exponent-bit scorer, d = 128): every GQA ratio, g in {32, 64, 128},
+    ragged token counts, against approx_scores over the FIER round trip."""
+    F = fier()
+    torch.manual_seed(hpg * 1000 + L)
+    dt, Hkv, B, d = TDT[dtype], 2, 2, 128
+    K = (torch.randn(B, Hkv, L, d, device=cuda) * 3).to(dt)
+    q = torch.randn(B, Hkv * hpg, d, device=cuda).to(dt)
+    pk = F.quantize(K, g)
+    s = F.approx_scores(q, pk).cpu().numpy().astype(np.float64)
+    for b in range(B):
+        for h in range(Hkv * hpg):
+            kv = h // hpg
+            buf = pk.to_fier(b, kv)
+            ref = port.approx_scores_fier(q[b, h].double().cpu().numpy(), buf)
+            assert score_err(s[b, h], ref) <= SCORE_TOL, (b, h)
+
+
+@pytest.mark.parametrize("hpg,g,pos", [(1, 32, 4100), (4, 32, 4127), (4, 64, 4097), (8, 128, 4000),
+                                       (2, 32, 31), (1, 32, 0)])
+def test_fused_append_score_tensor_core(cuda, port, hpg, g, pos):
+    """The decode step's fused append + score: open group re-packed, then scored by the same CTA."""
+    F = fier()
+    torch.manual_seed(pos + hpg)
+    B, Hkv, d, cap, n = 1, 4, 128, 4200, 1
+    dt = torch.bfloat16
+    layer = F.DecodeLayer(B, Hkv * hpg, Hkv, cap, d, g, dtype=dt, device=cuda)
+    layer.K.copy_(torch.randn(B, Hkv, cap, d, device=cuda).to(dt))
+    layer.V.copy_(torch.randn(B, Hkv, cap, d, device=cuda).to(dt))
+    if pos > 0:
+        layer.prefill(pos)
+    q = torch.randn(B, Hkv * hpg, d, device=cuda).to(dt)
+    kn = torch.randn(B, Hkv, d, device=cuda).to(dt)
+    ld = pos + 1 + (-(pos + 1)) % 32
+    scores = torch.empty(B, Hkv * hpg, ld, device=cuda)
+    layer.step(q, kn, kn, pos, n, scores_out=scores)
+    torch.cuda.synchronize()
+    sc = scores.cpu().numpy().astype(np.float64)
+    for h in range(Hkv * hpg):
+        kv = h // hpg
+        buf = layer.pk.to_fier(0, kv)
+        assert buf == port.quantize_fier(layer.K[0, kv, :pos + 1].double().cpu().numpy(), g)
+        ref = port.approx_scores_fier(q[0, h].double().cpu().numpy(), buf)
+        assert score_err(sc[0, h, :pos + 1], ref) <= SCORE_TOL, h
