@@ -327,3 +327,32 @@ def test_fused_append_score_tensor_core(cuda, port, hpg, g, pos):
         assert buf == port.quantize_fier(layer.K[0, kv, :pos + 1].double().cpu().numpy(), g)
         ref = port.approx_scores_fier(q[0, h].double().cpu().numpy(), buf)
         assert score_err(sc[0, h, :pos + 1], ref) <= SCORE_TOL, h
+
+
+@pytest.mark.parametrize("rows,l,k", [(32, 32768, 3604), (32, 131072, 4096), (200, 32768, 3604), (8, 8192, 1),
+                                      (4, 262144, 28835), (16, 32768, 32768)])
+def test_topk_register_path_shapes(cuda, port, rows, l, k):
+    """K3 at the bench shapes (cluster sizes 1..8) plus value distributions that stress
+    each branch: clustered candidates (refinement), exact-tie plateaus at the threshold,
+    outliers stretching the range, and -inf padding (the shard merge)."""
+    F = fier()
+    g = torch.Generator(device="cpu").manual_seed(rows * 7 + l)
+    s = torch.randn(rows, l, generator=g) * 20
+    s[1] = torch.round(s[1])                             # ties everywhere
+    s[2, :] = 1.0
+    s[2, ::97] = 2.0                                     # a plateau straddling the k-th value
+    if rows > 3:
+        s[3, 5] = 3e38
+        s[3, 6] = -3e38                                  # range blow-up -> candidates cluster
+    if rows > 4:
+        s[4, l // 3:] = -float("inf")                    # padding
+        s[4, : l // 3] = torch.round(s[4, : l // 3] * 8) / 8
+    if rows > 5:
+        s[5] = 1e-3 * torch.randn(l, generator=g) + 5.0  # narrow band
+    sel = F.topk_oracle(s.to(cuda), k).cpu().numpy()
+    for r in range(min(rows, 8)):
+        np.testing.assert_array_equal(sel[r], port.topk(s[r].double().numpy(), k), err_msg=f"row {r}")
+    if rows > 8:  # remaining rows: cheap structural checks + a sample against the oracle
+        assert (np.diff(sel, axis=1) > 0).all()
+        for r in range(8, rows, max(1, rows // 16)):
+            np.testing.assert_array_equal(sel[r], port.topk(s[r].double().numpy(), k))
