@@ -532,6 +532,10 @@ AttnPlan sparse_plan(const fier_shape* s, int n) {
         p.rows_per_cta = (int)ceil_div(ceil_div(n, kMaxSplit), 32) * 32;
         p.nsplit = (int)ceil_div(n, p.rows_per_cta);
     }
+    if (p.rows_per_cta > 2048) {  // the tensor-core kernel stages <= 2048 indices per CTA
+        p.rows_per_cta = 2048;
+        p.nsplit = (int)ceil_div(n, p.rows_per_cta);
+    }
     return p;
 }
 

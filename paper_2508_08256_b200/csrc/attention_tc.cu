@@ -18,72 +18,12 @@
 //                                         B = V via ldmatrix.trans
 // Warp states are merged per CTA, CTA partials by log-sum-exp (the last CTA of
 // each head merges), exactly like attention.cu.
-#include "common.cuh"
+#include "mma.cuh"
 
 namespace fier_cuda {
 
 constexpr int kTcWarps = 4;
 constexpr int kTcRows = 16;  // rows per stage
-
-template <typename T>
-struct MmaType;
-template <>
-struct MmaType<__nv_bfloat16> {
-    static constexpr const char* name = "bf16";
-};
-template <>
-struct MmaType<__half> {
-    static constexpr const char* name = "f16";
-};
-
-__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
-    asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
-                 : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
-                 : "r"(addr));
-}
-__device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
-    asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
-                 : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
-                 : "r"(addr));
-}
-
-template <typename T>
-__device__ __forceinline__ void mma16816(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
-                                         uint32_t b0, uint32_t b1) {
-    if constexpr (std::is_same<T, __nv_bfloat16>::value) {
-        asm volatile(
-            "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
-            "{%0,%1,%2,%3};"
-            : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
-            : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
-    } else {
-        asm volatile(
-            "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
-            "{%0,%1,%2,%3};"
-            : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
-            : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
-    }
-}
-
-// two floats -> packed 16-bit pair (lo in the low half), RNE
-template <typename T>
-__device__ __forceinline__ uint32_t pack2(float lo, float hi) {
-    if constexpr (std::is_same<T, __nv_bfloat16>::value) {
-        __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
-        return *reinterpret_cast<uint32_t*>(&v);
-    } else {
-        __half2 v = __floats2half2_rn(lo, hi);
-        return *reinterpret_cast<uint32_t*>(&v);
-    }
-}
-template <typename T>
-__device__ __forceinline__ float2 unpack2(uint32_t w) {
-    if constexpr (std::is_same<T, __nv_bfloat16>::value) {
-        return make_float2(__uint_as_float(w << 16), __uint_as_float(w & 0xFFFF0000u));
-    } else {
-        return __half22float2(*reinterpret_cast<const __half2*>(&w));
-    }
-}
 
 __device__ __forceinline__ void cp_async16_tc(uint32_t smem, const void* gmem) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem), "l"(gmem) : "memory");
@@ -93,6 +33,12 @@ __device__ __forceinline__ void cp_async16_tc(uint32_t smem, const void* gmem) {
 template <int RB>
 __device__ __forceinline__ uint32_t swz(int r, int c) {
     return (uint32_t)(r * RB + ((c ^ (r & 7)) << 4));
+}
+
+// wres must also hold the 2 * nsplit (<= 2 * 256) merge weights
+template <int D, int HPG>
+__host__ __device__ constexpr int tc_wres_floats() {
+    return kTcWarps * HPG * (D + 2) > 512 ? kTcWarps * HPG * (D + 2) : 512;
 }
 
 template <typename T, int D, int HPG, bool GATHER, int NST>
@@ -111,6 +57,8 @@ __global__ void __launch_bounds__(kTcWarps * 32) attn_tc_kernel(
 
     extern __shared__ __align__(128) uint8_t smem[];
     float* wres = reinterpret_cast<float*>(smem + (size_t)kTcWarps * NST * 2 * STAGE);  // [warp][HPG][D+2]
+    // the CTA's selected token indices, staged once (keeps index loads off the gather's critical path)
+    int32_t* sidx = reinterpret_cast<int32_t*>(wres + tc_wres_floats<D, HPG>());
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int g = lane >> 2, t = lane & 3;
@@ -129,6 +77,19 @@ __global__ void __launch_bounds__(kTcWarps * 32) attn_tc_kernel(
     const int nstages = (wr1 - wr0 + kTcRows - 1) / kTcRows;
     const int32_t* selrow = GATHER ? sel + ((int64_t)b * hq + head) * n : nullptr;
     const int qh0 = GATHER ? head : head * HPG;
+    if constexpr (GATHER) {
+        // one round of (mostly 16-byte) loads; r_begin is a multiple of 32 and n rows are contiguous
+        const int cnt = r_end - r_begin;
+        const bool vec = ((reinterpret_cast<uintptr_t>(selrow + r_begin) & 15) == 0);
+        if (vec) {
+            for (int i = threadIdx.x; i < cnt / 4; i += blockDim.x)
+                reinterpret_cast<int4*>(sidx)[i] = __ldg(reinterpret_cast<const int4*>(selrow + r_begin) + i);
+            for (int i = (cnt & ~3) + threadIdx.x; i < cnt; i += blockDim.x) sidx[i] = __ldg(selrow + r_begin + i);
+        } else {
+            for (int i = threadIdx.x; i < cnt; i += blockDim.x) sidx[i] = __ldg(selrow + r_begin + i);
+        }
+        __syncthreads();
+    }
 
     // A fragments of Q (row m = query head m of the group; rows >= HPG zero)
     uint32_t qa[KSTEPS][2];
@@ -152,7 +113,7 @@ __global__ void __launch_bounds__(kTcWarps * 32) attn_tc_kernel(
             const int nr = min(kTcRows, wr1 - r0);
             int tok = 0;
             if constexpr (GATHER) {
-                if (lane < nr) tok = __ldg(selrow + r0 + lane);
+                if (lane < nr) tok = sidx[r0 - r_begin + lane];
             }
 #pragma unroll
             for (int i = 0; i < CPL; ++i) {
@@ -338,11 +299,12 @@ __global__ void __launch_bounds__(kTcWarps * 32) attn_tc_kernel(
 
 // ---- host side -------------------------------------------------------------------
 
+constexpr int kTcMaxRowsPerCta = 2048;  // staged selection indices per CTA (sparse_plan caps rows_per_cta)
+
 template <int D, int HPG>
 constexpr size_t tc_smem(int nst) {
-    // wres must also hold the 2 * nsplit (<= 2 * 256) merge weights
-    return (size_t)kTcWarps * nst * 2 * kTcRows * D * 2 +
-           (size_t)(kTcWarps * HPG * (D + 2) > 512 ? kTcWarps * HPG * (D + 2) : 512) * 4;
+    return (size_t)kTcWarps * nst * 2 * kTcRows * D * 2 + (size_t)tc_wres_floats<D, HPG>() * 4 +
+           (size_t)kTcMaxRowsPerCta * 4;
 }
 
 constexpr int kTcNst = 3;

@@ -137,6 +137,7 @@ int fier_sparse_attention(const fier_shape* s, const void* q, const void* K, con
                           void* workspace, size_t workspace_bytes, void* stream) {
     if (int rc = check_shape(s, "gather_attention")) return rc;
     FIER_REQUIRE(n >= 1, "gather_attention: empty selection");
+    FIER_REQUIRE(n <= (1 << 19), "gather_attention: selection longer than 2^19 rows");
     FIER_REQUIRE(tokens >= 1 && tokens <= s->capacity && n <= tokens,
                  "gather_attention: selection invalid for cache");
     FIER_REQUIRE(q && K && V && sel && out, "gather_attention: null buffer");

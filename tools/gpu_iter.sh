@@ -1,3 +1,2 @@
-timeout 900 python -m pytest tests/test_kernels_gpu.py tests/test_shard.py -x -q 2>&1 | tail -3
-for c in c2 c3 c4; do timeout 300 python tools/kbench.py --config $c 2>&1 | grep -E "topk|score"; done
-for cl in 2 4; do echo cluster $cl; FIER_TOPK_CLUSTER=$cl timeout 300 python tools/kbench.py --config c2 2>&1 | grep topk; done
+timeout 600 ncu --set full --clock-control none -k regex:gather_cpasync -s 3 -c 1 -o gpurun_out/prof_gprobe ./tools/gather_probe > /dev/null 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:attn_ws -s 4 -c 1 -o gpurun_out/prof_ws_c2 python tools/kbench.py --config c2 --reps 3 --layers 2 > /dev/null 2>&1
