@@ -45,8 +45,11 @@ CONFIGS = {
                desc="C3: Llama-3-8B GQA layer (32 q / 8 kv), d=128, 128k ctx, n=4096, batch 1, bf16"),
     "c4": dict(B=32, Hq=32, Hkv=8, L=32768, d=128, n=3604, g=32, dtype="bf16",
                desc="C4: batched decode, batch 32, 32k ctx, Llama-3-8B GQA shape, 11% budget, bf16"),
+    "c5": dict(B=1, Hq=32, Hkv=8, L=1048576, d=128, n=4096, g=32, dtype="bf16",
+               desc="C5: 1M-token context, Llama-3-8B GQA layer, n=4096, sequence-sharded over the GPUs "
+                    "(per-shard Top-k + candidate all-gather + LSE merge over NVLink)"),
 }
-KERNELS_PER_STEP = 5  # append, score, top-k, sparse attention, LSE merge
+KERNELS_PER_STEP = 3  # append+score (fused), top-k, sparse attention (+ in-kernel LSE merge)
 
 
 def peaks():
@@ -246,50 +249,69 @@ def run_ours(args, cfg, world, rank, local):
     ms = max_over_ranks(ms, world)
     us_per_step = ms * 1000.0 / args.steps
 
-    # ---- per-kernel breakdown (events between the same C-ABI launches, same stream) ----
+    # ---- per-kernel breakdown: each C-ABI kernel alone, `reps` launches captured in one
+    # CUDA graph rotating over the layer instances (no host gaps), CUDA events on `stream` ----
+    import ctypes as C
     ld = lib.fier_step_scores_ld(pos + 1)
     scores = [torch.empty((B, Hq, ld), dtype=torch.float32, device=dev) for _ in range(n_layers)]
-    part_bytes = lib.fier_sparse_attention_workspace(__import__("ctypes").byref(layers[0].shape), n)
-    parts = [torch.empty(part_bytes, dtype=torch.uint8, device=dev) for _ in range(n_layers)]
-    names = ["append", "score", "topk", "sparse_attn"]
-    reps = max(3 * n_layers, 30)
-    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(reps)]
-    import ctypes as C
-    for r in range(reps + n_layers):
-        li = r % n_layers
-        lay, (q, kn, vn) = layers[li], inputs[li]
-        sh = C.byref(lay.shape)
-        e = ev[r - n_layers] if r >= n_layers else None
-        if e: e[0].record(stream)
-        _lib.check(lib.fier_append(sh, _p(lay.K), _p(lay.V), _p(kn), _p(vn), pos, _p(lay.pk.bits),
-                                   _p(lay.pk.params), None, _stream()))
-        if e: e[1].record(stream)
-        _lib.check(lib.fier_score(sh, _p(q), _p(lay.pk.bits), _p(lay.pk.params), pos + 1, _p(scores[li]),
-                                  ld, _stream()))
-        if e: e[2].record(stream)
-        _lib.check(lib.fier_topk(_p(scores[li]), B * Hq, pos + 1, ld, n, _p(sels[li]), None, 0, _stream()))
-        if e: e[3].record(stream)
-        _lib.check(lib.fier_sparse_attention(sh, _p(q), _p(lay.K), _p(lay.V), _p(sels[li]), n, pos + 1,
-                                             1.0 / math.sqrt(d), _p(outs[li]), _p(parts[li]),
-                                             parts[li].numel(), _stream()))
-        if e: e[4].record(stream)
-    torch.cuda.synchronize()
-    per = {k: statistics.mean(ev[r][i].elapsed_time(ev[r][i + 1]) * 1000.0 for r in range(reps))
-           for i, k in enumerate(names)}
-
-    # ---- K0: in-house full-KV decode attention on the same caches ----
-    fws = torch.empty(lib.fier_full_attention_workspace(C.byref(layers[0].shape), pos + 1),
+    part_bytes = lib.fier_sparse_attention_workspace(C.byref(layers[0].shape), n)
+    parts = [torch.zeros(part_bytes, dtype=torch.uint8, device=dev) for _ in range(n_layers)]
+    fws = torch.zeros(lib.fier_full_attention_workspace(C.byref(layers[0].shape), pos + 1),
                       dtype=torch.uint8, device=dev)
-    for i in range(max(args.warmup, n_layers)):
-        layers[i % n_layers].full_step(inputs[i % n_layers][0], pos + 1, out=outs[i % n_layers], ws=fws)
-    torch.cuda.synchronize()
-    fsteps = max(n_layers * 4, min(args.steps, 400))
-    e0.record(stream)
-    for i in range(fsteps):
-        layers[i % n_layers].full_step(inputs[i % n_layers][0], pos + 1, out=outs[i % n_layers], ws=fws)
-    e1.record(stream)
-    torch.cuda.synchronize()
-    full_us = e0.elapsed_time(e1) * 1000.0 / fsteps
+
+    def k_append(li):
+        lay, (q, kn, vn) = layers[li], inputs[li]
+        _lib.check(lib.fier_append(C.byref(lay.shape), _p(lay.K), _p(lay.V), _p(kn), _p(vn), pos,
+                                   _p(lay.pk.bits), _p(lay.pk.params), None, _stream()))
+
+    def k_score(li):
+        lay, (q, _, _) = layers[li], inputs[li]
+        _lib.check(lib.fier_score(C.byref(lay.shape), _p(q), _p(lay.pk.bits), _p(lay.pk.params), pos + 1,
+                                  _p(scores[li]), ld, _stream()))
+
+    def k_topk(li):
+        _lib.check(lib.fier_topk(_p(scores[li]), B * Hq, pos + 1, ld, n, _p(sels[li]), None, 0, _stream()))
+
+    def k_attn(li):
+        lay, (q, _, _) = layers[li], inputs[li]
+        _lib.check(lib.fier_sparse_attention(C.byref(lay.shape), _p(q), _p(lay.K), _p(lay.V), _p(sels[li]), n,
+                                             pos + 1, 1.0 / math.sqrt(d), _p(outs[li]), _p(parts[li]),
+                                             parts[li].numel(), _stream()))
+
+    def k_full(li):
+        lay, (q, _, _) = layers[li], inputs[li]
+        _lib.check(lib.fier_full_attention(C.byref(lay.shape), _p(q), _p(lay.K), _p(lay.V), pos + 1,
+                                           1.0 / math.sqrt(d), _p(outs[li]), _p(fws), fws.numel(), _stream()))
+
+    def graph_time(fn, reps):
+        """Average device time of one launch: `reps` launches (rotating layers) in one graph."""
+        for li in range(n_layers):
+            fn(li)
+        torch.cuda.synchronize()
+        gph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(gph, stream=stream):
+            for r in range(reps):
+                fn(r % n_layers)
+        gph.replay()
+        torch.cuda.synchronize()
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        best = []
+        for _ in range(3):
+            s0.record(stream)
+            gph.replay()
+            s1.record(stream)
+            torch.cuda.synchronize()
+            best.append(s0.elapsed_time(s1) * 1000.0 / reps)
+        return statistics.median(best)
+
+    kreps = max(4 * n_layers, 40)
+    for li in range(n_layers):  # scores/selections of every layer for the isolated K3/K4 runs
+        k_score(li)
+        k_topk(li)
+    per = {"append": graph_time(k_append, kreps), "score": graph_time(k_score, kreps),
+           "topk": graph_time(k_topk, kreps), "sparse_attn": graph_time(k_attn, kreps)}
+    # ---- K0: in-house full-KV decode attention on the same caches (the speedup baseline) ----
+    full_us = graph_time(k_full, max(2 * n_layers, 20))
 
     # ---- e2e: public API with host buffers, H2D + step + D2H inside the timed region ----
     hq_in = [tuple(t.cpu().pin_memory() for t in inp) for inp in inputs]
@@ -334,11 +356,17 @@ def run_ours(args, cfg, world, rank, local):
     es = elem_size(cfg["dtype"])
     alg = {
         "score": packed + B * Hq * d * es,
-        "sparse_attn": B * Hq * n * d * 2 * es + qo,
+        # U = unique selected (kv head, token) rows (the GQA q heads of a group share
+        # rows through L2); U = B*Hq*n for MHA
+        "sparse_attn": unique_rows * d * 2 * es + qo,
         "append": B * Hkv * (g * d * es + 2 * d * es + g * d // 8 + d * 4),
         "topk": None,
     }
     dom = max(per, key=per.get)
+    gather_ceiling = None
+    gpath = os.path.join(ROOT, "profiles", "gather_ceiling.json")
+    if os.path.exists(gpath):
+        gather_ceiling = json.load(open(gpath)).get("cold_l2_gbs")
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tpath):
@@ -349,6 +377,11 @@ def run_ours(args, cfg, world, rank, local):
         roof = {"bound": "hbm", "kernel": dom, "achieved": round(ach, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(ach / peak, 4), "traffic": traffic, "alg_bytes": alg[dom],
                 "peak_source": peak_src}
+        if dom == "sparse_attn" and gather_ceiling:
+            # random 256-B row gathers at this density cap below the copy peak on B200
+            # (tools/gather_probe.cu, profiles/gather_ceiling.json)
+            roof["gather_ceiling_gbs"] = gather_ceiling
+            roof["frac_of_gather_ceiling"] = round(ach / gather_ceiling, 4)
     pk_u, kv_u, qo_u = algorithmic_bytes(cfg, unique_rows)
     step_bytes = packed + kvb + qo
     step_gbs = step_bytes / (us_per_step * 1e-6) / 1e9
@@ -370,6 +403,47 @@ def run_ours(args, cfg, world, rank, local):
     # data for the CPU baseline: layer 0's caches and step-0 query, exactly as the GPU saw them
     res["_cpu_inputs"] = (layers[0].K, layers[0].V, inputs[0])
     return us_per_step, ms, res
+
+
+def run_sharded(args, cfg, world, rank, local):
+    """C5 over N > 1 GPUs: the context is sequence-sharded (whole groups per rank); every step
+    runs shard-local append/score/Top-k, one NCCL all-gather of the (score, index) candidates,
+    the global merge, ragged K4 and a second all-gather of the (o, lse) partials
+    (paper_2508_08256_b200.shard.sharded_step).  Eager launches; time = max over ranks."""
+    import torch
+
+    from paper_2508_08256_b200.shard import DistExchange, ShardedDecodeLayer, sharded_step
+
+    dev = torch.device("cuda", local)
+    B, Hq, Hkv, L, d, n, g = (cfg[k] for k in ("B", "Hq", "Hkv", "L", "d", "n", "g"))
+    dt = {"bf16": torch.bfloat16, "f16": torch.float16, "f32": torch.float32}[cfg["dtype"]]
+    shard = ShardedDecodeLayer(B, Hq, Hkv, L, d, g, rank=rank, shards=world, dtype=dt, device=dev)
+    gen = torch.Generator(device=dev).manual_seed(1234 + rank)
+    shard.K.copy_(torch.randn(shard.K.shape, generator=gen, device=dev).to(dt))
+    shard.V.copy_(torch.randn(shard.V.shape, generator=gen, device=dev).to(dt))
+    gq = torch.Generator(device=dev).manual_seed(99)  # identical query / new token on every rank
+    q = torch.randn((B, Hq, d), generator=gq, device=dev).to(dt)
+    kn = torch.randn((B, Hkv, d), generator=gq, device=dev).to(dt)
+    vn = torch.randn((B, Hkv, d), generator=gq, device=dev).to(dt)
+    pos = L - 1
+    shard.prefill(pos)
+    ex = DistExchange()
+    for _ in range(args.warmup):
+        sharded_step(shard, ex, q, kn, vn, pos, n)
+    torch.cuda.synchronize()
+    barrier(world)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    sampler = ClockSampler(local)
+    with sampler:
+        e0.record()
+        for _ in range(args.steps):
+            sharded_step(shard, ex, q, kn, vn, pos, n)
+        e1.record()
+        torch.cuda.synchronize()
+    barrier(world)
+    us = max_over_ranks(e0.elapsed_time(e1), world) * 1000.0 / args.steps
+    return us, sampler.summary()
 
 
 def cpu_baseline(cfg, K, V, inp, budget_s=20.0):
@@ -503,6 +577,22 @@ def main():
             print(json.dumps(out))
         return
 
+    if world > 1 and args.config == "c5":
+        us, clocks = run_sharded(args, cfg, world, rank, local)
+        if rank == 0:
+            packed, kvb, qo = algorithmic_bytes(cfg)
+            print(json.dumps({
+                "metric": METRIC, "value": round(us, 3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": round(us / 1000.0, 6), "higher_is_better": False,
+                "scaling": "strong", "vs_baseline": None, "dtype": cfg["dtype"],
+                "data": "synthetic random-init Q/K/V (torch Philox), prefix index pre-packed",
+                "config": dict(config_block(args, cfg, world), parallelism=f"sequence-sharded x{world} (NCCL)"),
+                "roofline": None, "cpu_baseline": None, "e2e": None,
+                "gpu_launches": args.steps * (4 + 3 + 1) * 1, "clocks": clocks,
+                "alg_bytes_per_step": packed + kvb + qo}))
+        import torch.distributed as dist
+        dist.destroy_process_group()
+        return
     us, ms, res = run_ours(args, cfg, world, rank, local)
     K, V, inp = res.pop("_cpu_inputs")
     if rank == 0:

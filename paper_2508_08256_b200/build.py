@@ -79,6 +79,22 @@ def build(force: bool = False, verbose: bool = False) -> str:
     return OUT
 
 
+SHIM_SRC = os.path.join(ROOT, "tests", "cpp", "shim_test.cpp")
+SHIM_BIN = os.path.join(ROOT, "tests", "cpp", "shim_test")
+
+
+def build_shim_test() -> str:
+    """Host C++ driver of include/fier_cuda.hpp (the C++ drop-in), linked to the in-tree library."""
+    build()
+    if os.path.exists(SHIM_BIN) and os.path.getmtime(SHIM_BIN) > max(
+            os.path.getmtime(f) for f in (SHIM_SRC, OUT, os.path.join(ROOT, "include", "fier_cuda.hpp"))):
+        return SHIM_BIN
+    subprocess.run([nvcc(), *ARCH, "-std=c++17", "-O2", "-I" + os.path.join(ROOT, "include"), SHIM_SRC,
+                    "-L" + PKG, "-lfier_cuda", "-Xlinker", "-rpath=$ORIGIN/../../paper_2508_08256_b200",
+                    "-o", SHIM_BIN], check=True)
+    return SHIM_BIN
+
+
 def dump_sass(path: str) -> None:
     cuobjdump = os.path.join(os.path.dirname(nvcc()), "cuobjdump")
     with open(path, "w") as f:

@@ -150,3 +150,51 @@ def test_sass_has_no_odd_memory_descriptor_registers():
     sass = subprocess.run([tool, "-sass", _lib.LIB_PATH], capture_output=True, text=True, check=True).stdout
     assert "LDGSTS" in sass
     assert not re.search(r"desc\[UR\d*[13579]\]", sass)
+
+
+def _read_blobs(path):
+    out = []
+    with open(path, "rb") as f:
+        data = f.read()
+    off = 0
+    dtypes = [np.float64, np.float64, np.float64, np.uint64, np.float64, np.float64, np.float64, np.int64,
+              np.float64, np.int64, np.float64, np.uint8, np.uint8]
+    for dt in dtypes:
+        n = int(np.frombuffer(data[off:off + 8], np.uint64)[0])
+        off += 8
+        nbytes = n * np.dtype(dt).itemsize
+        out.append(np.frombuffer(data[off:off + nbytes], dt).copy())
+        off += nbytes
+    return out
+
+
+@pytest.mark.gpu
+def test_cpp_shim_matches_oracle(cuda, port, tmp_path):
+    """Host C++ through include/fier_cuda.hpp (fier::cuda::quantize / approx_scores /
+    topk_oracle / gather_attention / fier_select / fier_attend) against the oracle."""
+    import subprocess
+    from paper_2508_08256_b200 import build as b
+    exe = b.SHIM_BIN
+    if not os.path.exists(exe):
+        exe = b.build_shim_test()
+    res = str(tmp_path / "shim.bin")
+    r = subprocess.run([exe, res], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0, r.stderr
+    K, V, q, cw, s, z, est, sel, out, sel2, out2, e1, e2 = _read_blobs(res)
+    l, d, g, n = 1000, 128, 32, 77
+    K, V = K.reshape(l, d), V.reshape(l, d)
+    cw_ref, s_ref, z_ref = port.quantize(K, g)
+    assert np.array_equal(cw, cw_ref)  # bit-exact code words
+    rh = np.vectorize(lambda x: port.half_to_double(port.double_to_half(x)))
+    assert np.array_equal(s, rh(s_ref)) and np.array_equal(z, rh(z_ref))  # == round_through_half
+    buf = port.serialize(l, d, g, cw, s, z)
+    assert buf == port.quantize_fier(K, g)  # serialize_packed_keys byte-identical
+    ref_scores = port.approx_scores_fier(q, buf)
+    assert np.max(np.abs(est - ref_scores) / np.maximum(1, np.abs(ref_scores))) <= 1e-3
+    assert np.array_equal(sel, port.topk(est, n))
+    assert np.array_equal(sel2, sel)
+    want = port.gather_attention(q, K, V, sel)
+    assert port.relative_l2_error(out, want) < 1e-2
+    assert port.relative_l2_error(out2, want) < 1e-2
+    assert bytes(e1).decode() == "topk_oracle: k out of range"
+    assert bytes(e2).decode() == "fier_select: budget out of range"

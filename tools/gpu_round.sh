@@ -1,11 +1,15 @@
+# Round measurement: GPU tests, smoke, bench lines for every config, launch list and
+# per-kernel ncu captures of the C2 step (copied into profiles/ afterwards).
 set -x
-nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv
-timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -15 > gpurun_out/pytest_gpu.log
-cat gpurun_out/pytest_gpu.log
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; tail -3 gpurun_out/smoke.log
-for c in c2 c1 c3 c4; do timeout 600 python bench.py --config $c --steps 400 --warmup 10 > gpurun_out/bench_$c.json 2> gpurun_out/bench_$c.err; tail -c 3000 gpurun_out/bench_$c.json; done
-timeout 300 python tools/kbench.py --config c2 > gpurun_out/kbench_c2.txt 2>&1; cat gpurun_out/kbench_c2.txt
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches_c2.csv python bench.py --config c2 --steps 20 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_bench.log 2>&1
-python tools/launches.py gpurun_out/launches_c2.csv
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:'score128|attn_tc|topk_kernel|append' -s 20 -c 8 -o gpurun_out/prof_c2 python tools/kbench.py --config c2 --reps 5 --layers 2 > gpurun_out/ncu_full.log 2>&1
-tail -3 gpurun_out/ncu_full.log
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,clocks.mem --format=csv
+timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -4 > gpurun_out/pytest_gpu.log; cat gpurun_out/pytest_gpu.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; tail -2 gpurun_out/smoke.log
+timeout 600 python bench.py > gpurun_out/bench_default.json 2> gpurun_out/bench_default.err; cat gpurun_out/bench_default.json
+for c in c1 c3 c4 c5; do timeout 600 python bench.py --config $c --steps 200 --warmup 5 > gpurun_out/bench_$c.json 2> gpurun_out/bench_$c.err; tail -c 2500 gpurun_out/bench_$c.json; done
+timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_reference.json 2>&1; tail -c 1500 gpurun_out/bench_reference.json
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 300 --csv --log-file gpurun_out/launches_c2.csv python bench.py --steps 20 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
+for k in score128 topk2 attn_tc_kernel; do
+  timeout 600 ncu --set full --clock-control none --import-source on -k regex:$k -s 8 -c 1 -o gpurun_out/prof_c2_$k python tools/kbench.py --config c2 --reps 3 --layers 4 > /dev/null 2>&1
+done
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:score_mma -s 8 -c 1 -o gpurun_out/prof_c3_score_mma python tools/kbench.py --config c3 --reps 3 --layers 2 > /dev/null 2>&1
+ls gpurun_out
