@@ -9,7 +9,8 @@ from __future__ import annotations
 import ctypes as C
 import os
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libfier_cuda.so")
+# FIER_LIB: load another in-tree build of the same sources (tools: the -DFIER_STEP_TRACE variant)
+LIB_PATH = os.environ.get("FIER_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libfier_cuda.so")
 
 FIER_OK, FIER_EINVAL, FIER_EDATA, FIER_ECUDA = 0, 1, 2, 3
 FIER_F32, FIER_F16, FIER_BF16 = 0, 1, 2

@@ -42,22 +42,27 @@ def headers():
     return sorted(glob.glob(os.path.join(CSRC, "*.cuh"))) + [os.path.join(ROOT, "include", "fier_cuda.h")]
 
 
-def stale() -> bool:
-    if not os.path.exists(OUT):
+OUT_TRACE = os.path.join(PKG, "libfier_cuda_trace.so")  # -DFIER_STEP_TRACE: phase timestamps (tools/)
+
+
+def stale(out: str = OUT) -> bool:
+    if not os.path.exists(out):
         return True
-    t = os.path.getmtime(OUT)
+    t = os.path.getmtime(out)
     return any(os.path.getmtime(f) > t for f in sources() + headers() + [__file__])
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not stale():
-        return OUT
-    os.makedirs(BUILD, exist_ok=True)
+def build(force: bool = False, verbose: bool = False, trace: bool = False) -> str:
+    out_so = OUT_TRACE if trace else OUT
+    if not force and not stale(out_so):
+        return out_so
+    bdir = BUILD + ("_trace" if trace else "")
+    os.makedirs(bdir, exist_ok=True)
     objs = []
     procs = []
     for src in sources():
-        obj = os.path.join(BUILD, os.path.basename(src) + ".o")
-        cmd = [nvcc(), *ARCH, *FLAGS, "-c", src, "-o", obj]
+        obj = os.path.join(bdir, os.path.basename(src) + ".o")
+        cmd = [nvcc(), *ARCH, *FLAGS, *(["-DFIER_STEP_TRACE"] if trace else []), "-c", src, "-o", obj]
         if verbose:
             cmd += ["-Xptxas", "-v"]
             print(" ".join(cmd))
@@ -73,10 +78,10 @@ def build(force: bool = False, verbose: bool = False) -> str:
             print(f"nvcc failed on {src}", file=sys.stderr)
     if failed:
         raise RuntimeError("CUDA build failed")
-    tmp = OUT + ".tmp"
+    tmp = out_so + ".tmp"
     subprocess.run([nvcc(), *ARCH, "-shared", "-o", tmp, *objs], check=True)
-    os.replace(tmp, OUT)
-    return OUT
+    os.replace(tmp, out_so)
+    return out_so
 
 
 SHIM_SRC = os.path.join(ROOT, "tests", "cpp", "shim_test.cpp")
@@ -106,7 +111,10 @@ if __name__ == "__main__":
     ap.add_argument("--verbose", action="store_true")
     ap.add_argument("--force", action="store_true")
     ap.add_argument("--sass", default=None, help="write cuobjdump -sass listing here")
+    ap.add_argument("--trace", action="store_true", help="also build libfier_cuda_trace.so (phase timestamps)")
     a = ap.parse_args()
     print(build(force=a.force or a.verbose, verbose=a.verbose))
+    if a.trace:
+        print(build(force=a.force, trace=True))
     if a.sass:
         dump_sass(a.sass)

@@ -18,22 +18,11 @@
 //                                         B = V via ldmatrix.trans
 // Warp states are merged per CTA, CTA partials by log-sum-exp (the last CTA of
 // each head merges), exactly like attention.cu.
-#include "mma.cuh"
+#include "attn_tc.cuh"
 
 namespace fier_cuda {
 
 constexpr int kTcWarps = 4;
-constexpr int kTcRows = 16;  // rows per stage
-
-__device__ __forceinline__ void cp_async16_tc(uint32_t smem, const void* gmem) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem), "l"(gmem) : "memory");
-}
-
-// byte offset of 16-byte chunk c of row r inside a stage buffer (rows of RB bytes)
-template <int RB>
-__device__ __forceinline__ uint32_t swz(int r, int c) {
-    return (uint32_t)(r * RB + ((c ^ (r & 7)) << 4));
-}
 
 // wres must also hold the 2 * nsplit (<= 2 * 256) merge weights
 template <int D, int HPG>
@@ -49,11 +38,8 @@ __global__ void __launch_bounds__(kTcWarps * 32) attn_tc_kernel(
     float* __restrict__ out, const int32_t* __restrict__ counts, float* __restrict__ lse) {
     static_assert(HPG <= 8, "query rows live in mma rows 0..7");
     constexpr int RB = D * 2;              // bytes per row
-    constexpr int CPR = RB / 16;           // 16-byte chunks per row
     constexpr int KSTEPS = D / 16;         // mma k-steps over channels
-    constexpr int NT = D / 8;              // n-tiles over channels (PV)
     constexpr int STAGE = kTcRows * RB;    // bytes per K (or V) stage
-    constexpr int CPL = kTcRows * CPR / 32;  // chunks per lane per K (or V) stage
 
     extern __shared__ __align__(128) uint8_t smem[];
     float* wres = reinterpret_cast<float*>(smem + (size_t)kTcWarps * NST * 2 * STAGE);  // [warp][HPG][D+2]
@@ -61,7 +47,6 @@ __global__ void __launch_bounds__(kTcWarps * 32) attn_tc_kernel(
     int32_t* sidx = reinterpret_cast<int32_t*>(wres + tc_wres_floats<D, HPG>());
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int g = lane >> 2, t = lane & 3;
     const int split = blockIdx.x, head = blockIdx.y, b = blockIdx.z;
     const int kvh = GATHER ? head / (hq / hkv) : head;
     const int64_t seq = (int64_t)b * hkv + kvh;
@@ -74,7 +59,6 @@ __global__ void __launch_bounds__(kTcWarps * 32) attn_tc_kernel(
     const int rpw = (int)((((r_end - r_begin) + kTcWarps - 1) / kTcWarps + kTcRows - 1) / kTcRows * kTcRows);
     const int wr0 = min(r_begin + warp * rpw, r_end);
     const int wr1 = min(wr0 + rpw, r_end);
-    const int nstages = (wr1 - wr0 + kTcRows - 1) / kTcRows;
     const int32_t* selrow = GATHER ? sel + ((int64_t)b * hq + head) * n : nullptr;
     const int qh0 = GATHER ? head : head * HPG;
     if constexpr (GATHER) {
@@ -91,149 +75,16 @@ __global__ void __launch_bounds__(kTcWarps * 32) attn_tc_kernel(
         __syncthreads();
     }
 
-    // A fragments of Q (row m = query head m of the group; rows >= HPG zero)
-    uint32_t qa[KSTEPS][2];
-#pragma unroll
-    for (int ks = 0; ks < KSTEPS; ++ks) {
-        qa[ks][0] = qa[ks][1] = 0u;
-        if (g < HPG) {
-            const T* qp = q + ((int64_t)b * hq + qh0 + g) * D + ks * 16 + 2 * t;
-            qa[ks][0] = *reinterpret_cast<const uint32_t*>(qp);
-            qa[ks][1] = *reinterpret_cast<const uint32_t*>(qp + 8);
-        }
-    }
-
+    uint32_t qb[KSTEPS][2];
+    tc_load_q<T, D, HPG>(q + ((int64_t)b * hq + qh0) * D, qb);
+    TcState<D> st;
+    st.init();
     const uint32_t ring = smem_u32(smem) + (uint32_t)warp * NST * 2 * STAGE;
-
-    auto issue = [&](int st) {
-        if (st < nstages) {
-            const uint32_t kdst = ring + (uint32_t)(st % NST) * 2 * STAGE;
-            const uint32_t vdst = kdst + STAGE;
-            const int r0 = wr0 + st * kTcRows;
-            const int nr = min(kTcRows, wr1 - r0);
-            int tok = 0;
-            if constexpr (GATHER) {
-                if (lane < nr) tok = sidx[r0 - r_begin + lane];
-            }
-#pragma unroll
-            for (int i = 0; i < CPL; ++i) {
-                const int chunk = lane + 32 * i;
-                const int rr = chunk / CPR, c = chunk % CPR;
-                int tk;
-                if constexpr (GATHER) {
-                    tk = __shfl_sync(0xffffffffu, tok, rr);
-                } else {
-                    tk = r0 + rr;
-                }
-                const uint32_t o = swz<RB>(rr, c);
-                if (rr < nr) {
-                    cp_async16_tc(kdst + o, Kseq + (int64_t)tk * D + c * 8);
-                    cp_async16_tc(vdst + o, Vseq + (int64_t)tk * D + c * 8);
-                } else {  // rows past the end: V must be finite zeros (p = 0 there)
-                    asm volatile("st.shared.v4.u32 [%0], {%1,%1,%1,%1};" ::"r"(vdst + o), "r"(0u) : "memory");
-                    asm volatile("st.shared.v4.u32 [%0], {%1,%1,%1,%1};" ::"r"(kdst + o), "r"(0u) : "memory");
-                }
-            }
-        }
-        asm volatile("cp.async.commit_group;" ::: "memory");
-    };
-
-#pragma unroll
-    for (int s = 0; s < NST - 1; ++s) issue(s);
-
-    float o[NT][2];  // O[g][nt*8 + 2t + {0,1}]
-#pragma unroll
-    for (int i = 0; i < NT; ++i) o[i][0] = o[i][1] = 0.f;
-    float mrow = -INFINITY, lrow = 0.f;  // row g's running max / partial sum (this lane's tokens)
-
-    for (int st = 0; st < nstages; ++st) {
-        issue(st + NST - 1);
-        asm volatile("cp.async.wait_group %0;" ::"n"(NST - 1) : "memory");
-        __syncwarp();
-        const uint32_t kst = ring + (uint32_t)(st % NST) * 2 * STAGE;
-        const uint32_t vst = kst + STAGE;
-        const int nr = min(kTcRows, wr1 - (wr0 + st * kTcRows));
-
-        // ---- S = Q K^T for 16 rows: two n-tiles of 8 rows ----
-        float s[2][4];
-#pragma unroll
-        for (int nt = 0; nt < 2; ++nt) {
-            s[nt][0] = s[nt][1] = s[nt][2] = s[nt][3] = 0.f;
-#pragma unroll
-            for (int kp = 0; kp < KSTEPS / 2; ++kp) {  // pairs of k-steps = 4 chunks
-                uint32_t b0, b1, b2, b3;
-                const int row = nt * 8 + (lane & 7);
-                ldsm_x4(kst + swz<RB>(row, 4 * kp + (lane >> 3)), b0, b1, b2, b3);
-                mma16816<T>(s[nt], qa[2 * kp][0], 0u, qa[2 * kp][1], 0u, b0, b1);
-                mma16816<T>(s[nt], qa[2 * kp + 1][0], 0u, qa[2 * kp + 1][1], 0u, b2, b3);
-            }
-        }
-        // this lane's 4 logits of query row g: tokens nt*8 + 2t + {0,1}
-        float x[4];
-#pragma unroll
-        for (int nt = 0; nt < 2; ++nt)
-#pragma unroll
-            for (int e = 0; e < 2; ++e) {
-                const int tkn = nt * 8 + 2 * t + e;
-                x[nt * 2 + e] = tkn < nr ? s[nt][e] * scale_log2 : -INFINITY;
-            }
-        float mst = fmaxf(fmaxf(x[0], x[1]), fmaxf(x[2], x[3]));
-        mst = fmaxf(mst, __shfl_xor_sync(0xffffffffu, mst, 1));
-        mst = fmaxf(mst, __shfl_xor_sync(0xffffffffu, mst, 2));
-        const float mnew = fmaxf(mrow, mst);
-        const float alpha = exp2f(mrow - mnew);
-        float p[4];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) p[i] = exp2f(x[i] - mnew);
-        lrow = lrow * alpha + (p[0] + p[1]) + (p[2] + p[3]);
-        mrow = mnew;
-        if (__any_sync(0xffffffffu, alpha != 1.f)) {
-#pragma unroll
-            for (int i = 0; i < NT; ++i) {
-                o[i][0] *= alpha;
-                o[i][1] *= alpha;
-            }
-        }
-        // P as A fragments (row g): hi + lo 16-bit parts
-        const uint32_t ph0 = pack2<T>(p[0], p[1]), ph2 = pack2<T>(p[2], p[3]);
-        const float2 q0 = unpack2<T>(ph0), q2 = unpack2<T>(ph2);
-        const uint32_t pl0 = pack2<T>(p[0] - q0.x, p[1] - q0.y), pl2 = pack2<T>(p[2] - q2.x, p[3] - q2.y);
-        // ---- O += P V: n-tile pairs of 16 channels ----
-#pragma unroll
-        for (int np = 0; np < NT / 2; ++np) {
-            uint32_t b0, b1, b2, b3;
-            const int row = (lane & 7) + 8 * ((lane >> 3) & 1);
-            ldsm_x4_t(vst + swz<RB>(row, 2 * np + (lane >> 4)), b0, b1, b2, b3);
-            float d0[4] = {o[2 * np][0], o[2 * np][1], 0.f, 0.f};
-            float d1[4] = {o[2 * np + 1][0], o[2 * np + 1][1], 0.f, 0.f};
-            mma16816<T>(d0, ph0, 0u, ph2, 0u, b0, b1);
-            mma16816<T>(d0, pl0, 0u, pl2, 0u, b0, b1);
-            mma16816<T>(d1, ph0, 0u, ph2, 0u, b2, b3);
-            mma16816<T>(d1, pl0, 0u, pl2, 0u, b2, b3);
-            o[2 * np][0] = d0[0];
-            o[2 * np][1] = d0[1];
-            o[2 * np + 1][0] = d1[0];
-            o[2 * np + 1][1] = d1[1];
-        }
-        __syncwarp();
-    }
-    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    tc_stream_rows<T, D, GATHER, NST>(qb, Kseq, Vseq, wr0, wr1, ring, scale_log2,
+                                      [&](int r) { return sidx[r - r_begin]; }, st);
 
     // ---- warp states -> smem -> CTA partial -> last-CTA merge ----
-    lrow += __shfl_xor_sync(0xffffffffu, lrow, 1);
-    lrow += __shfl_xor_sync(0xffffffffu, lrow, 2);
-    float* wr = wres + warp * HPG * (D + 2);
-    if (g < HPG) {
-#pragma unroll
-        for (int i = 0; i < NT; ++i) {
-            wr[g * (D + 2) + i * 8 + 2 * t] = o[i][0];
-            wr[g * (D + 2) + i * 8 + 2 * t + 1] = o[i][1];
-        }
-        if (t == 0) {
-            wr[g * (D + 2) + D] = mrow;
-            wr[g * (D + 2) + D + 1] = lrow;
-        }
-    }
+    tc_store_state<D, HPG>(st, wres + warp * HPG * (D + 2));
     __syncthreads();
     for (int i = threadIdx.x; i < HPG * D; i += blockDim.x) {
         const int hh = i / D, c = i % D;

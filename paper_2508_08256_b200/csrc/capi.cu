@@ -40,6 +40,8 @@ int full_dispatch(const fier_shape*, const void*, const void*, const void*, int,
 size_t sparse_counter_offset(const fier_shape*, int);
 int append_score_dispatch(const fier_shape*, const void*, void*, void*, const void*, const void*, int,
                           uint32_t*, void*, float*, int64_t, int*, int, cudaStream_t);
+int fused_step_dispatch(const fier_shape*, const void*, const void*, const void*, int, void*, void*, uint32_t*,
+                        void*, int, float, float*, int32_t*, float*, int64_t, cudaStream_t);
 
 static int check_shape(const fier_shape* s, const char* fn) {
     const std::string f(fn);
@@ -201,6 +203,10 @@ int fier_decode_step(const fier_shape* s, const void* q, const void* k_new, cons
                  "fier_decode_step: workspace too small");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     const int64_t ld = fier_step_scores_ld(tokens);
+    // MHA, d = 128: the whole step in one cluster launch (step_fused.cu)
+    const int frc = fused_step_dispatch(s, q, k_new, v_new, pos, K, V, bits, params, n, scale, out, sel,
+                                        scores_out, ld, st);
+    if (frc >= 0) return frc;
     uint8_t* ws = static_cast<uint8_t*>(workspace);
     float* scores = scores_out ? scores_out : reinterpret_cast<float*>(ws);
     uint8_t* attn_ws = ws + align_up((size_t)s->batch * s->q_heads * ld * sizeof(float));

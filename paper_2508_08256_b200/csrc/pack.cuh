@@ -79,4 +79,57 @@ __device__ __forceinline__ void pack_group(const T* Kseq,  // no restrict: appen
     }  // channel slices
 }
 
+// Decode-time re-pack of the open group [gi*g, t_end) (one group per launch, so
+// the code stays small: no divergent unrolled paths).  Threads [0, 32*W) take
+// part, thread c owns channel c; the same rules as pack_group (first-seen
+// min/max, fp64 z/s, cvt.rn.f16.f64, compare against the unrounded z).
+template <typename T>
+__device__ __forceinline__ void pack_open_group(const T* Kseq,  // no restrict: re-reads the appended row
+                                                int d, int g, int gi, int t_end, uint32_t* __restrict__ bits_seq,
+                                                __half2* __restrict__ sz_seq) {
+    const int W = (d + 31) / 32;
+    const int c = threadIdx.x, lane = c & 31, w = c >> 5;
+    if (w >= W) return;
+    const bool valid = c < d;
+    const int t0 = gi * g;
+    const int t1 = min(t0 + g, t_end);  // short final group (quant1bit.hpp:84)
+    float mn = 0.f, mx = 0.f;
+    float v[32];  // the current chunk (g <= 32: the whole group, reused by the ballot pass)
+    for (int tc = t0; tc < t1; tc += 32) {  // chunks of 32 tokens: 32 loads in flight
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+            const int t = min(tc + i, t1 - 1);  // past the end: repeat the last token (no effect)
+            v[i] = valid ? to_f32(Kseq[(int64_t)t * d + c]) : 0.f;
+        }
+        if (tc == t0) mn = mx = v[0];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {  // std::min/max: a tie keeps the first-seen value
+            mn = (v[i] < mn) ? v[i] : mn;
+            mx = (mx < v[i]) ? v[i] : mx;
+        }
+    }
+    const double z = ((double)mx + (double)mn) / 2.0;
+    const double s = ((double)mx - (double)mn) / 2.0;
+    if (valid) sz_seq[(int64_t)gi * d + c] = __halves2half2(__double2half(s), __double2half(z));
+    float zc = __double2float_rn(z);
+    if ((double)zc < z) zc = nextafterf(zc, INFINITY);
+    const bool all_one = (s == 0.0);
+    for (int tc = t0; tc < t1; tc += 32) {
+        if (t1 - t0 > 32) {  // g > 32: reload this chunk
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+                const int t = min(tc + i, t1 - 1);
+                v[i] = valid ? to_f32(Kseq[(int64_t)t * d + c]) : 0.f;
+            }
+        }
+        uint32_t mine = 0;
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+            const uint32_t word = __ballot_sync(0xffffffffu, valid && (all_one || v[i] >= zc));
+            mine = lane == i ? word : mine;
+        }
+        if (tc + lane < t1) bits_seq[(int64_t)(tc + lane) * W + w] = mine;
+    }
+}
+
 }  // namespace fier_cuda

@@ -1,0 +1,433 @@
+// step_fused.cu -- the whole decode step of an MHA layer in ONE launch:
+// append -> score -> Top-n -> sparse attention, one thread-block cluster per
+// (sequence, head).
+//
+// Reference: fier_attend (retrieval.hpp:136-146) = approx_scores
+// (quant1bit.hpp:121-140) -> topk_oracle (core.hpp:134-148) -> gather_attention
+// (core.hpp:152-179), for every (sequence, head) of a layer, after the decode-time
+// append of the new token to the packed index (quantize's short-group rule,
+// quant1bit.hpp:84).  The separate-kernel path (score.cu -> topk2.cu ->
+// attention_tc.cu) computes the same thing with the scores and the selection
+// round-tripping through memory; here they stay on chip:
+//
+//   phase A  the CTA whose slice holds `pos` writes the new k/v row and re-packs
+//            the open group (K1 append, pack.cuh)
+//   phase B  CTA r of the cluster scores tokens [r*S, (r+1)*S) into shared-memory
+//            keys (S = 256*kpt; lane = token, the layout select.cuh wants).
+//            Scorer: a per-group nibble table.  For each 4-channel nibble
+//            position p the 16 entries hold  sum_{i in p} q_i (z_i - s_i)
+//            + sum_{i in p, bit i set} 2 q_i s_i,  so a token's score is the sum
+//            of 32 table reads, one per nibble of its 128-bit row: per nibble one
+//            PRMT (address), one LDS, one FADD -- ~3.5 lane-instructions per 4
+//            bits instead of ~2.5 per bit (score.cu).  Tables are rebuilt per
+//            32-token slab (lane p builds position p), double-buffered per warp.
+//   phase C  cluster Top-k on the register keys (select.cuh: min/max, one
+//            512-bin DSMEM histogram, candidate refinement, exact rank), then the
+//            ballot compaction writes the ascending selection to `sel` and this
+//            CTA's own selected tokens to shared memory.
+//   phase D  8 warps gather the CTA's selected K/V rows through cp.async rings
+//            and run the tensor-core online softmax (attn_tc.cuh); warp partials
+//            merge in shared memory, CTA partials are pushed to rank 0 over DSMEM
+//            and merged there by log-sum-exp.
+//
+// Only one kernel boundary per step, no score or index round trip through HBM,
+// and no split/merge workspace.  Every phase runs once per CTA, so the code is
+// kept as compact loops (a fully unrolled version streamed ~300 KB of SASS
+// through a cold instruction cache and ran 3x slower).  Applies to MHA (Hq == Hkv), d = 128, 32 | g,
+// 16-bit caches, rows up to 16 * 8192 tokens; other shapes use the
+// separate-kernel path.
+#include <climits>
+#include <cstdlib>
+#include <string>
+
+#include "common.cuh"
+
+#ifdef FIER_STEP_TRACE
+// debug build only (build.py --trace): globaltimer at the phase boundaries, per CTA
+namespace fier_cuda {
+constexpr int kFsTraceCtas = 4096;
+__device__ unsigned long long g_fs_trace[kFsTraceCtas][16];
+}  // namespace fier_cuda
+#define FS_MARK(i)                                                                            \
+    do {                                                                                      \
+        if (threadIdx.x == 0) {                                                               \
+            const int cta_ = blockIdx.y * gridDim.x + blockIdx.x;                             \
+            unsigned long long t_;                                                            \
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                            \
+            if (cta_ < ::fier_cuda::kFsTraceCtas) ::fier_cuda::g_fs_trace[cta_][i] = t_;                                \
+        }                                                                                     \
+    } while (0)
+#else
+#define FS_MARK(i) \
+    do {           \
+    } while (0)
+#endif
+#define T2_MARK(i) FS_MARK(i)
+
+#include "attn_tc.cuh"
+#include "nibble.cuh"
+#include "pack.cuh"
+#include "select.cuh"
+
+namespace fier_cuda {
+
+constexpr int kFsThreads = 512;  // 16 warps: ALU/LDS latency in the scorer needs the warps
+constexpr int kFsWarps = kFsThreads / 32;
+constexpr int kFsD = 128;
+constexpr int kFsGatherWarps = 8;
+constexpr int kFsNst = 3;
+constexpr int kFsMaxKpt = 16;  // slice <= 8192 tokens (u16 slots in sidx)
+constexpr int kFsAppendSlabs = 3;  // sealed slabs the append warps hand to the others (~ the append's time)
+constexpr int kFsLutBytes = kNibTableBytes;
+// shared memory map (bytes from a 256-aligned base)
+constexpr int kFsRing = kFsGatherWarps * kFsNst * 2 * tc_stage_bytes<kFsD>();  // phase D rings
+constexpr int kFsLut = 0;                                                    // phase B (inside the ring area)
+constexpr int kFsSel = kFsLut + kFsWarps * 2 * kFsLutBytes;                  // phase C T2Shared (ditto)
+constexpr int kFsKeys = kFsSel + ((int)sizeof(T2Shared) + 255) / 256 * 256;  // phase B/C keys (ditto)
+constexpr int kFsSidx = kFsRing;                                             // u16 selected slots
+constexpr int kFsWres = kFsSidx + kFsThreads * kFsMaxKpt * 2;                // warp partials
+constexpr int kFsCres = kFsWres + kFsGatherWarps * (kFsD + 2) * 4;           // CTA partials (rank 0)
+constexpr int kFsSmem = kFsCres + kT2MaxCluster * (kFsD + 2) * 4 + 256;      // + base alignment
+static_assert(kFsKeys + kFsThreads * kFsMaxKpt * 4 <= kFsRing, "LUTs, T2Shared and keys must fit in the ring area");
+static_assert(kFsSmem <= 227 * 1024, "fused step exceeds shared memory");
+
+
+struct FsArgs {
+    const void* q;
+    void* K;
+    void* V;
+    const void* k_new;
+    const void* v_new;
+    uint32_t* bits;
+    __half2* sz;
+    float* scores;  // optional
+    float* out;
+    int32_t* sel;
+    int64_t ld;
+    int pos, tokens, cap, G, hq, g, g_shift, k, kpt;  // g_shift = log2(g) or -1
+    float scale_log2;
+};
+
+template <typename T>
+__global__ void __launch_bounds__(kFsThreads, 1) step_fused_kernel(const FsArgs a) {
+    constexpr int D = kFsD;
+    constexpr int PF = 4;  // slabs in flight per warp
+    cg::cluster_group cluster = cg::this_cluster();
+    const int rank = (int)cluster.block_rank();
+    const int nct = (int)cluster.num_blocks();
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int row = blockIdx.y;  // b * hq + h; MHA: kv head = h, sequence index = row
+    const int64_t seq = row;
+    const int kpt = a.kpt;  // slabs (keys) per thread
+    const int slice = kFsThreads * kpt;
+    const int s0 = rank * slice;
+    const int wbase = warp * 32 * kpt;
+
+    extern __shared__ uint8_t smem_raw[];
+    const uint32_t raw = smem_u32(smem_raw);
+    const uint32_t base = (raw + 255u) & ~255u;
+    uint8_t* smem = smem_raw + (base - raw);
+    T2Shared& S = *reinterpret_cast<T2Shared*>(smem + kFsSel);
+    uint16_t* sidx = reinterpret_cast<uint16_t*>(smem + kFsSidx);
+    float* wres = reinterpret_cast<float*>(smem + kFsWres);
+    float* cres = reinterpret_cast<float*>(smem + kFsCres);
+    uint32_t* keys_s = reinterpret_cast<uint32_t*>(smem + kFsKeys);
+
+    // peers store into this CTA's shared memory only after the wait in t2_threshold
+    asm volatile("barrier.cluster.arrive.relaxed;" ::: "memory");
+    FS_MARK(0);
+
+    T* Kseq = static_cast<T*>(a.K) + seq * a.cap * D;
+    T* Vseq = static_cast<T*>(a.V) + seq * a.cap * D;
+    uint32_t* bseq = a.bits + seq * a.cap * 4;
+    __half2* zseq = a.sz + seq * a.G * D;
+
+    // ---- phase A: append (the CTA whose slice holds pos; warps 0..3 re-pack the open
+    // group while the other warps start scoring; the open group's slabs are scored last) ----
+    const bool appender = a.pos / slice == rank;  // CTA-uniform
+    const int open_lo = appender ? (a.pos / a.g) * a.g : INT_MAX;  // first token of the open group
+    if (appender && tid < D) {
+        Kseq[(int64_t)a.pos * D + tid] = static_cast<const T*>(a.k_new)[seq * D + tid];
+        Vseq[(int64_t)a.pos * D + tid] = static_cast<const T*>(a.v_new)[seq * D + tid];
+        pack_open_group<T>(Kseq, D, a.g, a.pos / a.g, a.pos + 1, bseq, zseq);
+    }
+
+    FS_MARK(1);
+    // ---- phase B: score this CTA's slice into shared-memory keys ----
+    float qv[4];
+    {
+        const T* qp = static_cast<const T*>(a.q) + seq * D + 4 * lane;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) qv[i] = to_f32(qp[i]);
+    }
+    const uint32_t tab0 = base + kFsLut + warp * 2 * kFsLutBytes;
+    float mn = INFINITY, mx = -INFINITY;
+    float* srow = a.scores ? a.scores + (int64_t)row * a.ld : nullptr;
+    // Scoring is assigned per slab (32 tokens), independently of which warp owns the
+    // slab's keys in phase C (keys are stored token-ordered: slab sl -> keys_s[32 sl ..]).
+    // Sealed slabs are split into contiguous per-warp ranges; in the appending CTA the
+    // four append warps take kFsAppendSlabs fewer.  Open (and empty) slabs are scored
+    // after the barrier that publishes the re-packed group.
+    const int nsl = slice / 32;
+    const int ntok = max(0, min(a.tokens, s0 + slice) - s0);
+    const int nsealed = appender ? (open_lo - s0) / 32 : (ntok + 31) / 32;
+    int start, cnt;
+    {
+        const int per = nsealed / kFsWarps;
+        const int na = appender ? max(0, per - kFsAppendSlabs) : per;  // warps 0..3
+        const int rest = nsealed - 4 * na, nb = kFsWarps - 4;
+        if (warp < 4) {
+            start = warp * na;
+            cnt = na;
+        } else {
+            const int w = warp - 4, q = rest / nb, r = rest % nb;
+            start = 4 * na + w * q + min(w, r);
+            cnt = q + (w < r ? 1 : 0);
+        }
+    }
+    auto score_slab = [&](int sl, int u, const uint4& p, const uint4& bw) {
+        const int t0 = s0 + 32 * sl, t = t0 + lane;
+        uint32_t key = 0u;  // 0 = empty slot (past the row end, or NaN)
+        if (t0 < a.tokens) {  // warp-uniform
+            const uint32_t tab = tab0 + (u & 1) * kFsLutBytes;
+            build_nibble_table(tab, p, qv);
+            __syncwarp();
+            const float sc = nibble_score(tab, bw);
+            if (t < a.tokens) {
+                key = isnan(sc) ? 0u : float_key(sc);
+                if (isfinite(sc)) {
+                    mn = fminf(mn, sc);
+                    mx = fmaxf(mx, sc);
+                }
+                if (srow) srow[t] = sc;
+            }
+        }
+        keys_s[32 * sl + lane] = key;
+    };
+    auto load = [&](int sl, uint4& p, uint4& bw) {
+        const int t0 = s0 + 32 * sl;
+        p = make_uint4(0, 0, 0, 0);
+        bw = make_uint4(0, 0, 0, 0);
+        if (t0 < a.tokens) {
+            const int gi = a.g_shift >= 0 ? t0 >> a.g_shift : t0 / a.g;
+            p = ld_cg16(zseq + (int64_t)gi * D + 4 * lane);
+            if (t0 + lane < a.tokens) bw = ld_cg16(bseq + (int64_t)(t0 + lane) * 4);
+        }
+    };
+    uint4 pb[PF], bb[PF];  // register ring: (s, z) and bit rows of the next PF slabs
+#pragma unroll
+    for (int u = 0; u < PF; ++u)
+        if (u < cnt) load(start + u, pb[u], bb[u]);
+    for (int j0 = 0; j0 < cnt; j0 += PF) {
+#pragma unroll
+        for (int u = 0; u < PF; ++u) {
+            const int j = j0 + u;
+            if (j < cnt) {  // warp-uniform
+                const uint4 p = pb[u], bw = bb[u];
+                if (j + PF < cnt) load(start + j + PF, pb[u], bb[u]);
+                score_slab(start + j, u, p, bw);
+            }
+        }
+    }
+    if (appender) {
+        __syncthreads();  // the re-packed open group is visible to every warp of this CTA
+        for (int sl = nsealed + warp; sl < nsl; sl += kFsWarps) {
+            uint4 p, bw;
+            load(sl, p, bw);
+            score_slab(sl, sl, p, bw);
+        }
+    }
+
+    // ---- phase C: cluster Top-k, compaction to sel (global) and sidx (this CTA) ----
+    FS_MARK(2);
+    const SmemKeys keys{keys_s + wbase, kpt};  // phase C ownership: warp w, slot j, lane L
+    const T2Threshold th = t2_threshold<kFsThreads>(cluster, keys, mn, mx, s0, wbase, a.k, S);
+    FS_MARK(3);
+    int32_t* selrow = a.sel + (int64_t)row * a.k;
+    uint32_t cbase = 0, ccount = 0;
+    t2_compact<kFsThreads>(cluster, keys, th, S, &cbase, &ccount, [&](uint32_t slot, int j) {
+        const int local = wbase + 32 * j + lane;
+        selrow[slot] = s0 + local;
+        sidx[slot - cbase] = (uint16_t)local;
+    });
+    __syncthreads();  // sidx complete; T2Shared (inside the ring area) no longer read
+    FS_MARK(4);
+
+    // ---- phase D: attention over this CTA's selected rows ----
+    if (warp < kFsGatherWarps) {
+        uint32_t qb[D / 16][2];
+        tc_load_q<T, D, 1>(static_cast<const T*>(a.q) + seq * D, qb);
+        TcState<D> st;
+        st.init();
+        const int cnt = (int)ccount;
+        const int rpw = ((cnt + kFsGatherWarps - 1) / kFsGatherWarps + kTcRows - 1) / kTcRows * kTcRows;
+        const int wr0 = min(warp * rpw, cnt), wr1 = min(wr0 + rpw, cnt);
+        const uint32_t ring = base + (uint32_t)warp * kFsNst * 2 * tc_stage_bytes<D>();
+        tc_stream_rows<T, D, true, kFsNst>(qb, Kseq, Vseq, wr0, wr1, ring, a.scale_log2,
+                                           [&](int r) { return s0 + (int)sidx[r]; }, st);
+        tc_store_state<D, 1>(st, wres + warp * (D + 2));
+    }
+    FS_MARK(5);
+    __syncthreads();
+    // CTA partial -> rank 0's cres[rank] over DSMEM
+    float* dst = cluster.map_shared_rank(cres, 0) + rank * (D + 2);
+    if (tid < D) {
+        float M = -INFINITY;
+#pragma unroll
+        for (int w = 0; w < kFsGatherWarps; ++w) M = fmaxf(M, wres[w * (D + 2) + D]);
+        float oo = 0.f, L = 0.f;
+#pragma unroll
+        for (int w = 0; w < kFsGatherWarps; ++w) {
+            const float* xx = wres + w * (D + 2);
+            const float sc = xx[D] == -INFINITY ? 0.f : exp2f(xx[D] - M);
+            oo = fmaf(xx[tid], sc, oo);
+            L = fmaf(xx[D + 1], sc, L);
+        }
+        dst[tid] = oo;
+        if (tid == 0) {
+            dst[D] = M;
+            dst[D + 1] = L;
+        }
+    }
+    cluster.sync();
+    FS_MARK(6);
+    if (rank != 0 || tid >= D) return;
+    float M = -INFINITY;
+    for (int r = 0; r < nct; ++r) M = fmaxf(M, cres[r * (D + 2) + D]);
+    float oo = 0.f, L = 0.f;
+    for (int r = 0; r < nct; ++r) {
+        const float* xx = cres + r * (D + 2);
+        if (xx[D] == -INFINITY) continue;
+        const float sc = exp2f(xx[D] - M);
+        oo = fmaf(xx[tid], sc, oo);
+        L = fmaf(xx[D + 1], sc, L);
+    }
+    a.out[(int64_t)row * D + tid] = L > 0.f ? oo / L : 0.f;
+    FS_MARK(7);
+}
+
+// ---- host side -------------------------------------------------------------------
+
+static bool fused_disabled() {  // FIER_STEP=unfused: the separate-kernel path (A/B measurements)
+    static const bool v = [] {
+        const char* e = getenv("FIER_STEP");
+        return e && std::string(e) == "unfused";
+    }();
+    return v;
+}
+
+template <typename T>
+static int launch_fused(int cluster, int rows, const FsArgs& args, cudaStream_t st) {
+    auto kern = step_fused_kernel<T>;
+    static const bool ok = [&] {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kFsSmem);
+        cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        return true;
+    }();
+    (void)ok;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(cluster, rows, 1);
+    cfg.blockDim = dim3(kFsThreads, 1, 1);
+    cfg.dynamicSmemBytes = kFsSmem;
+    cfg.stream = st;
+    cudaLaunchAttribute attrs[1];
+    attrs[0].id = cudaLaunchAttributeClusterDimension;
+    attrs[0].val.clusterDim.x = cluster;
+    attrs[0].val.clusterDim.y = 1;
+    attrs[0].val.clusterDim.z = 1;
+    cfg.attrs = attrs;
+    cfg.numAttrs = 1;
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, args);
+    if (e != cudaSuccess) return fail(FIER_ECUDA, std::string("fier_decode_step: ") + cudaGetErrorString(e));
+    return FIER_OK;
+}
+
+// Cluster size and keys per thread for `tokens` per row: one CTA per SM (the
+// smem footprint), the whole grid in one wave when it fits, >= 2 slabs per warp.
+static bool fused_plan(int rows, int tokens, int g, int* cluster, int* kpt) {
+    int c = 1;
+    while (c < kT2MaxCluster && ceil_div(tokens, c) > (int64_t)kFsThreads * kFsMaxKpt) c *= 2;
+    if (ceil_div(tokens, c) > (int64_t)kFsThreads * kFsMaxKpt) return false;
+    while (c < kT2MaxCluster && (int64_t)rows * c * 2 <= num_sms() && ceil_div(tokens, 2 * c) >= 2 * kFsThreads) c *= 2;
+    int k = (int)ceil_div(ceil_div(tokens, c), kFsThreads);
+    while (((int64_t)kFsThreads * k) % g != 0) ++k;  // the open group lies inside one CTA's slice
+    if (k > kFsMaxKpt) return false;
+    *kpt = k;
+    *cluster = (int)ceil_div(tokens, (int64_t)kFsThreads * k);
+    return true;
+}
+
+// Returns -1 when the shape is not covered (the caller runs the separate kernels).
+int fused_step_dispatch(const fier_shape* s, const void* q, const void* k_new, const void* v_new, int pos, void* K,
+                        void* V, uint32_t* bits, void* params, int n, float scale, float* out, int32_t* sel,
+                        float* scores_out, int64_t ld, cudaStream_t st) {
+    if (fused_disabled()) return -1;
+    if (s->q_heads != s->kv_heads || s->dim != kFsD || s->group % 32 != 0) return -1;
+    if (s->dtype != FIER_BF16 && s->dtype != FIER_F16) return -1;
+    const int tokens = pos + 1, rows = s->batch * s->q_heads;
+    if (rows > 65535) return -1;
+    int cluster = 0, kpt = 0;
+    if (!fused_plan(rows, tokens, s->group, &cluster, &kpt)) return -1;
+    FsArgs args;
+    args.q = q;
+    args.K = K;
+    args.V = V;
+    args.k_new = k_new;
+    args.v_new = v_new;
+    args.bits = bits;
+    args.sz = static_cast<__half2*>(params);
+    args.scores = scores_out;
+    args.out = out;
+    args.sel = sel;
+    args.ld = ld;
+    args.pos = pos;
+    args.tokens = tokens;
+    args.cap = s->capacity;
+    args.G = (int)ceil_div(s->capacity, s->group);
+    args.hq = s->q_heads;
+    args.g = s->group;
+    args.g_shift = (s->group & (s->group - 1)) == 0 ? __builtin_ctz(s->group) : -1;
+    args.k = n;
+    args.kpt = kpt;
+    args.scale_log2 = scale * kLog2e;
+    if (s->dtype == FIER_BF16) return launch_fused<__nv_bfloat16>(cluster, rows, args, st);
+    return launch_fused<__half>(cluster, rows, args, st);
+}
+
+}  // namespace fier_cuda
+
+#ifdef FIER_STEP_TRACE
+// max co-resident clusters of the bf16 instance at this cluster size
+extern "C" FIER_API int fier_debug_step_occupancy(int cluster) {
+    auto kern = fier_cuda::step_fused_kernel<__nv_bfloat16>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, fier_cuda::kFsSmem);
+    cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(cluster, 64, 1);
+    cfg.blockDim = dim3(fier_cuda::kFsThreads, 1, 1);
+    cfg.dynamicSmemBytes = fier_cuda::kFsSmem;
+    cudaLaunchAttribute attr;
+    attr.id = cudaLaunchAttributeClusterDimension;
+    attr.val.clusterDim.x = cluster;
+    attr.val.clusterDim.y = 1;
+    attr.val.clusterDim.z = 1;
+    cfg.attrs = &attr;
+    cfg.numAttrs = 1;
+    int n = -1;
+    if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess) return -1;
+    return n;
+}
+
+extern "C" FIER_API int fier_debug_step_trace_clear(void) {
+    static unsigned long long zeros[fier_cuda::kFsTraceCtas][16];
+    return cudaMemcpyToSymbol(fier_cuda::g_fs_trace, zeros, sizeof(zeros)) == cudaSuccess ? 0 : 3;
+}
+
+extern "C" FIER_API int fier_debug_step_trace(unsigned long long* host, int ctas) {
+    const int n = ctas < fier_cuda::kFsTraceCtas ? ctas : fier_cuda::kFsTraceCtas;
+    return cudaMemcpyFromSymbol(host, fier_cuda::g_fs_trace, (size_t)n * 16 * sizeof(unsigned long long)) ==
+                   cudaSuccess
+               ? 0
+               : 3;
+}
+#endif

@@ -1,0 +1,181 @@
+// score_probe.cu -- what bounds the fused step's scoring phase (phase B of
+// csrc/step_fused.cu)?  C2 layout: 32 heads x 32768 tokens, d = 128, g = 32;
+// 128 CTAs x 512 threads, CTA b scores 8192 tokens of head b / 4 (like the
+// fused step).  Modes:
+//   0  loads only (bits + (s, z) rows, xor-reduced)          -> memory bound
+//   1  full scorer (table build + 32 lookups per token)
+//   2  scorer on register-resident data (no global loads)     -> compute bound
+//   3  loads + lookups, table built once per warp (no rebuild) -> build cost
+//   4  lookups only (register data, table built once)            -> LDS path
+//   5  as 4 with the LDS replaced by an ALU op                    -> issue path
+// L2 is flushed (512 MB read) before every timed launch.
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -Ipaper_2508_08256_b200/csrc -Iinclude \
+//        -o tools/score_probe tools/score_probe.cu
+#include <cstdio>
+#include <vector>
+#include <algorithm>
+
+#include "nibble.cuh"
+
+using namespace fier_cuda;
+
+constexpr int H = 32, L = 32768, D = 128, G = L / 32, KPT = 16, NT = 512;
+
+template <int MODE, int PF>
+__global__ void __launch_bounds__(NT, 1) probe(const uint32_t* bits, const __half2* sz, const float* q,
+                                                float* out) {
+    extern __shared__ __align__(256) uint8_t sm[];
+    unsigned long long t_start;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int head = blockIdx.x / 4, s0 = (blockIdx.x % 4) * (NT * KPT);
+    const int wbase = warp * 32 * KPT;
+    const uint32_t base = (uint32_t)__cvta_generic_to_shared(sm);
+    const uint32_t tab0 = base + warp * 2 * kNibTableBytes;
+    uint32_t* run = reinterpret_cast<uint32_t*>(sm + 16 * 2 * kNibTableBytes) + wbase;
+    const uint32_t* bseq = bits + (size_t)head * L * 4;
+    const __half2* zseq = sz + (size_t)head * G * D;
+    float qv[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) qv[i] = q[head * D + 4 * lane + i];
+    uint32_t x = 0;
+    auto load = [&](int j, uint4& p, uint4& bw) {
+        const int t0 = s0 + wbase + 32 * j;
+        p = make_uint4(0, 0, 0, 0);
+        bw = make_uint4(0, 0, 0, 0);
+        if (j < KPT) {
+            p = ld_cg16(zseq + (size_t)(t0 >> 5) * D + 4 * lane);
+            bw = ld_cg16(bseq + (size_t)(t0 + lane) * 4);
+        }
+    };
+    uint4 pb[PF], bb[PF];
+#pragma unroll
+    for (int u = 0; u < PF; ++u) load(u, pb[u], bb[u]);
+    if (MODE >= 3) {
+        build_nibble_table(tab0, pb[0], qv);
+        __syncwarp();
+    }
+    for (int j0 = 0; j0 < KPT; j0 += PF) {
+#pragma unroll
+        for (int u = 0; u < PF; ++u) {
+            const int j = j0 + u;
+            const uint4 p = pb[u], bw = bb[u];
+            if (MODE != 2 && MODE < 4) load(j + PF, pb[u], bb[u]);
+            if (MODE == 0) {
+                x ^= p.x ^ p.y ^ p.z ^ p.w ^ bw.x ^ bw.y ^ bw.z ^ bw.w;
+            } else {
+                const uint32_t tab = MODE >= 3 ? tab0 : tab0 + (u & 1) * kNibTableBytes;
+                if (MODE < 3) {
+                    build_nibble_table(tab, p, qv);
+                    __syncwarp();
+                }
+                uint4 b2 = bw;
+                if (MODE == 2 || MODE >= 4) b2.x ^= (uint32_t)j * 0x9E3779B9u;
+                float sc;
+                if (MODE == 5) {
+                    const uint32_t w4[4] = {b2.x, b2.y, b2.z, b2.w};
+                    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+                    for (int wd = 0; wd < 4; ++wd) {
+                        const uint32_t ev = ((w4[wd] << 2) & 0x3C3C3C3Cu) ^ kFsSwz;
+                        const uint32_t od = ((w4[wd] >> 2) & 0x3C3C3C3Cu) ^ kFsSwz;
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) {
+                            acc[i] += __uint_as_float(__byte_perm(ev, tab, 0x7650u + i) + wd * 512);
+                            acc[(i + 2) & 3] += __uint_as_float(__byte_perm(od, tab, 0x7650u + i) + wd * 256);
+                        }
+                    }
+                    sc = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+                } else {
+                    sc = nibble_score(tab, b2);
+                }
+                run[32 * j + lane] = __float_as_uint(sc);
+            }
+        }
+    }
+    __syncthreads();
+    if (MODE != 0)
+        for (int j = 0; j < KPT; ++j) x ^= run[32 * j + lane];
+    if (x == 0x12345678u) out[0] = 1.f;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long t_end;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
+        atomicMin(reinterpret_cast<unsigned long long*>(out) + 8, t_start);
+        atomicMax(reinterpret_cast<unsigned long long*>(out) + 9, t_end);
+    }
+}
+
+__global__ void flush(const uint4* p, size_t n, float* out) {
+    uint32_t acc = 0;
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+        acc ^= p[i].x;
+    if (acc == 0x12345) out[1] = acc;
+}
+
+template <int MODE, int PF>
+float run(const uint32_t* bits, const __half2* sz, const float* q, float* out, const uint4* fl, size_t fn) {
+    const int smem = 16 * 2 * kNibTableBytes + NT * KPT * 4;
+    cudaFuncSetAttribute(probe<MODE, PF>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    std::vector<float> ts, ds;
+    for (int r = 0; r < 7; ++r) {
+        flush<<<1184, 512>>>(fl, fn, out);
+        unsigned long long init[2] = {~0ull, 0ull};
+        cudaMemcpy(reinterpret_cast<unsigned long long*>(out) + 8, init, 16, cudaMemcpyHostToDevice);
+        cudaEventRecord(a);
+        probe<MODE, PF><<<128, NT, smem>>>(bits, sz, q, out);
+        cudaEventRecord(b);
+        cudaEventSynchronize(b);
+        float ms;
+        cudaEventElapsedTime(&ms, a, b);
+        ts.push_back(ms * 1000.f);
+        unsigned long long tt[2];
+        cudaMemcpy(tt, reinterpret_cast<unsigned long long*>(out) + 8, 16, cudaMemcpyDeviceToHost);
+        ds.push_back((tt[1] - tt[0]) / 1000.f);
+    }
+    std::sort(ts.begin(), ts.end());
+    std::sort(ds.begin(), ds.end());
+    printf("  [events %6.2f us, in-kernel first-start..last-end %6.2f us]  ", ts[3], ds[3]);
+    return ds[3];
+}
+
+int main() {
+    const size_t nb = (size_t)H * L * 4, nz = (size_t)H * G * D;
+    uint32_t* bits;
+    __half2* sz;
+    float *q, *out;
+    uint4* fl;
+    const size_t fn = (512ull << 20) / 16;
+    cudaMalloc(&bits, nb * 4);
+    cudaMalloc(&sz, nz * 4);
+    cudaMalloc(&q, H * D * 4);
+    cudaMalloc(&out, 128);
+    cudaMalloc(&fl, fn * 16);
+    std::vector<uint32_t> hb(nb);
+    for (size_t i = 0; i < nb; ++i) hb[i] = (uint32_t)(i * 2654435761u) ^ (uint32_t)(i >> 7);
+    cudaMemcpy(bits, hb.data(), nb * 4, cudaMemcpyHostToDevice);
+    std::vector<__half2> hz(nz, __halves2half2(__float2half(0.7f), __float2half(-0.1f)));
+    cudaMemcpy(sz, hz.data(), nz * 4, cudaMemcpyHostToDevice);
+    std::vector<float> hq(H * D, 0.3f);
+    cudaMemcpy(q, hq.data(), H * D * 4, cudaMemcpyHostToDevice);
+    cudaMemset(fl, 1, fn * 16);
+    const double bytes = (double)H * L * 32;  // 16 B bits + 16 B (s, z) per token
+    auto rep = [&](const char* name, float us) {
+        printf("%-34s %8.2f us  %7.0f GB/s\n", name, us, bytes / us / 1e3);
+    };
+    rep("mode0 loads only PF=4", run<0, 4>(bits, sz, q, out, fl, fn));
+    rep("mode0 loads only PF=8", run<0, 8>(bits, sz, q, out, fl, fn));
+    rep("mode1 full PF=4", run<1, 4>(bits, sz, q, out, fl, fn));
+    rep("mode1 full PF=2", run<1, 2>(bits, sz, q, out, fl, fn));
+    rep("mode1 full PF=8", run<1, 8>(bits, sz, q, out, fl, fn));
+    rep("mode2 compute only", run<2, 4>(bits, sz, q, out, fl, fn));
+    rep("mode3 loads+lookups (no rebuild)", run<3, 4>(bits, sz, q, out, fl, fn));
+    rep("mode4 lookups only", run<4, 4>(bits, sz, q, out, fl, fn));
+    rep("mode5 lookups as ALU", run<5, 4>(bits, sz, q, out, fl, fn));
+    cudaError_t e = cudaGetLastError();
+    printf("status: %s\n", cudaGetErrorString(e));
+    return 0;
+}
