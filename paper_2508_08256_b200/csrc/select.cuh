@@ -53,7 +53,7 @@ constexpr int kT2Cand = 2048;      // merged candidates per row
 
 struct T2Shared {
     float mm[kT2MaxCluster][2];          // pushed (min, max) of every CTA
-    alignas(16) uint32_t hist[kT2Bins];  // this CTA's histogram (read remotely)
+    alignas(16) uint32_t hist[kT2Bins + 4];  // this CTA's histogram (read remotely); [kT2Bins] = trash
     alignas(16) uint32_t tot[kT2Bins];   // merged histogram / scratch
     uint32_t ncand;                      // this CTA's candidate count (read remotely)
     uint32_t ckey[kT2CtaCand];           // this CTA's candidates (read remotely)
@@ -109,29 +109,40 @@ struct SmemKeys {
     __device__ __forceinline__ int count() const { return n; }
 };
 
+// f(j, key of slot j) for every slot of this thread.  Shared-memory keys are read in
+// batches of 8 before any use, so their load latency overlaps (the bodies contain
+// shared-memory atomics, which the compiler will not move loads across).
 template <typename Keys, typename F>
 __device__ __forceinline__ void t2_for_keys(const Keys& keys, F&& f) {
     if constexpr (Keys::kStatic > 0) {
 #pragma unroll
-        for (int j = 0; j < Keys::kStatic; ++j) f(j);
+        for (int j = 0; j < Keys::kStatic; ++j) f(j, keys(j));
     } else {
-#pragma unroll 2
-        for (int j = 0; j < keys.count(); ++j) f(j);
+        const int n = keys.count();
+        int j0 = 0;
+        for (; j0 + 8 <= n; j0 += 8) {
+            uint32_t kk[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) kk[u] = keys(j0 + u);
+#pragma unroll
+            for (int u = 0; u < 8; ++u) f(j0 + u, kk[u]);
+        }
+        for (; j0 < n; ++j0) f(j0, keys(j0));
     }
 }
 
 // Over bins held in cnt[0..kT2Bins) (smem), find b with above(b) < krem <= above(b) + cnt[b],
 // above(b) = sum of bins > b.  Writes (b, above) to res[0..1] (res[0] = ~0u if none).
-template <int NT>
-__device__ __forceinline__ void t2_find_bin(const uint32_t* cnt, uint32_t krem, T2Shared& S) {
+template <int NT, int BINS = kT2Bins, typename SH = T2Shared>
+__device__ __forceinline__ void t2_find_bin(const uint32_t* cnt, uint32_t krem, SH& S) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    constexpr int BPT = kT2Bins / NT;  // bins per thread
+    constexpr int BPT = BINS >= NT ? BINS / NT : 1;  // bins per thread
     if (tid == 0) S.res[0] = ~0u;
     uint32_t cb[BPT];
     uint32_t c = 0;
 #pragma unroll
     for (int i = 0; i < BPT; ++i) {
-        cb[i] = cnt[BPT * tid + i];
+        cb[i] = (BINS >= NT || BPT * tid + i < BINS) ? cnt[BPT * tid + i] : 0u;
         c += cb[i];
     }
     uint32_t s = c;  // inclusive suffix within the warp (higher lanes own higher bins)
@@ -165,11 +176,11 @@ __device__ __forceinline__ void t2_find_bin(const uint32_t* cnt, uint32_t krem, 
     __syncthreads();
 }
 
-// tot[i] = sum over the cluster's CTAs of hist[i]: 16-byte DSMEM loads by the first
-// kT2Bins/4 threads (scattered 4-byte remote loads are throughput-bound).
+// tot[i] = sum over the cluster's CTAs of hist[i]: 16-byte DSMEM loads
+// (scattered 4-byte remote loads are throughput-bound).
+template <int BINS = kT2Bins>
 __device__ __forceinline__ void t2_merge_hist(cg::cluster_group& cluster, int nct, uint32_t* hist, uint32_t* tot) {
-    const int t = threadIdx.x;
-    if (t < kT2Bins / 4) {
+    for (int t = threadIdx.x; t < BINS / 4; t += blockDim.x) {
         uint4 a = make_uint4(0, 0, 0, 0);
         for (int r = 0; r < nct; ++r) {
             const uint4 v = reinterpret_cast<const uint4*>(cluster.map_shared_rank(hist, r))[t];
@@ -180,6 +191,39 @@ __device__ __forceinline__ void t2_merge_hist(cg::cluster_group& cluster, int nc
         }
         reinterpret_cast<uint4*>(tot)[t] = a;
     }
+}
+
+// Exact MSD radix select on the order-preserving keys (9/9/9/5-bit digits, one
+// cluster barrier + DSMEM histogram merge per digit): the degenerate-row path.
+template <int NT, typename Keys, typename SH>
+__device__ __forceinline__ T2Threshold t2_radix_select(cg::cluster_group& cluster, const Keys& keys, int k, SH& S) {
+    const int nct = (int)cluster.num_blocks();
+    const int tid = threadIdx.x;
+    T2Threshold res = {0u, 0u, 0u};
+    uint32_t prefix = 0, pmask = 0, kr = (uint32_t)k;
+    uint32_t* h = S.hist;
+#pragma unroll 1
+    for (int pass = 0; pass < 4; ++pass) {
+        const int shift = 23 - 9 * pass > 0 ? 23 - 9 * pass : 0;
+        const int bins = pass == 3 ? 32 : 512;
+        cluster.sync();  // remote readers of the previous histogram are done
+        for (int i = tid; i < kT2Bins; i += NT) h[i] = 0;
+        __syncthreads();
+        t2_for_keys(keys, [&](int, uint32_t kj) {
+            if (kj && (kj & pmask) == prefix) atomicAdd(&h[(kj >> shift) & (bins - 1)], 1u);
+        });
+        cluster.sync();
+        t2_merge_hist(cluster, nct, h, S.tot);  // (bins beyond `bins` are zero everywhere)
+        __syncthreads();
+        t2_find_bin<NT>(S.tot, kr, S);
+        kr -= S.res[1];
+        if (pass == 3) res.ties = S.tot[S.res[0]];
+        prefix |= S.res[0] << shift;
+        pmask |= (uint32_t)(bins - 1) << shift;
+    }
+    res.T = prefix;
+    res.keep_ties = kr;
+    return res;
 }
 
 // Steps 1-4 (+ the radix fallback): the threshold of the k largest over the
@@ -233,11 +277,10 @@ __device__ __forceinline__ T2Threshold t2_threshold(cg::cluster_group& cluster, 
     };
     if (!radix) {
         // ---- 2. histogram ----
-        t2_for_keys(keys, [&](int j) {
-            const uint32_t kj = keys(j);
-            const int b = kj ? t2_bin(key_float(kj), lo, inv) : 0;
+        t2_for_keys(keys, [&](int j, uint32_t kj) {  // branch-free: empty slots count into the trash bin
+            const int b = t2_bin(key_float(kj), lo, inv);
             if constexpr (kCacheBin) binc[j] = (uint16_t)b;
-            if (kj) atomicAdd(&S.hist[b], 1u);
+            atomicAdd(&S.hist[kj ? b : kT2Bins], 1u);
         });
         T2_MARK(9);
         cluster.sync();  // #2
@@ -250,21 +293,48 @@ __device__ __forceinline__ T2Threshold t2_threshold(cg::cluster_group& cluster, 
         uint32_t krem = (uint32_t)k - S.res[1];
         // ---- 3. candidates of bin b* ----
         if (bstar != ~0u) {
-            t2_for_keys(keys, [&](int j) {
-                const uint32_t kj = keys(j);
-                const bool c = kj != 0u && bin_of(j) == (int)bstar;
-                const uint32_t m = __ballot_sync(0xffffffffu, c);
-                if (m) {
+            if constexpr (Keys::kStatic == 0) {
+                // two stages: branch-free candidate masks (keys.count() <= 32), then the rare hits
+                uint32_t mine = 0;
+                t2_for_keys(keys, [&](int j, uint32_t kj) {
+                    mine |= (uint32_t)(kj != 0u && t2_bin(key_float(kj), lo, inv) == (int)bstar) << j;
+                });
+                const uint32_t c = __popc(mine);
+                uint32_t pre = c;  // inclusive prefix over lanes
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t y = __shfl_up_sync(0xffffffffu, pre, o);
+                    if (lane >= o) pre += y;
+                }
+                const uint32_t total = __shfl_sync(0xffffffffu, pre, 31);
+                if (total) {
                     uint32_t base = 0;
-                    if (lane == __ffs(m) - 1) base = atomicAdd(&S.ncand, (uint32_t)__popc(m));
-                    base = __shfl_sync(0xffffffffu, base, __ffs(m) - 1);
-                    const uint32_t slot = base + __popc(m & t2_lanemask_lt());
-                    if (c && slot < kT2CtaCand) {
-                        S.ckey[slot] = kj;
-                        S.cidx[slot] = s0 + wbase + 32 * j + lane;
+                    if (lane == 0) base = atomicAdd(&S.ncand, total);
+                    uint32_t slot = __shfl_sync(0xffffffffu, base, 0) + pre - c;
+                    for (uint32_t m = mine; m; m &= m - 1, ++slot) {
+                        const int j = __ffs(m) - 1;
+                        if (slot < kT2CtaCand) {
+                            S.ckey[slot] = keys(j);
+                            S.cidx[slot] = s0 + wbase + 32 * j + lane;
+                        }
                     }
                 }
-            });
+            } else {
+                t2_for_keys(keys, [&](int j, uint32_t kj) {
+                    const bool c = kj != 0u && bin_of(j) == (int)bstar;
+                    const uint32_t m = __ballot_sync(0xffffffffu, c);
+                    if (m) {
+                        uint32_t base = 0;
+                        if (lane == __ffs(m) - 1) base = atomicAdd(&S.ncand, (uint32_t)__popc(m));
+                        base = __shfl_sync(0xffffffffu, base, __ffs(m) - 1);
+                        const uint32_t slot = base + __popc(m & t2_lanemask_lt());
+                        if (c && slot < kT2CtaCand) {
+                            S.ckey[slot] = kj;
+                            S.cidx[slot] = s0 + wbase + 32 * j + lane;
+                        }
+                    }
+                });
+            }
         }
         T2_MARK(12);
         cluster.sync();  // #3: candidate lists complete; merged histogram reads done
@@ -393,33 +463,7 @@ __device__ __forceinline__ T2Threshold t2_threshold(cg::cluster_group& cluster, 
             }
         }
     }
-    if (radix) {
-        // ---- exact MSD radix select on the order-preserving keys (9/9/9/5 bits) ----
-        uint32_t prefix = 0, pmask = 0, kr = (uint32_t)k;
-        uint32_t* h = S.hist;
-#pragma unroll 1
-        for (int pass = 0; pass < 4; ++pass) {
-            const int shift = 23 - 9 * pass > 0 ? 23 - 9 * pass : 0;
-            const int bins = pass == 3 ? 32 : 512;
-            cluster.sync();  // remote readers of the previous histogram are done
-            for (int i = tid; i < kT2Bins; i += NT) h[i] = 0;
-            __syncthreads();
-            t2_for_keys(keys, [&](int j) {
-                const uint32_t kj = keys(j);
-                if (kj && (kj & pmask) == prefix) atomicAdd(&h[(kj >> shift) & (bins - 1)], 1u);
-            });
-            cluster.sync();
-            t2_merge_hist(cluster, nct, h, S.tot);  // (bins beyond `bins` are zero everywhere)
-            __syncthreads();
-            t2_find_bin<NT>(S.tot, kr, S);
-            kr -= S.res[1];
-            if (pass == 3) res.ties = S.tot[S.res[0]];
-            prefix |= S.res[0] << shift;
-            pmask |= (uint32_t)(bins - 1) << shift;
-        }
-        res.T = prefix;
-        res.keep_ties = kr;
-    }
+    if (radix) res = t2_radix_select<NT>(cluster, keys, k, S);
     return res;
 }
 
@@ -427,9 +471,9 @@ __device__ __forceinline__ T2Threshold t2_threshold(cg::cluster_group& cluster, 
 // j of this thread, slot = its position in the row's ascending selection.
 // Returns this CTA's first slot in *cta_base and its kept count in *cta_count.
 // Ends with a cluster barrier: after it no CTA touches a peer's shared memory.
-template <int NT, typename Keys, typename Emit>
+template <int NT, typename Keys, typename Emit, typename SH>
 __device__ __forceinline__ void t2_compact(cg::cluster_group& cluster, const Keys& keys,
-                                           const T2Threshold& th, T2Shared& S, uint32_t* cta_base,
+                                           const T2Threshold& th, SH& S, uint32_t* cta_base,
                                            uint32_t* cta_count, Emit&& emit) {
     const int nct = (int)cluster.num_blocks();
     const int rank = (int)cluster.block_rank();
@@ -439,15 +483,14 @@ __device__ __forceinline__ void t2_compact(cg::cluster_group& cluster, const Key
     // Otherwise ties are ranked by index: kept iff key > T or (key == T and tie rank < keep_ties).
     const bool all_ties = keep_ties >= th.ties;  // cluster-uniform
     uint32_t g = 0, e = 0;
-    t2_for_keys(keys, [&](int j) {
-        const uint32_t kj = keys(j);
-        if (all_ties) {
-            g += __popc(__ballot_sync(0xffffffffu, kj >= T));
-        } else {
+    if (all_ties) {
+        t2_for_keys(keys, [&](int, uint32_t kj) { g += __popc(__ballot_sync(0xffffffffu, kj >= T)); });
+    } else {
+        t2_for_keys(keys, [&](int, uint32_t kj) {
             g += __popc(__ballot_sync(0xffffffffu, kj > T));
             e += __popc(__ballot_sync(0xffffffffu, kj == T));
-        }
-    });
+        });
+    }
     if (lane == 0) {
         S.wg[warp] = g;
         S.we[warp] = e;
@@ -486,15 +529,14 @@ __device__ __forceinline__ void t2_compact(cg::cluster_group& cluster, const Key
     uint32_t gt_run = gb + S.wsum[warp], eq_run = eb + S.wsuf[warp];
     const uint32_t lt = t2_lanemask_lt();
     if (all_ties) {
-        t2_for_keys(keys, [&](int j) {
-            const bool gg = keys(j) >= T;
+        t2_for_keys(keys, [&](int j, uint32_t kj) {
+            const bool gg = kj >= T;
             const uint32_t mg = __ballot_sync(0xffffffffu, gg);
             if (gg) emit(gt_run + __popc(mg & lt), j);
             gt_run += __popc(mg);
         });
     } else {
-        t2_for_keys(keys, [&](int j) {
-            const uint32_t kj = keys(j);
+        t2_for_keys(keys, [&](int j, uint32_t kj) {
             const bool gg = kj > T, ee = kj == T;
             const uint32_t mg = __ballot_sync(0xffffffffu, gg);
             const uint32_t me = __ballot_sync(0xffffffffu, ee);

@@ -1,0 +1,318 @@
+// select_radix.cuh -- Top-k threshold of the fused decode step with a FIXED radix
+// digit histogram built while scoring.
+//
+// Reference: topk_oracle (core.hpp:134-148): the k largest, ties to the lower
+// index, ascending output.  Same cluster/key layout as select.cuh (warp w owns
+// slots [w*32*kpt, (w+1)*32*kpt) of its CTA's slice; key 0 = empty), but the
+// first histogram needs no (min, max) exchange: digit 1 = the top 12 bits of the
+// order-preserving key (sign, exponent, 3 mantissa bits), counted by the scorer
+// as it produces each key (rx_count).  Then:
+//   [cluster barrier]  merge the digit-1 histograms over DSMEM -> bin b1 of the
+//                      k-th largest, krem;
+//   one pass over the keys: candidates (digit 1 == b1) -> this CTA's list, and
+//                      per-warp counts of keys above b1; publish (candidates,
+//                      above);
+//   [cluster barrier]  every CTA gathers all candidates (identical list) and
+//                      refines it by digit 2 (bits 19..8) and digit 3 (bits 7..0)
+//                      down to <= 32 -> exact rank (value desc, index asc) ->
+//                      (T, idx_T); a tie group larger than 32 is resolved by the
+//                      same digit refinement on the indices;
+//   keep rule:         key > T, or key == T and index <= idx_T -- a local test, so
+//                      every CTA derives every CTA's kept count from the published
+//                      "above" counts and the shared candidate list: the output
+//                      offsets need no further cluster barrier.
+// Two cluster barriers instead of four, two passes over the keys instead of four.
+// Candidate overflow (a digit-1 bin holding more than kRxCand keys: very narrow
+// score ranges) falls back to the exact MSD radix select of select.cuh.
+#pragma once
+
+#include "select.cuh"
+
+namespace fier_cuda {
+
+constexpr int kRxBins = 4096;      // digit 1: key >> 20
+constexpr int kRxCtaCand = 512;    // candidates one CTA may contribute
+constexpr int kRxCand = 2048;      // merged candidates per row
+
+// Read by peers until the kernel's final cluster barrier: must not alias anything the
+// CTA reuses after the second barrier.
+struct RxPublished {
+    uint32_t pub[4];               // (candidates, keys above b1) of this CTA
+    uint32_t ckey[kRxCtaCand];     // this CTA's candidates
+    int32_t cidx[kRxCtaCand];
+};
+
+struct RxShared {
+    alignas(16) uint32_t hist[kRxBins + 4];  // digit-1 histogram (scoring; read remotely); [kRxBins] = trash
+    alignas(16) uint32_t tot[kRxBins];       // merged histogram / refinement histograms
+    uint32_t mkey[3][kRxCand];  // [0] all candidates of the row (kept), [1], [2] refinement
+    int32_t midx[3][kRxCand];
+    uint32_t cn[kT2MaxCluster], ca[kT2MaxCluster];     // every CTA's published pair
+    uint32_t ck[kT2MaxCluster];                        // kept candidates per CTA
+    uint32_t wab[32], wkc[32];                         // per warp: keys above b1, kept candidates
+    uint32_t wsum[32], wsuf[32];
+    uint32_t wg[kT2Warps], we[kT2Warps];               // (fallback compaction)
+    uint32_t cgt[kT2MaxCluster], ceq[kT2MaxCluster];
+    uint32_t res[8];
+};
+
+// The scorer's contribution: count key kj (0 = empty -> trash bin).
+__device__ __forceinline__ void rx_count(RxShared& S, uint32_t kj) {
+    atomicAdd(&S.hist[kj ? kj >> 20 : kRxBins], 1u);
+}
+
+// Zero this CTA's digit-1 histogram (before any rx_count; then __syncthreads).
+template <int NT>
+__device__ __forceinline__ void rx_clear(RxShared& S) {
+    for (int i = threadIdx.x; i < kRxBins + 4; i += NT) S.hist[i] = 0u;
+}
+
+// Refine list `src` (n entries) to the entries of the bin holding the krem-th
+// largest of digit(value) (BINS bins); returns the survivors' count (in `dst`).
+template <int NT, int BINS, typename Digit>
+__device__ __forceinline__ uint32_t rx_refine(RxShared& S, const uint32_t* sk, const int32_t* si, uint32_t n,
+                                              uint32_t* dk, int32_t* di, uint32_t& krem, Digit&& digit) {
+    const int tid = threadIdx.x, lane = tid & 31;
+    for (int i = tid; i < BINS; i += NT) S.tot[i] = 0u;
+    __syncthreads();
+    for (uint32_t i = tid; i < n; i += NT) atomicAdd(&S.tot[digit(sk[i], si[i])], 1u);
+    __syncthreads();
+    t2_find_bin<NT, BINS>(S.tot, krem, S);
+    const uint32_t b = S.res[0];
+    krem -= S.res[1];
+    if (tid == 0) S.res[2] = 0;
+    __syncthreads();
+    for (uint32_t i0 = 0; i0 < n; i0 += NT) {
+        const uint32_t i = i0 + tid;
+        const bool c = i < n && digit(sk[i], si[i]) == b;
+        const uint32_t m = __ballot_sync(0xffffffffu, c);
+        if (m) {
+            uint32_t base = 0;
+            if (lane == __ffs(m) - 1) base = atomicAdd(&S.res[2], (uint32_t)__popc(m));
+            base = __shfl_sync(0xffffffffu, base, __ffs(m) - 1);
+            if (c) {
+                const uint32_t slot = base + __popc(m & t2_lanemask_lt());
+                dk[slot] = sk[i];
+                di[slot] = si[i];
+            }
+        }
+    }
+    __syncthreads();
+    return S.res[2];
+}
+
+// Exact rank of <= 32 (key, index) pairs by (key desc, index asc): the krem-th -> (T, idx_T).
+__device__ __forceinline__ void rx_rank32(RxShared& S, const uint32_t* mk, const int32_t* mi, uint32_t n,
+                                          uint32_t krem) {
+    const int lane = threadIdx.x & 31;
+    if ((threadIdx.x >> 5) == 0) {
+        const bool v = (uint32_t)lane < n;
+        const uint32_t ki = v ? mk[lane] : 0u;
+        const int32_t ii = v ? mi[lane] : 0x7fffffff;
+        uint32_t rk = 0;
+        for (uint32_t o = 0; o < n; ++o) {  // smem broadcast reads
+            const uint32_t kj = mk[o];
+            const int32_t ij = mi[o];
+            rk += (kj > ki) || (kj == ki && ij < ii);
+        }
+        const uint32_t hit = __ballot_sync(0xffffffffu, v && rk == krem - 1);
+        const int src = __ffs(hit) - 1;  // unique
+        if (lane == 0) {
+            S.res[4] = __shfl_sync(0xffffffffu, ki, src);
+            S.res[5] = (uint32_t)__shfl_sync(0xffffffffu, ii, src);
+        } else {
+            __shfl_sync(0xffffffffu, ki, src);
+            __shfl_sync(0xffffffffu, ii, src);
+        }
+    }
+    __syncthreads();
+}
+
+struct RxResult {
+    bool fallback;      // cluster-uniform: the caller runs t2_radix_select + t2_compact
+    uint32_t T;         // key of the k-th largest
+    int32_t idxT;       // T-valued keys with index <= idxT are kept
+    uint32_t cta_base;  // this CTA's first output slot
+    uint32_t cta_count; // this CTA's kept keys
+};
+
+// The caller has cleared (rx_clear + __syncthreads) and filled (rx_count) the digit-1
+// histogram and passes slice = tokens per CTA (s0 = rank * slice).  No cluster
+// barrier may be pending: the first one here also proves every CTA is running.
+template <int NT, typename Keys>
+__device__ __forceinline__ RxResult rx_threshold(cg::cluster_group& cluster, const Keys& keys, int s0, int wbase,
+                                                 int slice, int k, RxShared& S, RxPublished& P) {
+    const int nct = (int)cluster.num_blocks();
+    const int rank = (int)cluster.block_rank();
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int kpt = keys.count();
+    RxResult R = {false, 0u, 0, 0u, 0u};
+    __syncthreads();  // this CTA's histogram is complete
+    asm volatile("barrier.cluster.arrive.release;\n\tbarrier.cluster.wait.acquire;" ::: "memory");
+    T2_MARK(8);
+    // ---- digit 1 over the cluster ----
+    t2_merge_hist<kRxBins>(cluster, nct, S.hist, S.tot);
+    if (tid < 32) {
+        S.wkc[tid] = 0u;
+        if (tid < kT2MaxCluster) S.ck[tid] = 0u;
+    }
+    if (tid == 0) P.pub[0] = 0u;
+    __syncthreads();
+    t2_find_bin<NT, kRxBins>(S.tot, (uint32_t)k, S);
+    const uint32_t b1 = S.res[0];
+    uint32_t krem = (uint32_t)k - S.res[1];
+    T2_MARK(9);
+    // ---- candidates (digit 1 == b1) and per-warp counts above b1 ----
+    uint32_t mine = 0, above = 0;
+    t2_for_keys(keys, [&](int j, uint32_t kj) {
+        const uint32_t d = kj ? kj >> 20 : 0u;  // empty slots: never above, never candidates
+        mine |= (uint32_t)(kj != 0u && d == b1) << j;
+        above += __popc(__ballot_sync(0xffffffffu, kj != 0u && d > b1));
+    });
+    {
+        const uint32_t c = __popc(mine);
+        uint32_t pre = c;  // inclusive prefix over lanes
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, pre, o);
+            if (lane >= o) pre += y;
+        }
+        const uint32_t total = __shfl_sync(0xffffffffu, pre, 31);
+        uint32_t base = 0;
+        if (lane == 0) {
+            S.wab[warp] = above;
+            if (total) base = atomicAdd(&P.pub[0], total);
+        }
+        uint32_t slot = __shfl_sync(0xffffffffu, base, 0) + pre - c;
+        for (uint32_t m = mine; m; m &= m - 1, ++slot) {
+            const int j = __ffs(m) - 1;
+            if (slot < kRxCtaCand) {
+                P.ckey[slot] = keys(j);
+                P.cidx[slot] = s0 + wbase + 32 * j + lane;
+            }
+        }
+    }
+    __syncthreads();
+    if (tid == 0) {
+        uint32_t a = 0;
+        for (int w = 0; w < NT / 32; ++w) a += S.wab[w];
+        P.pub[1] = a;
+    }
+    T2_MARK(10);
+    asm volatile("barrier.cluster.arrive.release;\n\tbarrier.cluster.wait.acquire;" ::: "memory");
+    T2_MARK(11);
+    if (tid < nct) {
+        const uint32_t* pp = cluster.map_shared_rank(P.pub, tid);
+        S.cn[tid] = pp[0];
+        S.ca[tid] = pp[1];
+    }
+    __syncthreads();
+    uint32_t n = 0;
+    bool over = b1 == ~0u;
+    for (int r = 0; r < nct; ++r) {
+        over |= S.cn[r] > kRxCtaCand;
+        n += S.cn[r];
+    }
+    over |= n > kRxCand;
+    if (over) {  // cluster-uniform
+        R.fallback = true;
+        return R;
+    }
+    // ---- all candidates of the row, identical in every CTA ----
+    for (uint32_t i = tid; i < n; i += NT) {
+        int r = 0;
+        uint32_t base = 0;
+        while (i >= base + S.cn[r]) base += S.cn[r++];
+        S.mkey[0][i] = cluster.map_shared_rank(P.ckey, r)[i - base];
+        S.midx[0][i] = cluster.map_shared_rank(P.cidx, r)[i - base];
+    }
+    __syncthreads();
+    T2_MARK(12);
+    // ---- refine by digits 2 and 3 of the key, then rank; big exact-tie groups by the index ----
+    const uint32_t* ck = S.mkey[0];
+    const int32_t* ci = S.midx[0];
+    int buf = 1;
+    if (n > 32u) {
+        n = rx_refine<NT, kRxBins>(S, ck, ci, n, S.mkey[buf], S.midx[buf], krem,
+                                   [](uint32_t kk, int32_t) { return (kk >> 8) & 0xFFFu; });
+        ck = S.mkey[buf];
+        ci = S.midx[buf];
+        buf ^= 3;  // 1 <-> 2
+    }
+    if (n > 32u) {
+        n = rx_refine<NT, 256>(S, ck, ci, n, S.mkey[buf], S.midx[buf], krem,
+                               [](uint32_t kk, int32_t) { return kk & 0xFFu; });
+        ck = S.mkey[buf];
+        ci = S.midx[buf];
+        buf ^= 3;
+    }
+    if (n > 32u) {
+        // n > 32 keys all equal to T: keep the krem lowest indices -> the krem-th largest of ~idx
+        const uint32_t T = ck[0];
+        for (int lvl = 0; lvl < 3 && n > 1u; ++lvl) {
+            const int sh = lvl == 0 ? 20 : (lvl == 1 ? 8 : 0);
+            const uint32_t msk = lvl == 2 ? 0xFFu : 0xFFFu;
+            n = rx_refine<NT, kRxBins>(S, ck, ci, n, S.mkey[buf], S.midx[buf], krem,
+                                       [sh, msk](uint32_t, int32_t ii) { return (~(uint32_t)ii >> sh) & msk; });
+            ck = S.mkey[buf];
+            ci = S.midx[buf];
+            buf ^= 3;
+        }
+        if (tid == 0) {
+            S.res[4] = T;
+            S.res[5] = (uint32_t)ci[0];
+        }
+        __syncthreads();
+    } else {
+        rx_rank32(S, ck, ci, n, krem);
+    }
+    R.T = S.res[4];
+    R.idxT = (int32_t)S.res[5];
+    T2_MARK(13);
+    // ---- kept counts: per CTA (from the shared list), per warp (from this CTA's list) ----
+    const uint32_t T = R.T;
+    const int32_t idxT = R.idxT;
+    const uint32_t n0 = [&] {
+        uint32_t t = 0;
+        for (int r = 0; r < nct; ++r) t += S.cn[r];
+        return t;
+    }();
+    for (uint32_t i = tid; i < n0; i += NT) {
+        const uint32_t kk = S.mkey[0][i];
+        const int32_t ii = S.midx[0][i];
+        if (kk > T || (kk == T && ii <= idxT)) atomicAdd(&S.ck[ii / slice], 1u);
+    }
+    for (uint32_t i = tid; i < S.cn[rank]; i += NT) {
+        const uint32_t kk = P.ckey[i];
+        const int32_t ii = P.cidx[i];
+        if (kk > T || (kk == T && ii <= idxT)) atomicAdd(&S.wkc[(ii - s0) / (32 * kpt)], 1u);
+    }
+    __syncthreads();
+    uint32_t cb = 0;
+    for (int r = 0; r < rank; ++r) cb += S.ca[r] + S.ck[r];
+    R.cta_base = cb;
+    R.cta_count = S.ca[rank] + S.ck[rank];
+    return R;
+}
+
+// Emit pass: emit(slot, j) for every kept key j of this thread (slot = position in the
+// row's ascending selection).
+template <int NT, typename Keys, typename Emit>
+__device__ __forceinline__ void rx_emit(const Keys& keys, const RxResult& R, int s0, int wbase, RxShared& S,
+                                        Emit&& emit) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t run = R.cta_base;
+    for (int w = 0; w < warp; ++w) run += S.wab[w] + S.wkc[w];
+    const uint32_t lt = t2_lanemask_lt();
+    const uint32_t T = R.T;
+    const int32_t idxT = R.idxT;
+    t2_for_keys(keys, [&](int j, uint32_t kj) {
+        const int32_t idx = s0 + wbase + 32 * j + lane;
+        const bool kept = kj > T || (kj == T && kj != 0u && idx <= idxT);
+        const uint32_t m = __ballot_sync(0xffffffffu, kept);
+        if (kept) emit(run + __popc(m & lt), j);
+        run += __popc(m);
+    });
+}
+
+}  // namespace fier_cuda

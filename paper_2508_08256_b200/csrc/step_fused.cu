@@ -21,10 +21,11 @@
 //            PRMT (address), one LDS, one FADD -- ~3.5 lane-instructions per 4
 //            bits instead of ~2.5 per bit (score.cu).  Tables are rebuilt per
 //            32-token slab (lane p builds position p), double-buffered per warp.
-//   phase C  cluster Top-k on the register keys (select.cuh: min/max, one
-//            512-bin DSMEM histogram, candidate refinement, exact rank), then the
-//            ballot compaction writes the ascending selection to `sel` and this
-//            CTA's own selected tokens to shared memory.
+//   phase C  cluster Top-k on the shared-memory keys (select_radix.cuh: a fixed
+//            12-bit radix histogram counted by the scorer, merged over DSMEM,
+//            candidate refinement by further digits, exact rank; two cluster
+//            barriers), then the emit pass writes the ascending selection to `sel`
+//            and this CTA's own selected tokens to shared memory.
 //   phase D  8 warps gather the CTA's selected K/V rows through cp.async rings
 //            and run the tensor-core online softmax (attn_tc.cuh); warp partials
 //            merge in shared memory, CTA partials are pushed to rank 0 over DSMEM
@@ -67,7 +68,7 @@ __device__ unsigned long long g_fs_trace[kFsTraceCtas][16];
 #include "attn_tc.cuh"
 #include "nibble.cuh"
 #include "pack.cuh"
-#include "select.cuh"
+#include "select_radix.cuh"
 
 namespace fier_cuda {
 
@@ -82,13 +83,15 @@ constexpr int kFsLutBytes = kNibTableBytes;
 // shared memory map (bytes from a 256-aligned base)
 constexpr int kFsRing = kFsGatherWarps * kFsNst * 2 * tc_stage_bytes<kFsD>();  // phase D rings
 constexpr int kFsLut = 0;                                                    // phase B (inside the ring area)
-constexpr int kFsSel = kFsLut + kFsWarps * 2 * kFsLutBytes;                  // phase C T2Shared (ditto)
-constexpr int kFsKeys = kFsSel + ((int)sizeof(T2Shared) + 255) / 256 * 256;  // phase B/C keys (ditto)
+constexpr int kFsKeys = kFsLut + kFsWarps * 2 * kFsLutBytes;                 // phase B/C keys (ditto)
+constexpr int kFsRx = kFsKeys + kFsThreads * kFsMaxKpt * 4;                  // phase B/C RxShared (ditto)
 constexpr int kFsSidx = kFsRing;                                             // u16 selected slots
-constexpr int kFsWres = kFsSidx + kFsThreads * kFsMaxKpt * 2;                // warp partials
+constexpr int kFsPub = kFsSidx + kFsThreads * kFsMaxKpt * 2;                 // RxPublished (read by peers)
+constexpr int kFsWres = kFsPub + ((int)sizeof(RxPublished) + 15) / 16 * 16;  // warp partials
 constexpr int kFsCres = kFsWres + kFsGatherWarps * (kFsD + 2) * 4;           // CTA partials (rank 0)
 constexpr int kFsSmem = kFsCres + kT2MaxCluster * (kFsD + 2) * 4 + 256;      // + base alignment
-static_assert(kFsKeys + kFsThreads * kFsMaxKpt * 4 <= kFsRing, "LUTs, T2Shared and keys must fit in the ring area");
+static_assert(kFsRx + (int)sizeof(RxShared) <= kFsRing, "LUTs, keys and RxShared must fit in the ring area");
+static_assert(sizeof(T2Shared) <= sizeof(RxShared), "");
 static_assert(kFsSmem <= 227 * 1024, "fused step exceeds shared memory");
 
 
@@ -127,14 +130,15 @@ __global__ void __launch_bounds__(kFsThreads, 1) step_fused_kernel(const FsArgs 
     const uint32_t raw = smem_u32(smem_raw);
     const uint32_t base = (raw + 255u) & ~255u;
     uint8_t* smem = smem_raw + (base - raw);
-    T2Shared& S = *reinterpret_cast<T2Shared*>(smem + kFsSel);
+    RxShared& S = *reinterpret_cast<RxShared*>(smem + kFsRx);
+    RxPublished& P = *reinterpret_cast<RxPublished*>(smem + kFsPub);
     uint16_t* sidx = reinterpret_cast<uint16_t*>(smem + kFsSidx);
     float* wres = reinterpret_cast<float*>(smem + kFsWres);
     float* cres = reinterpret_cast<float*>(smem + kFsCres);
     uint32_t* keys_s = reinterpret_cast<uint32_t*>(smem + kFsKeys);
 
-    // peers store into this CTA's shared memory only after the wait in t2_threshold
-    asm volatile("barrier.cluster.arrive.relaxed;" ::: "memory");
+    rx_clear<kFsThreads>(S);  // the scorer counts every key into the digit-1 histogram
+    __syncthreads();
     FS_MARK(0);
 
     T* Kseq = static_cast<T*>(a.K) + seq * a.cap * D;
@@ -161,7 +165,6 @@ __global__ void __launch_bounds__(kFsThreads, 1) step_fused_kernel(const FsArgs 
         for (int i = 0; i < 4; ++i) qv[i] = to_f32(qp[i]);
     }
     const uint32_t tab0 = base + kFsLut + warp * 2 * kFsLutBytes;
-    float mn = INFINITY, mx = -INFINITY;
     float* srow = a.scores ? a.scores + (int64_t)row * a.ld : nullptr;
     // Scoring is assigned per slab (32 tokens), independently of which warp owns the
     // slab's keys in phase C (keys are stored token-ordered: slab sl -> keys_s[32 sl ..]).
@@ -195,14 +198,11 @@ __global__ void __launch_bounds__(kFsThreads, 1) step_fused_kernel(const FsArgs 
             const float sc = nibble_score(tab, bw);
             if (t < a.tokens) {
                 key = isnan(sc) ? 0u : float_key(sc);
-                if (isfinite(sc)) {
-                    mn = fminf(mn, sc);
-                    mx = fmaxf(mx, sc);
-                }
                 if (srow) srow[t] = sc;
             }
         }
         keys_s[32 * sl + lane] = key;
+        rx_count(S, key);
     };
     auto load = [&](int sl, uint4& p, uint4& bw) {
         const int t0 = s0 + 32 * sl;
@@ -241,16 +241,22 @@ __global__ void __launch_bounds__(kFsThreads, 1) step_fused_kernel(const FsArgs 
     // ---- phase C: cluster Top-k, compaction to sel (global) and sidx (this CTA) ----
     FS_MARK(2);
     const SmemKeys keys{keys_s + wbase, kpt};  // phase C ownership: warp w, slot j, lane L
-    const T2Threshold th = t2_threshold<kFsThreads>(cluster, keys, mn, mx, s0, wbase, a.k, S);
+    const RxResult rx = rx_threshold<kFsThreads>(cluster, keys, s0, wbase, slice, a.k, S, P);
     FS_MARK(3);
     int32_t* selrow = a.sel + (int64_t)row * a.k;
-    uint32_t cbase = 0, ccount = 0;
-    t2_compact<kFsThreads>(cluster, keys, th, S, &cbase, &ccount, [&](uint32_t slot, int j) {
+    uint32_t cbase = rx.cta_base, ccount = rx.cta_count;
+    auto emit = [&](uint32_t slot, int j) {
         const int local = wbase + 32 * j + lane;
         selrow[slot] = s0 + local;
         sidx[slot - cbase] = (uint16_t)local;
-    });
-    __syncthreads();  // sidx complete; T2Shared (inside the ring area) no longer read
+    };
+    if (!rx.fallback) {
+        rx_emit<kFsThreads>(keys, rx, s0, wbase, S, emit);
+    } else {  // candidate overflow (very narrow score range): exact MSD radix select
+        const T2Threshold th = t2_radix_select<kFsThreads>(cluster, keys, a.k, S);
+        t2_compact<kFsThreads>(cluster, keys, th, S, &cbase, &ccount, emit);
+    }
+    __syncthreads();  // sidx complete; RxShared (inside the ring area) no longer read
     FS_MARK(4);
 
     // ---- phase D: attention over this CTA's selected rows ----

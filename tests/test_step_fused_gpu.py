@@ -88,6 +88,27 @@ def test_fused_step_all_ties(cuda, port):
     check(port, layer, q, kn, out, sel, scores, pos, n, 32)
 
 
+@pytest.mark.parametrize("tokens,n", [(1000, 300), (700, 699), (40, 7)])
+def test_fused_step_tie_groups(cuda, port, tokens, n):
+    """Constant keys with fewer ties than the radix candidate buffer: the threshold is
+    one tie group resolved by the digit refinement on the indices (lowest indices kept)."""
+    B, H, cap = 1, 3, tokens + 64
+    K = torch.full((B, H, cap, 128), -0.25, device=cuda)
+    layer, q, kn, vn, out, sel, scores = run_step(cuda, B, H, cap, tokens - 1, n, 32, "bf16", K=K)
+    np.testing.assert_array_equal(sel.cpu().numpy(), np.broadcast_to(np.arange(n), (B, H, n)))
+    check(port, layer, q, kn, out, sel, scores, tokens - 1, n, 32)
+
+
+def test_fused_step_narrow_scores(cuda, port):
+    """Scores squeezed into one radix bin (keys = 8 + tiny noise, q > 0): candidate
+    overflow takes the exact MSD radix fallback."""
+    torch.manual_seed(21)
+    B, H, cap, pos, n = 1, 2, 6000, 5000, 551
+    K = 8.0 + 1e-3 * torch.randn(B, H, cap, 128, device=cuda)
+    layer, q, kn, vn, out, sel, scores = run_step(cuda, B, H, cap, pos, n, 32, "bf16", K=K)
+    check(port, layer, q, kn, out, sel, scores, pos, n, 32)
+
+
 def test_fused_step_repeated_decode(cuda, port):
     """Several consecutive steps through the same layer (appends crossing a group boundary)
     leave the index equal to a one-shot quantize of the grown cache."""
