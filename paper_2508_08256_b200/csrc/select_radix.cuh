@@ -7,13 +7,14 @@
 // first histogram needs no (min, max) exchange: digit 1 = the top 12 bits of the
 // order-preserving key (sign, exponent, 3 mantissa bits), counted by the scorer
 // as it produces each key (rx_count).  Then:
-//   [cluster barrier]  merge the digit-1 histograms over DSMEM -> bin b1 of the
-//                      k-th largest, krem;
+//   [cluster barrier]  merge the 64 coarse sums (64 digit-1 bins each) over DSMEM ->
+//                      coarse bin of the k-th largest -> merge its 64 fine bins ->
+//                      bin b1, krem (one warp, shuffles; 2 KB of remote reads);
 //   one pass over the keys: candidates (digit 1 == b1) -> this CTA's list, and
 //                      per-warp counts of keys above b1; publish (candidates,
 //                      above);
 //   [cluster barrier]  every CTA gathers all candidates (identical list) and
-//                      refines it by digit 2 (bits 19..8) and digit 3 (bits 7..0)
+//                      refines it by 8-bit digits (bits 19..12, 11..4, 3..0)
 //                      down to <= 32 -> exact rank (value desc, index asc) ->
 //                      (T, idx_T); a tie group larger than 32 is resolved by the
 //                      same digit refinement on the indices;
@@ -30,7 +31,7 @@
 
 namespace fier_cuda {
 
-constexpr int kRxBins = 4096;      // digit 1: key >> 20
+constexpr int kRxBins = 4096;      // digit 1: key >> 20 (64 coarse x 64 fine bins)
 constexpr int kRxCtaCand = 512;    // candidates one CTA may contribute
 constexpr int kRxCand = 2048;      // merged candidates per row
 
@@ -44,7 +45,8 @@ struct RxPublished {
 
 struct RxShared {
     alignas(16) uint32_t hist[kRxBins + 4];  // digit-1 histogram (scoring; read remotely); [kRxBins] = trash
-    alignas(16) uint32_t tot[kRxBins];       // merged histogram / refinement histograms
+    alignas(16) uint32_t tot[kRxBins];       // refinement histograms
+    alignas(16) uint32_t coarse[64];         // sums of 64 consecutive digit-1 bins (read remotely)
     uint32_t mkey[3][kRxCand];  // [0] all candidates of the row (kept), [1], [2] refinement
     int32_t midx[3][kRxCand];
     uint32_t cn[kT2MaxCluster], ca[kT2MaxCluster];     // every CTA's published pair
@@ -128,6 +130,51 @@ __device__ __forceinline__ void rx_rank32(RxShared& S, const uint32_t* mk, const
     __syncthreads();
 }
 
+// One warp, 64 bins held 2 per lane (bin 2l -> c0, 2l+1 -> c1): the bin b with
+// above(b) < kr <= above(b) + cnt(b), above(b) = count in bins > b.  Returns b (-1 if none)
+// and above(b) in *ab (every lane).
+__device__ __forceinline__ int rx_warp_find64(uint32_t c0, uint32_t c1, uint32_t kr, uint32_t* ab) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t sl = c0 + c1;
+    uint32_t suf = sl;  // inclusive suffix over lanes (higher lanes hold higher bins)
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_down_sync(0xffffffffu, suf, o);
+        if (lane + o < 32) suf += y;
+    }
+    const uint32_t a1 = suf - sl, a0 = a1 + c1;
+    const bool h1 = a1 < kr && kr <= a1 + c1, h0 = a0 < kr && kr <= a0 + c0;
+    const uint32_t m = __ballot_sync(0xffffffffu, h0 || h1);
+    if (!m) return -1;
+    const int src = __ffs(m) - 1;
+    const int b = 2 * src + (__shfl_sync(0xffffffffu, (int)h1, src) ? 1 : 0);
+    *ab = __shfl_sync(0xffffffffu, h1 ? a1 : a0, src);
+    return b;
+}
+
+// Sum over the cluster's CTAs of two consecutive u32 words at local shared address `a`.
+__device__ __forceinline__ uint2 rx_cluster_sum2(uint32_t a, int nct) {
+    uint2 t = make_uint2(0u, 0u);
+    for (int r0 = 0; r0 < nct; r0 += 4) {
+        uint2 v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            v[u] = make_uint2(0u, 0u);
+            if (r0 + u < nct) {
+                uint32_t ra;
+                asm("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(a), "r"(r0 + u));
+                asm volatile("ld.shared::cluster.v2.u32 {%0,%1}, [%2];" : "=r"(v[u].x), "=r"(v[u].y) : "r"(ra));
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            t.x += v[u].x;
+            t.y += v[u].y;
+        }
+    }
+    return t;
+}
+
 struct RxResult {
     bool fallback;      // cluster-uniform: the caller runs t2_radix_select + t2_compact
     uint32_t T;         // key of the k-th largest
@@ -148,19 +195,44 @@ __device__ __forceinline__ RxResult rx_threshold(cg::cluster_group& cluster, con
     const int kpt = keys.count();
     RxResult R = {false, 0u, 0, 0u, 0u};
     __syncthreads();  // this CTA's histogram is complete
+    for (int c = warp; c < 64; c += NT / 32) {  // coarse bins: 64 fine bins each, two per lane
+        const uint2 v = reinterpret_cast<const uint2*>(S.hist + 64 * c)[lane];
+        uint32_t x = v.x + v.y;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+        if (lane == 0) S.coarse[c] = x;
+    }
     asm volatile("barrier.cluster.arrive.release;\n\tbarrier.cluster.wait.acquire;" ::: "memory");
     T2_MARK(8);
-    // ---- digit 1 over the cluster ----
-    t2_merge_hist<kRxBins>(cluster, nct, S.hist, S.tot);
+    // ---- digit 1 over the cluster: coarse bin, then its 64 fine bins (2 KB of DSMEM reads) ----
     if (tid < 32) {
         S.wkc[tid] = 0u;
         if (tid < kT2MaxCluster) S.ck[tid] = 0u;
     }
     if (tid == 0) P.pub[0] = 0u;
+    if (warp == 0) {
+        uint32_t ab = 0, kr = (uint32_t)k;
+        const uint2 cc = rx_cluster_sum2(smem_u32(S.coarse) + 8u * lane, nct);
+        const int cb = rx_warp_find64(cc.x, cc.y, kr, &ab);
+        int b = -1;
+        if (cb >= 0) {
+            kr -= ab;
+            const uint2 ff = rx_cluster_sum2(smem_u32(S.hist + 64 * cb) + 8u * lane, nct);
+            const int fb = rx_warp_find64(ff.x, ff.y, kr, &ab);
+            if (fb >= 0) {
+                b = 64 * cb + fb;
+                kr -= ab;
+            }
+        }
+        if (lane == 0) {
+            S.res[0] = (uint32_t)b;
+            S.res[1] = kr;
+        }
+    }
     __syncthreads();
-    t2_find_bin<NT, kRxBins>(S.tot, (uint32_t)k, S);
-    const uint32_t b1 = S.res[0];
-    uint32_t krem = (uint32_t)k - S.res[1];
+    T2_MARK(14);
+    const uint32_t b1 = S.res[0];  // ~0u: fewer keys than k (NaN scores) -> fallback
+    uint32_t krem = S.res[1];
     T2_MARK(9);
     // ---- candidates (digit 1 == b1) and per-warp counts above b1 ----
     uint32_t mine = 0, above = 0;
@@ -232,28 +304,24 @@ __device__ __forceinline__ RxResult rx_threshold(cg::cluster_group& cluster, con
     const uint32_t* ck = S.mkey[0];
     const int32_t* ci = S.midx[0];
     int buf = 1;
-    if (n > 32u) {
-        n = rx_refine<NT, kRxBins>(S, ck, ci, n, S.mkey[buf], S.midx[buf], krem,
-                                   [](uint32_t kk, int32_t) { return (kk >> 8) & 0xFFFu; });
+#pragma unroll 1
+    for (int lvl = 0; lvl < 3 && n > 32u; ++lvl) {  // key bits 19..12, 11..4, 3..0
+        const int sh = lvl == 0 ? 12 : (lvl == 1 ? 4 : 0);
+        const uint32_t msk = lvl == 2 ? 0xFu : 0xFFu;
+        n = rx_refine<NT, 256>(S, ck, ci, n, S.mkey[buf], S.midx[buf], krem,
+                               [sh, msk](uint32_t kk, int32_t) { return (kk >> sh) & msk; });
         ck = S.mkey[buf];
         ci = S.midx[buf];
         buf ^= 3;  // 1 <-> 2
     }
     if (n > 32u) {
-        n = rx_refine<NT, 256>(S, ck, ci, n, S.mkey[buf], S.midx[buf], krem,
-                               [](uint32_t kk, int32_t) { return kk & 0xFFu; });
-        ck = S.mkey[buf];
-        ci = S.midx[buf];
-        buf ^= 3;
-    }
-    if (n > 32u) {
         // n > 32 keys all equal to T: keep the krem lowest indices -> the krem-th largest of ~idx
         const uint32_t T = ck[0];
-        for (int lvl = 0; lvl < 3 && n > 1u; ++lvl) {
-            const int sh = lvl == 0 ? 20 : (lvl == 1 ? 8 : 0);
-            const uint32_t msk = lvl == 2 ? 0xFFu : 0xFFFu;
-            n = rx_refine<NT, kRxBins>(S, ck, ci, n, S.mkey[buf], S.midx[buf], krem,
-                                       [sh, msk](uint32_t, int32_t ii) { return (~(uint32_t)ii >> sh) & msk; });
+#pragma unroll 1
+        for (int lvl = 0; lvl < 4 && n > 1u; ++lvl) {
+            const int sh = 24 - 8 * lvl;
+            n = rx_refine<NT, 256>(S, ck, ci, n, S.mkey[buf], S.midx[buf], krem,
+                                   [sh](uint32_t, int32_t ii) { return (~(uint32_t)ii >> sh) & 0xFFu; });
             ck = S.mkey[buf];
             ci = S.midx[buf];
             buf ^= 3;
@@ -306,13 +374,19 @@ __device__ __forceinline__ void rx_emit(const Keys& keys, const RxResult& R, int
     const uint32_t lt = t2_lanemask_lt();
     const uint32_t T = R.T;
     const int32_t idxT = R.idxT;
+    uint32_t kept = 0;  // stage 1: this lane's kept slots (keys.count() <= 32), branch-free
     t2_for_keys(keys, [&](int j, uint32_t kj) {
         const int32_t idx = s0 + wbase + 32 * j + lane;
-        const bool kept = kj > T || (kj == T && kj != 0u && idx <= idxT);
-        const uint32_t m = __ballot_sync(0xffffffffu, kept);
-        if (kept) emit(run + __popc(m & lt), j);
-        run += __popc(m);
+        kept |= (uint32_t)(kj > T || (kj == T && idx <= idxT)) << j;
     });
+    const int n = keys.count();  // stage 2: positions by ballots, no key reads
+#pragma unroll 4
+    for (int j = 0; j < n; ++j) {
+        const bool kb = (kept >> j) & 1u;
+        const uint32_t m = __ballot_sync(0xffffffffu, kb);
+        if (kb) emit(run + __popc(m & lt), j);
+        run += __popc(m);
+    }
 }
 
 }  // namespace fier_cuda

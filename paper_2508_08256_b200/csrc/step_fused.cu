@@ -111,6 +111,22 @@ struct FsArgs {
     float scale_log2;
 };
 
+// The degenerate-row path, out of line: its code would otherwise sit between the hot
+// phases and be streamed through the instruction cache every step.
+__device__ __noinline__ void fused_fallback_select(cg::cluster_group& cluster, const SmemKeys& keys, int k,
+                                                   RxShared& S, int32_t* selrow, uint16_t* sidx, int s0,
+                                                   int wbase, uint32_t* cbase, uint32_t* ccount) {
+    const int lane = threadIdx.x & 31;
+    const T2Threshold th = t2_radix_select<kFsThreads>(cluster, keys, k, S);
+    uint32_t base = 0;
+    t2_compact<kFsThreads>(cluster, keys, th, S, cbase, ccount, [&](uint32_t slot, int j) {
+        const int local = wbase + 32 * j + lane;
+        selrow[slot] = s0 + local;
+        sidx[slot - *cbase] = (uint16_t)local;
+    });
+    (void)base;
+}
+
 template <typename T>
 __global__ void __launch_bounds__(kFsThreads, 1) step_fused_kernel(const FsArgs a) {
     constexpr int D = kFsD;
@@ -253,8 +269,7 @@ __global__ void __launch_bounds__(kFsThreads, 1) step_fused_kernel(const FsArgs 
     if (!rx.fallback) {
         rx_emit<kFsThreads>(keys, rx, s0, wbase, S, emit);
     } else {  // candidate overflow (very narrow score range): exact MSD radix select
-        const T2Threshold th = t2_radix_select<kFsThreads>(cluster, keys, a.k, S);
-        t2_compact<kFsThreads>(cluster, keys, th, S, &cbase, &ccount, emit);
+        fused_fallback_select(cluster, keys, a.k, S, selrow, sidx, s0, wbase, &cbase, &ccount);
     }
     __syncthreads();  // sidx complete; RxShared (inside the ring area) no longer read
     FS_MARK(4);

@@ -23,7 +23,7 @@ import paper_2508_08256_b200 as F  # noqa: E402
 from paper_2508_08256_b200 import _lib  # noqa: E402
 
 NAMES = ["start", "append", "score", "threshold", "compact", "gather", "merge_sync", "out",
-         "t:hist_sync", "t:find_bin", "t:cand_local", "t:cand_sync", "t:cand_gather", "t:rank", "-", "-"]
+         "t:hist_sync", "t:find_bin", "t:cand_local", "t:cand_sync", "t:cand_gather", "t:rank", "t:merged", "-"]
 
 
 def main():
