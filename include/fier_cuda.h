@@ -130,9 +130,13 @@ FIER_API int fier_full_attention(const fier_shape* s, const void* q, const void*
 /* fier_attend (retrieval.hpp:136-146) for a decode step of every (b, q head):
  * append(pos) -> score -> Top-n -> sparse attention, over tokens = pos + 1.
  * scores_out (may be NULL) receives the estimated logits (ld = tokens rounded
- * up to 32, see fier_step_scores_ld). */
+ * up to 32, see fier_step_scores_ld).  MHA layers with d = 128, 32 | g, 16-bit
+ * caches and tokens <= 131072 run as ONE cluster kernel (step_fused.cu);
+ * other shapes as append+score, Top-k and sparse-attention launches. */
 FIER_API size_t fier_decode_workspace(const fier_shape* s, int32_t tokens, int32_t n);
 FIER_API int64_t fier_step_scores_ld(int32_t tokens);
+/* Kernel launches fier_decode_step issues for this shape (1 = the fused kernel). */
+FIER_API int32_t fier_decode_step_launches(const fier_shape* s, int32_t tokens, int32_t n);
 FIER_API int fier_decode_step(const fier_shape* s, const void* q, const void* k_new, const void* v_new,
                      int32_t pos, void* K, void* V, uint32_t* bits, void* params, int32_t n,
                      float scale, float* out, int32_t* sel, float* scores_out, void* workspace,

@@ -21,6 +21,7 @@ EXPORTS = (
     "fier_pack_keys", "fier_append", "fier_score", "fier_topk_workspace", "fier_topk",
     "fier_sparse_attention_workspace", "fier_sparse_attention", "fier_full_attention_workspace",
     "fier_full_attention", "fier_decode_workspace", "fier_step_scores_ld", "fier_decode_step",
+    "fier_decode_step_launches",
     "fier_index_to_fier", "fier_fier_to_index", "fier_sparse_attention_ragged", "fier_shard_bounds",
     "fier_shard_candidates", "fier_shard_merge_workspace", "fier_shard_merge", "fier_lse_merge",
 )
@@ -64,6 +65,7 @@ _SIGS = {
     "fier_full_attention": ([_SP, _vp, _vp, _vp, _i32, C.c_float, _vp, _vp, _sz, _vp], C.c_int),
     "fier_decode_workspace": ([_SP, _i32, _i32], _sz),
     "fier_step_scores_ld": ([_i32], _i64),
+    "fier_decode_step_launches": ([_SP, _i32, _i32], _i32),
     "fier_decode_step": ([_SP, _vp, _vp, _vp, _i32, _vp, _vp, _vp, _vp, _i32, C.c_float, _vp, _vp,
                           _vp, _vp, _sz, _vp], C.c_int),
     "fier_sparse_attention_ragged": ([_SP, _vp, _vp, _vp, _vp, _vp, _i32, _i32, C.c_float, _vp, _vp, _vp,

@@ -651,6 +651,9 @@ int full_dispatch(const fier_shape* s, const void* q, const void* K, const void*
     return merge(s, part, p.nsplit, out, st);
 }
 
+// True when the sparse attention merges its CTA partials in-kernel (no merge launch).
+bool attn_fused_merge(const fier_shape* s) { return fast_dim(s); }
+
 // Offset of the counter words inside a sparse workspace (for the fused step).
 size_t sparse_counter_offset(const fier_shape* s, int n) { return part_bytes(s, sparse_plan(s, n).nsplit); }
 

@@ -42,6 +42,8 @@ int append_score_dispatch(const fier_shape*, const void*, void*, void*, const vo
                           uint32_t*, void*, float*, int64_t, int*, int, cudaStream_t);
 int fused_step_dispatch(const fier_shape*, const void*, const void*, const void*, int, void*, void*, uint32_t*,
                         void*, int, float, float*, int32_t*, float*, int64_t, cudaStream_t);
+bool fused_step_applies(const fier_shape*, int tokens);
+bool attn_fused_merge(const fier_shape*);
 
 static int check_shape(const fier_shape* s, const char* fn) {
     const std::string f(fn);
@@ -217,6 +219,13 @@ int fier_decode_step(const fier_shape* s, const void* q, const void* k_new, cons
     rc = topk_dispatch(scores, s->batch * s->q_heads, tokens, ld, n, sel, st);
     if (rc) return rc;
     return sparse_dispatch(s, q, K, V, sel, n, tokens, scale, out, attn_ws, true, st, nullptr, nullptr);
+}
+
+int32_t fier_decode_step_launches(const fier_shape* s, int32_t tokens, int32_t n) {
+    if (check_shape(s, "fier_decode_step") || tokens < 1 || n < 1 || n > tokens) return 0;
+    if (fused_step_applies(s, tokens)) return 1;
+    // append+score, Top-k, sparse attention (+ a separate LSE merge on the generic attention path)
+    return attn_fused_merge(s) ? 3 : 4;
 }
 
 // ---- host-side FIER conversion (io.hpp:197-277) ------------------------------------

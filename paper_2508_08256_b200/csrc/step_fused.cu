@@ -78,7 +78,7 @@ constexpr int kFsD = 128;
 constexpr int kFsGatherWarps = 8;
 constexpr int kFsNst = 3;
 constexpr int kFsMaxKpt = 16;  // slice <= 8192 tokens (u16 slots in sidx)
-constexpr int kFsAppendSlabs = 3;  // sealed slabs the append warps hand to the others (~ the append's time)
+constexpr int kFsAppendSlabs = 5;  // sealed slabs the append warps hand to the others (~ the append's time)
 constexpr int kFsLutBytes = kNibTableBytes;
 // shared memory map (bytes from a 256-aligned base)
 constexpr int kFsRing = kFsGatherWarps * kFsNst * 2 * tc_stage_bytes<kFsD>();  // phase D rings
@@ -378,13 +378,22 @@ static bool fused_plan(int rows, int tokens, int g, int* cluster, int* kpt) {
     return true;
 }
 
+static bool fused_shape_ok(const fier_shape* s) {
+    if (s->q_heads != s->kv_heads || s->dim != kFsD || s->group % 32 != 0) return false;
+    return s->dtype == FIER_BF16 || s->dtype == FIER_F16;
+}
+
+bool fused_step_applies(const fier_shape* s, int tokens) {
+    int cluster = 0, kpt = 0;
+    return !fused_disabled() && fused_shape_ok(s) && s->batch * s->q_heads <= 65535 &&
+           fused_plan(s->batch * s->q_heads, tokens, s->group, &cluster, &kpt);
+}
+
 // Returns -1 when the shape is not covered (the caller runs the separate kernels).
 int fused_step_dispatch(const fier_shape* s, const void* q, const void* k_new, const void* v_new, int pos, void* K,
                         void* V, uint32_t* bits, void* params, int n, float scale, float* out, int32_t* sel,
                         float* scores_out, int64_t ld, cudaStream_t st) {
-    if (fused_disabled()) return -1;
-    if (s->q_heads != s->kv_heads || s->dim != kFsD || s->group % 32 != 0) return -1;
-    if (s->dtype != FIER_BF16 && s->dtype != FIER_F16) return -1;
+    if (fused_disabled() || !fused_shape_ok(s)) return -1;
     const int tokens = pos + 1, rows = s->batch * s->q_heads;
     if (rows > 65535) return -1;
     int cluster = 0, kpt = 0;
