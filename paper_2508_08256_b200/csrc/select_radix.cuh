@@ -45,7 +45,7 @@ struct RxPublished {
 
 struct RxShared {
     alignas(16) uint32_t hist[kRxBins + 4];  // digit-1 histogram (scoring; read remotely); [kRxBins] = trash
-    alignas(16) uint32_t tot[kRxBins];       // refinement histograms
+    alignas(16) uint32_t tot[kT2Bins];       // refinement histograms (8-bit digits); fallback merges
     alignas(16) uint32_t coarse[64];         // sums of 64 consecutive digit-1 bins (read remotely)
     uint32_t mkey[3][kRxCand];  // [0] all candidates of the row (kept), [1], [2] refinement
     int32_t midx[3][kRxCand];

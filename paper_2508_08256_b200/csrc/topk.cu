@@ -609,10 +609,14 @@ static int launch_cluster(Kern kern, int cluster, int rows, int threads, size_t 
 
 int topk2_dispatch(const float*, int, int, int64_t, int, int32_t*, cudaStream_t);
 
+int topk_rx_dispatch(const float* scores, int rows, int tokens, int64_t ld, int k, int32_t* sel, cudaStream_t st);
+
 int topk_dispatch(const float* scores, int rows, int tokens, int64_t ld, int k, int32_t* sel,
                   cudaStream_t st) {
-    {
-        const int rc = topk2_dispatch(scores, rows, tokens, ld, k, sel, st);
+    {  // adaptive cluster select (topk2.cu); FIER_TOPK=rx: the fixed-radix one (topk_rx.cu)
+        int rc = topk_rx_dispatch(scores, rows, tokens, ld, k, sel, st);
+        if (rc >= 0) return rc;
+        rc = topk2_dispatch(scores, rows, tokens, ld, k, sel, st);
         if (rc >= 0) return rc;
     }
     // Register path: CTA slices up to 512 x 16 (or 256 x 64) keys, cluster of

@@ -356,3 +356,31 @@ def test_topk_register_path_shapes(cuda, port, rows, l, k):
         assert (np.diff(sel, axis=1) > 0).all()
         for r in range(8, rows, max(1, rows // 16)):
             np.testing.assert_array_equal(sel[r], port.topk(s[r].double().numpy(), k))
+
+
+_RX = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, {root!r})
+import paper_2508_08256_b200 as F
+from oracle.oracle import Port
+port = Port()
+g = torch.Generator().manual_seed(5)
+for rows, l, k in [(3, 5000, 550), (2, 70000, 4096), (4, 300, 300)]:
+    s = torch.randn(rows, l, generator=g)
+    got = F.topk_oracle(s.cuda(), k).cpu().numpy()
+    for r in range(rows):
+        assert np.array_equal(got[r], port.topk(s[r].double().numpy(), k))
+print("rx ok")
+"""
+
+
+def test_topk_rx_path_matches(cuda):
+    """FIER_TOPK=rx selects the fixed-radix cluster select (topk_rx.cu) instead of the
+    adaptive-histogram one (topk2.cu): both stay exact (A/B measurements)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", _RX.format(root=root)], env=dict(os.environ, FIER_TOPK="rx"),
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "rx ok" in r.stdout, r.stdout + r.stderr
