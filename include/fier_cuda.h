@@ -137,6 +137,25 @@ FIER_API size_t fier_decode_workspace(const fier_shape* s, int32_t tokens, int32
 FIER_API int64_t fier_step_scores_ld(int32_t tokens);
 /* Kernel launches fier_decode_step issues for this shape (1 = the fused kernel). */
 FIER_API int32_t fier_decode_step_launches(const fier_shape* s, int32_t tokens, int32_t n);
+
+/* Rotary position embedding fused into the step (the KV write +
+ * RoPE + append-pack that precedes scoring in a decode loop).  q (every q head) and
+ * k_new (every kv head) are rotated by position pos before use: frequency i < rd/2
+ * turns by pos * base^(-2i/rd) (angles evaluated in double on the host), channels
+ * >= rd pass through.  interleaved = 0: pairs (i, i + rd/2) ("rotate_half", NeoX /
+ * Llama); 1: pairs (2i, 2i + 1) (GPT-J).  v_new is not rotated.  The rotation is
+ * evaluated in fp32 and rounded to the cache dtype; the rotated k row is what the
+ * cache stores and the index packs. */
+typedef struct fier_rope {
+    float base;          /* e.g. 10000 */
+    int32_t rotary_dim;  /* rd: even, 2 <= rd <= min(dim, 128) */
+    int32_t interleaved;
+} fier_rope;
+/* fier_decode_step with an optional rope (NULL: none); same workspace. */
+FIER_API int fier_decode_step_ex(const fier_shape* s, const void* q, const void* k_new, const void* v_new,
+                        int32_t pos, void* K, void* V, uint32_t* bits, void* params, int32_t n,
+                        float scale, const fier_rope* rope, float* out, int32_t* sel, float* scores_out,
+                        void* workspace, size_t workspace_bytes, void* stream);
 FIER_API int fier_decode_step(const fier_shape* s, const void* q, const void* k_new, const void* v_new,
                      int32_t pos, void* K, void* V, uint32_t* bits, void* params, int32_t n,
                      float scale, float* out, int32_t* sel, float* scores_out, void* workspace,

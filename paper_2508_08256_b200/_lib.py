@@ -21,7 +21,7 @@ EXPORTS = (
     "fier_pack_keys", "fier_append", "fier_score", "fier_topk_workspace", "fier_topk",
     "fier_sparse_attention_workspace", "fier_sparse_attention", "fier_full_attention_workspace",
     "fier_full_attention", "fier_decode_workspace", "fier_step_scores_ld", "fier_decode_step",
-    "fier_decode_step_launches",
+    "fier_decode_step_launches", "fier_decode_step_ex",
     "fier_index_to_fier", "fier_fier_to_index", "fier_sparse_attention_ragged", "fier_shard_bounds",
     "fier_shard_candidates", "fier_shard_merge_workspace", "fier_shard_merge", "fier_lse_merge",
 )
@@ -31,6 +31,11 @@ class FierShape(C.Structure):
     _fields_ = [("batch", C.c_int32), ("q_heads", C.c_int32), ("kv_heads", C.c_int32),
                 ("capacity", C.c_int32), ("dim", C.c_int32), ("group", C.c_int32),
                 ("dtype", C.c_int32)]
+
+
+class FierRope(C.Structure):
+    """fier_rope: rotary embedding fused into the decode step (include/fier_cuda.h)."""
+    _fields_ = [("base", C.c_float), ("rotary_dim", C.c_int32), ("interleaved", C.c_int32)]
 
 
 class FierDataError(RuntimeError):
@@ -66,6 +71,8 @@ _SIGS = {
     "fier_decode_workspace": ([_SP, _i32, _i32], _sz),
     "fier_step_scores_ld": ([_i32], _i64),
     "fier_decode_step_launches": ([_SP, _i32, _i32], _i32),
+    "fier_decode_step_ex": ([_SP, _vp, _vp, _vp, _i32, _vp, _vp, _vp, _vp, _i32, C.c_float, C.POINTER(FierRope),
+                             _vp, _vp, _vp, _vp, _sz, _vp], C.c_int),
     "fier_decode_step": ([_SP, _vp, _vp, _vp, _i32, _vp, _vp, _vp, _vp, _i32, C.c_float, _vp, _vp,
                           _vp, _vp, _sz, _vp], C.c_int),
     "fier_sparse_attention_ragged": ([_SP, _vp, _vp, _vp, _vp, _vp, _i32, _i32, C.c_float, _vp, _vp, _vp,

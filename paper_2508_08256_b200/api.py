@@ -28,7 +28,7 @@ from __future__ import annotations
 import ctypes as C
 import math
 from dataclasses import dataclass
-from typing import Optional
+from typing import Optional, Tuple
 
 import numpy as np
 import torch
@@ -341,8 +341,11 @@ class DecodeLayer:
         return self._ws
 
     def step(self, q, k_new, v_new, pos: int, n: int, out=None, sel=None, scores_out=None,
-             scale: Optional[float] = None):
-        """fier_attend for a decode step: append token `pos`, score, select n, attend."""
+             scale: Optional[float] = None, rope: Optional[Tuple[float, int, bool]] = None):
+        """fier_attend for a decode step: append token `pos`, score, select n, attend.
+
+        rope = (base, rotary_dim, interleaved): rotate q and k_new by position `pos`
+        inside the step (fier_decode_step_ex; the cache stores the rotated k row)."""
         lib = _lib.load()
         tokens = pos + 1
         ws = self.workspace(tokens, n) if self._ws_key != (tokens, n) else self._ws
@@ -351,9 +354,13 @@ class DecodeLayer:
         if sel is None:
             sel = torch.empty((self.B, self.Hq, n), dtype=torch.int32, device=self.device)
         scale = 1.0 / math.sqrt(self.d) if scale is None else scale
-        check(lib.fier_decode_step(C.byref(self.shape), _p(q), _p(k_new), _p(v_new), pos, _p(self.K),
-                                   _p(self.V), _p(self.pk.bits), _p(self.pk.params), n, scale, _p(out),
-                                   _p(sel), _p(scores_out), _p(ws), ws.numel(), _stream()))
+        rp = None
+        if rope is not None:
+            base, rd, inter = rope
+            rp = C.byref(_lib.FierRope(float(base), int(rd), 1 if inter else 0))
+        check(lib.fier_decode_step_ex(C.byref(self.shape), _p(q), _p(k_new), _p(v_new), pos, _p(self.K),
+                                      _p(self.V), _p(self.pk.bits), _p(self.pk.params), n, scale, rp, _p(out),
+                                      _p(sel), _p(scores_out), _p(ws), ws.numel(), _stream()))
         self.pk.tokens = max(self.pk.tokens, tokens)
         self.tokens = max(self.tokens, tokens)
         return out, sel

@@ -55,6 +55,22 @@ __device__ __forceinline__ void tc_load_q(const T* qbase, uint32_t (&qb)[D / 16]
     }
 }
 
+// The same from an fp32 copy of the query heads in shared memory (e.g. after RoPE),
+// rounded to T the way a T query would be stored.
+template <typename T, int D, int HPG>
+__device__ __forceinline__ void tc_load_q_f32(const float* qf, uint32_t (&qb)[D / 16][2]) {
+    const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+#pragma unroll
+    for (int ks = 0; ks < D / 16; ++ks) {
+        qb[ks][0] = qb[ks][1] = 0u;
+        if (g < HPG) {
+            const float* qp = qf + g * D + ks * 16 + 2 * t;
+            qb[ks][0] = pack2<T>(qp[0], qp[1]);
+            qb[ks][1] = pack2<T>(qp[8], qp[9]);
+        }
+    }
+}
+
 // Per-warp attention state: o[mt] = O^T fragment of channels 16mt..16mt+15
 // ({c g, h 2t}, {c g, h 2t+1}, {c g+8, h 2t}, {c g+8, h 2t+1}); m[e] / l[e] =
 // running max (log2 domain) / partial sum of head 2t+e over this lane's tokens.

@@ -1,6 +1,7 @@
 // capi.cu -- the C ABI (include/fier_cuda.h): argument validation with the
 // reference's error texts, workspace sizing, the fused decode step, and the
 // host-side FIER format conversion.
+#include <cmath>
 #include <cstring>
 #include <string>
 
@@ -41,7 +42,8 @@ size_t sparse_counter_offset(const fier_shape*, int);
 int append_score_dispatch(const fier_shape*, const void*, void*, void*, const void*, const void*, int,
                           uint32_t*, void*, float*, int64_t, int*, int, cudaStream_t);
 int fused_step_dispatch(const fier_shape*, const void*, const void*, const void*, int, void*, void*, uint32_t*,
-                        void*, int, float, float*, int32_t*, float*, int64_t, cudaStream_t);
+                        void*, int, float, const fier_rope*, float*, int32_t*, float*, int64_t, cudaStream_t);
+int rope_dispatch(const fier_shape*, const void*, const void*, int, const fier_rope*, void*, void*, cudaStream_t);
 bool fused_step_applies(const fier_shape*, int tokens);
 bool attn_fused_merge(const fier_shape*);
 
@@ -186,16 +188,30 @@ int fier_full_attention(const fier_shape* s, const void* q, const void* K, const
 
 int64_t fier_step_scores_ld(int32_t tokens) { return ceil_div(tokens, 32) * 32; }
 
+// workspace: [scores][attention partials + counters][top-k][rotated q, k_new (RoPE, separate kernels)]
+static size_t rope_bytes(const fier_shape* s) {
+    return align_up((size_t)s->batch * (s->q_heads + s->kv_heads) * s->dim * elem_size(s->dtype));
+}
+
 size_t fier_decode_workspace(const fier_shape* s, int32_t tokens, int32_t n) {
     if (check_shape(s, "fier_decode_step") || tokens < 1 || n < 1) return 0;
     const size_t scores = (size_t)s->batch * s->q_heads * fier_step_scores_ld(tokens) * sizeof(float);
-    return align_up(scores) + align_up(sparse_workspace(s, n)) + align_up(topk_workspace(s->batch * s->q_heads, tokens, n));
+    return align_up(scores) + align_up(sparse_workspace(s, n)) +
+           align_up(topk_workspace(s->batch * s->q_heads, tokens, n)) + rope_bytes(s);
 }
 
 int fier_decode_step(const fier_shape* s, const void* q, const void* k_new, const void* v_new,
                      int32_t pos, void* K, void* V, uint32_t* bits, void* params, int32_t n,
                      float scale, float* out, int32_t* sel, float* scores_out, void* workspace,
                      size_t workspace_bytes, void* stream) {
+    return fier_decode_step_ex(s, q, k_new, v_new, pos, K, V, bits, params, n, scale, nullptr, out, sel, scores_out,
+                               workspace, workspace_bytes, stream);
+}
+
+int fier_decode_step_ex(const fier_shape* s, const void* q, const void* k_new, const void* v_new,
+                        int32_t pos, void* K, void* V, uint32_t* bits, void* params, int32_t n,
+                        float scale, const fier_rope* rope, float* out, int32_t* sel, float* scores_out,
+                        void* workspace, size_t workspace_bytes, void* stream) {
     if (int rc = check_shape(s, "fier_decode_step")) return rc;
     const int32_t tokens = pos + 1;
     FIER_REQUIRE(pos >= 0 && pos < s->capacity, "fier_append: position outside cache capacity");
@@ -203,16 +219,31 @@ int fier_decode_step(const fier_shape* s, const void* q, const void* k_new, cons
     FIER_REQUIRE(q && k_new && v_new && K && V && bits && params && out && sel, "fier_decode_step: null buffer");
     FIER_REQUIRE(workspace && workspace_bytes >= fier_decode_workspace(s, tokens, n),
                  "fier_decode_step: workspace too small");
+    if (rope) {
+        FIER_REQUIRE(rope->rotary_dim >= 2 && rope->rotary_dim % 2 == 0 && rope->rotary_dim <= s->dim &&
+                         rope->rotary_dim <= 128,
+                     "fier_decode_step: rotary_dim must be even, >= 2 and <= min(dim, 128)");
+        FIER_REQUIRE(rope->base > 0.f && std::isfinite(rope->base), "fier_decode_step: rope base must be > 0");
+    }
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     const int64_t ld = fier_step_scores_ld(tokens);
-    // MHA, d = 128: the whole step in one cluster launch (step_fused.cu)
-    const int frc = fused_step_dispatch(s, q, k_new, v_new, pos, K, V, bits, params, n, scale, out, sel,
+    // MHA, d = 128: the whole step (RoPE included) in one cluster launch (step_fused.cu)
+    const int frc = fused_step_dispatch(s, q, k_new, v_new, pos, K, V, bits, params, n, scale, rope, out, sel,
                                         scores_out, ld, st);
     if (frc >= 0) return frc;
     uint8_t* ws = static_cast<uint8_t*>(workspace);
     float* scores = scores_out ? scores_out : reinterpret_cast<float*>(ws);
     uint8_t* attn_ws = ws + align_up((size_t)s->batch * s->q_heads * ld * sizeof(float));
     int* counters = reinterpret_cast<int*>(attn_ws + sparse_counter_offset(s, n));
+    if (rope) {  // rotated copies of q and k_new for the separate kernels
+        uint8_t* rws = attn_ws + align_up(sparse_workspace(s, n)) +
+                       align_up(topk_workspace(s->batch * s->q_heads, tokens, n));
+        void* q_rot = rws;
+        void* k_rot = rws + (size_t)s->batch * s->q_heads * s->dim * elem_size(s->dtype);
+        if (int rc = rope_dispatch(s, q, k_new, pos, rope, q_rot, k_rot, st)) return rc;
+        q = q_rot;
+        k_new = k_rot;
+    }
     int rc = append_score_dispatch(s, q, K, V, k_new, v_new, pos, bits, params, scores, ld, counters,
                                    s->batch * s->q_heads, st);
     if (rc) return rc;
@@ -224,7 +255,8 @@ int fier_decode_step(const fier_shape* s, const void* q, const void* k_new, cons
 int32_t fier_decode_step_launches(const fier_shape* s, int32_t tokens, int32_t n) {
     if (check_shape(s, "fier_decode_step") || tokens < 1 || n < 1 || n > tokens) return 0;
     if (fused_step_applies(s, tokens)) return 1;
-    // append+score, Top-k, sparse attention (+ a separate LSE merge on the generic attention path)
+    // append+score, Top-k, sparse attention (+ a separate LSE merge on the generic attention path;
+    // + the RoPE kernel when fier_decode_step_ex gets a rope)
     return attn_fused_merge(s) ? 3 : 4;
 }
 

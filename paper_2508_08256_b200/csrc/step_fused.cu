@@ -68,6 +68,7 @@ __device__ unsigned long long g_fs_trace[kFsTraceCtas][16];
 #include "attn_tc.cuh"
 #include "nibble.cuh"
 #include "pack.cuh"
+#include "rope.cuh"
 #include "select_radix.cuh"
 
 namespace fier_cuda {
@@ -89,7 +90,8 @@ constexpr int kFsSidx = kFsRing;                                             // 
 constexpr int kFsPub = kFsSidx + kFsThreads * kFsMaxKpt * 2;                 // RxPublished (read by peers)
 constexpr int kFsWres = kFsPub + ((int)sizeof(RxPublished) + 15) / 16 * 16;  // warp partials
 constexpr int kFsCres = kFsWres + kFsGatherWarps * (kFsD + 2) * 4;           // CTA partials (rank 0)
-constexpr int kFsSmem = kFsCres + kT2MaxCluster * (kFsD + 2) * 4 + 256;      // + base alignment
+constexpr int kFsQrot = kFsCres + kT2MaxCluster * (kFsD + 2) * 4;           // fp32 (rotated) query
+constexpr int kFsSmem = kFsQrot + kFsD * 4 + 256;                            // + base alignment
 static_assert(kFsRx + (int)sizeof(RxShared) <= kFsRing, "LUTs, keys and RxShared must fit in the ring area");
 static_assert(sizeof(T2Shared) <= sizeof(RxShared), "");
 static_assert(kFsSmem <= 227 * 1024, "fused step exceeds shared memory");
@@ -109,6 +111,7 @@ struct FsArgs {
     int64_t ld;
     int pos, tokens, cap, G, hq, g, g_shift, k, kpt;  // g_shift = log2(g) or -1
     float scale_log2;
+    RopeTable rope;  // rd = 0: no rotary embedding
 };
 
 // The degenerate-row path, out of line: its code would otherwise sit between the hot
@@ -154,6 +157,12 @@ __global__ void __launch_bounds__(kFsThreads, 1) step_fused_kernel(const FsArgs 
     uint32_t* keys_s = reinterpret_cast<uint32_t*>(smem + kFsKeys);
 
     rx_clear<kFsThreads>(S);  // the scorer counts every key into the digit-1 histogram
+    float* qrot = reinterpret_cast<float*>(smem + kFsQrot);  // this head's query, rotated (RoPE)
+    if (tid < kFsD) {
+        const T* qh = static_cast<const T*>(a.q) + (int64_t)row * kFsD;
+        // rotated in fp32, rounded to the cache dtype like the rotated k row (rope.cuh)
+        qrot[tid] = to_f32(T(rope_channel(a.rope, tid, [&](int j) { return to_f32(qh[j]); })));
+    }
     __syncthreads();
     FS_MARK(0);
 
@@ -167,7 +176,8 @@ __global__ void __launch_bounds__(kFsThreads, 1) step_fused_kernel(const FsArgs 
     const bool appender = a.pos / slice == rank;  // CTA-uniform
     const int open_lo = appender ? (a.pos / a.g) * a.g : INT_MAX;  // first token of the open group
     if (appender && tid < D) {
-        Kseq[(int64_t)a.pos * D + tid] = static_cast<const T*>(a.k_new)[seq * D + tid];
+        const T* kn = static_cast<const T*>(a.k_new) + seq * D;
+        Kseq[(int64_t)a.pos * D + tid] = T(rope_channel(a.rope, tid, [&](int j) { return to_f32(kn[j]); }));
         Vseq[(int64_t)a.pos * D + tid] = static_cast<const T*>(a.v_new)[seq * D + tid];
         pack_open_group<T>(Kseq, D, a.g, a.pos / a.g, a.pos + 1, bseq, zseq);
     }
@@ -175,11 +185,8 @@ __global__ void __launch_bounds__(kFsThreads, 1) step_fused_kernel(const FsArgs 
     FS_MARK(1);
     // ---- phase B: score this CTA's slice into shared-memory keys ----
     float qv[4];
-    {
-        const T* qp = static_cast<const T*>(a.q) + seq * D + 4 * lane;
 #pragma unroll
-        for (int i = 0; i < 4; ++i) qv[i] = to_f32(qp[i]);
-    }
+    for (int i = 0; i < 4; ++i) qv[i] = qrot[4 * lane + i];
     const uint32_t tab0 = base + kFsLut + warp * 2 * kFsLutBytes;
     float* srow = a.scores ? a.scores + (int64_t)row * a.ld : nullptr;
     // Scoring is assigned per slab (32 tokens), independently of which warp owns the
@@ -277,7 +284,7 @@ __global__ void __launch_bounds__(kFsThreads, 1) step_fused_kernel(const FsArgs 
     // ---- phase D: attention over this CTA's selected rows ----
     if (warp < kFsGatherWarps) {
         uint32_t qb[D / 16][2];
-        tc_load_q<T, D, 1>(static_cast<const T*>(a.q) + seq * D, qb);
+        tc_load_q_f32<T, D, 1>(qrot, qb);
         TcState<D> st;
         st.init();
         const int cnt = (int)ccount;
@@ -391,8 +398,8 @@ bool fused_step_applies(const fier_shape* s, int tokens) {
 
 // Returns -1 when the shape is not covered (the caller runs the separate kernels).
 int fused_step_dispatch(const fier_shape* s, const void* q, const void* k_new, const void* v_new, int pos, void* K,
-                        void* V, uint32_t* bits, void* params, int n, float scale, float* out, int32_t* sel,
-                        float* scores_out, int64_t ld, cudaStream_t st) {
+                        void* V, uint32_t* bits, void* params, int n, float scale, const fier_rope* rope,
+                        float* out, int32_t* sel, float* scores_out, int64_t ld, cudaStream_t st) {
     if (fused_disabled() || !fused_shape_ok(s)) return -1;
     const int tokens = pos + 1, rows = s->batch * s->q_heads;
     if (rows > 65535) return -1;
@@ -420,6 +427,7 @@ int fused_step_dispatch(const fier_shape* s, const void* q, const void* k_new, c
     args.k = n;
     args.kpt = kpt;
     args.scale_log2 = scale * kLog2e;
+    args.rope = rope_table(rope, pos);
     if (s->dtype == FIER_BF16) return launch_fused<__nv_bfloat16>(cluster, rows, args, st);
     return launch_fused<__half>(cluster, rows, args, st);
 }

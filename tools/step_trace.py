@@ -65,6 +65,12 @@ def main():
         buf[:] = 0
         t0 = t[:, 0].min()
         rows.append(t - t0)
+    nct = rows[0].shape[0] // (B * Hq)  # CTAs per cluster (grid = cluster x rows)
+    if nct > 1:
+        by_rank = np.stack([r[:B * Hq * nct, 2].reshape(B * Hq, nct) for r in rows])  # score end
+        print("score end by cluster rank (median / max, us):",
+              [(round(float(np.median(by_rank[..., c])) / 1e3, 2), round(float(by_rank[..., c].max()) / 1e3, 2))
+               for c in range(nct)])
     t = np.concatenate(rows)
     print(f"{a.config}: {len(rows)} steps, {t.shape[0] // len(rows)} CTAs per step (us since first CTA start)")
     for i, nm in enumerate(NAMES):
