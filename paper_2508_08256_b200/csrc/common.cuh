@@ -136,6 +136,11 @@ __device__ __forceinline__ uint4 ldg_stream(const void* p) {
     return v;
 }
 
+__device__ __forceinline__ float4 ldg_stream_f4(const float* p) {
+    const uint4 u = ldg_stream(p);
+    return make_float4(__uint_as_float(u.x), __uint_as_float(u.y), __uint_as_float(u.z), __uint_as_float(u.w));
+}
+
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);

@@ -71,8 +71,8 @@ __device__ __forceinline__ void rx_clear(RxShared& S) {
 
 // Refine list `src` (n entries) to the entries of the bin holding the krem-th
 // largest of digit(value) (BINS bins); returns the survivors' count (in `dst`).
-template <int NT, int BINS, typename Digit>
-__device__ __forceinline__ uint32_t rx_refine(RxShared& S, const uint32_t* sk, const int32_t* si, uint32_t n,
+template <int NT, int BINS, typename Digit, typename SH>
+__device__ __forceinline__ uint32_t rx_refine(SH& S, const uint32_t* sk, const int32_t* si, uint32_t n,
                                               uint32_t* dk, int32_t* di, uint32_t& krem, Digit&& digit) {
     const int tid = threadIdx.x, lane = tid & 31;
     for (int i = tid; i < BINS; i += NT) S.tot[i] = 0u;
@@ -104,7 +104,8 @@ __device__ __forceinline__ uint32_t rx_refine(RxShared& S, const uint32_t* sk, c
 }
 
 // Exact rank of <= 32 (key, index) pairs by (key desc, index asc): the krem-th -> (T, idx_T).
-__device__ __forceinline__ void rx_rank32(RxShared& S, const uint32_t* mk, const int32_t* mi, uint32_t n,
+template <typename SH>
+__device__ __forceinline__ void rx_rank32(SH& S, const uint32_t* mk, const int32_t* mi, uint32_t n,
                                           uint32_t krem) {
     const int lane = threadIdx.x & 31;
     if ((threadIdx.x >> 5) == 0) {

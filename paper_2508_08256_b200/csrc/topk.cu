@@ -610,6 +610,7 @@ static int launch_cluster(Kern kern, int cluster, int rows, int threads, size_t 
 int topk2_dispatch(const float*, int, int, int64_t, int, int32_t*, cudaStream_t);
 
 int topk_rx_dispatch(const float* scores, int rows, int tokens, int64_t ld, int k, int32_t* sel, cudaStream_t st);
+int topk_long_dispatch(const float* scores, int rows, int tokens, int64_t ld, int k, int32_t* sel, cudaStream_t st);
 
 int topk_dispatch(const float* scores, int rows, int tokens, int64_t ld, int k, int32_t* sel,
                   cudaStream_t st) {
@@ -634,6 +635,10 @@ int topk_dispatch(const float* scores, int rows, int tokens, int64_t ld, int k, 
         if (slice <= 512 * 16) return launch_cluster(topk_kernel<16, 512>, c, rows, 512, smem, st, scores, tokens, ld, k, 8192, sel);
         if (slice <= 256 * 32) return launch_cluster(topk_kernel<32, 256>, c, rows, 256, smem, st, scores, tokens, ld, k, 8192, sel);
         return launch_cluster(topk_kernel<64, 256>, c, rows, 256, smem, st, scores, tokens, ld, k, kMaxSlice, sel);
+    }
+    {  // rows too long for the on-chip paths (C5): three streaming passes, radix threshold
+        const int rc = topk_long_dispatch(scores, rows, tokens, ld, k, sel, st);
+        if (rc >= 0) return rc;
     }
     const int sl = (int)(ceil_div(slice, 32) * 32);
     return launch_cluster(topk_stream_kernel, c, rows, 1024, 0, st, scores, tokens, ld, k, sl, sel);

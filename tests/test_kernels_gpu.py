@@ -384,3 +384,18 @@ def test_topk_rx_path_matches(cuda):
     r = subprocess.run([sys.executable, "-c", _RX.format(root=root)], env=dict(os.environ, FIER_TOPK="rx"),
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and "rx ok" in r.stdout, r.stdout + r.stderr
+
+
+@pytest.mark.parametrize("l,k", [(1048576, 4096), (600001, 66000)])
+def test_topk_long_rows(cuda, port, l, k):
+    """K3 for rows beyond the on-chip paths (topk_long.cu, C5's 1M tokens): random scores,
+    heavy ties, and a constant row (candidate overflow -> the streaming radix fallback)."""
+    F = fier()
+    g = torch.Generator(device="cpu").manual_seed(l + k)
+    s = torch.randn(3, l, generator=g) * 8
+    s[1] = torch.round(s[1] * 2) / 2                      # ties at the threshold
+    s[2] = 0.75
+    s[2, ::1000] = 1.5
+    sel = F.topk_oracle(s.to(cuda), k).cpu().numpy()
+    for r in range(3):
+        np.testing.assert_array_equal(sel[r], port.topk(s[r].double().numpy(), k))

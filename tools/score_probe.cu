@@ -8,6 +8,7 @@
 //   3  loads + lookups, table built once per warp (no rebuild) -> build cost
 //   4  lookups only (register data, table built once)            -> LDS path
 //   5  as 4 with the LDS replaced by an ALU op                    -> issue path
+//   6  full scorer + the digit-1 histogram (smem atomics, one per key, as in the fused step)
 // L2 is flushed (512 MB read) before every timed launch.
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -Ipaper_2508_08256_b200/csrc -Iinclude \
 //        -o tools/score_probe tools/score_probe.cu
@@ -16,6 +17,7 @@
 #include <algorithm>
 
 #include "nibble.cuh"
+#include "common.cuh"
 
 using namespace fier_cuda;
 
@@ -33,6 +35,11 @@ __global__ void __launch_bounds__(NT, 1) probe(const uint32_t* bits, const __hal
     const uint32_t base = (uint32_t)__cvta_generic_to_shared(sm);
     const uint32_t tab0 = base + warp * 2 * kNibTableBytes;
     uint32_t* run = reinterpret_cast<uint32_t*>(sm + 16 * 2 * kNibTableBytes) + wbase;
+    uint32_t* hist = reinterpret_cast<uint32_t*>(sm + 16 * 2 * kNibTableBytes + NT * KPT * 4);
+    if (MODE == 6) {
+        for (int i = threadIdx.x; i < 4096; i += NT) hist[i] = 0;
+        __syncthreads();
+    }
     const uint32_t* bseq = bits + (size_t)head * L * 4;
     const __half2* zseq = sz + (size_t)head * G * D;
     float qv[4];
@@ -90,12 +97,14 @@ __global__ void __launch_bounds__(NT, 1) probe(const uint32_t* bits, const __hal
                     sc = nibble_score(tab, b2);
                 }
                 run[32 * j + lane] = __float_as_uint(sc);
+                if (MODE == 6) atomicAdd(hist + (float_key(sc) >> 20), 1u);
             }
         }
     }
     __syncthreads();
     if (MODE != 0)
         for (int j = 0; j < KPT; ++j) x ^= run[32 * j + lane];
+    if (MODE == 6) x ^= hist[threadIdx.x];
     if (x == 0x12345678u) out[0] = 1.f;
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -115,7 +124,7 @@ __global__ void flush(const uint4* p, size_t n, float* out) {
 
 template <int MODE, int PF>
 float run(const uint32_t* bits, const __half2* sz, const float* q, float* out, const uint4* fl, size_t fn) {
-    const int smem = 16 * 2 * kNibTableBytes + NT * KPT * 4;
+    const int smem = 16 * 2 * kNibTableBytes + NT * KPT * 4 + 4096 * 4;
     cudaFuncSetAttribute(probe<MODE, PF>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     cudaEvent_t a, b;
     cudaEventCreate(&a);
@@ -175,6 +184,7 @@ int main() {
     rep("mode3 loads+lookups (no rebuild)", run<3, 4>(bits, sz, q, out, fl, fn));
     rep("mode4 lookups only", run<4, 4>(bits, sz, q, out, fl, fn));
     rep("mode5 lookups as ALU", run<5, 4>(bits, sz, q, out, fl, fn));
+    rep("mode6 full + digit histogram", run<6, 4>(bits, sz, q, out, fl, fn));
     cudaError_t e = cudaGetLastError();
     printf("status: %s\n", cudaGetErrorString(e));
     return 0;
