@@ -26,7 +26,14 @@ namespace fier_cuda {
 constexpr int kTcRows = 16;  // rows per stage
 
 __device__ __forceinline__ void cp_async16_tc(uint32_t smem, const void* gmem) {
+#ifndef FIER_NO_EVICT_FIRST
+    uint64_t pol;
+    asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(smem), "l"(gmem), "l"(pol)
+                 : "memory");
+#else
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem), "l"(gmem) : "memory");
+#endif
 }
 
 // byte offset of 16-byte chunk c of row r inside a stage buffer (rows of RB bytes)
@@ -86,27 +93,29 @@ struct TcState {
     }
 };
 
-// Stream rows [wr0, wr1) (GATHER: tok_of(r) = token of row r; else row r = token r)
-// through the ring at shared address `ring` (NST * 2 * tc_stage_bytes<D>() bytes).
+// Stream granules sg = 0, 1, ... of up to kTcRows rows through the ring at shared
+// address `ring` (NST * 2 * tc_stage_bytes<D>() bytes): gran(sg, r0) returns the row
+// count of granule sg and its first row r0 (<= 0: the stream has ended; monotone; called
+// in order, the loads one stage ahead of the math, so it may wait for rows to appear).
+// GATHER: tok_of(r) = token of row r; else row r = token r.
 // On return st.l holds the full per-head sums (reduced over the lane's column group).
-template <typename T, int D, bool GATHER, int NST, typename TokOf>
-__device__ __forceinline__ void tc_stream_rows(const uint32_t (&qb)[D / 16][2], const T* Kseq, const T* Vseq,
-                                               int wr0, int wr1, uint32_t ring, float scale_log2, TokOf&& tok_of,
-                                               TcState<D>& st) {
+template <typename T, int D, bool GATHER, int NST, typename Gran, typename TokOf>
+__device__ __forceinline__ void tc_stream_granules(const uint32_t (&qb)[D / 16][2], const T* Kseq, const T* Vseq,
+                                                   uint32_t ring, float scale_log2, Gran&& gran, TokOf&& tok_of,
+                                                   TcState<D>& st) {
     constexpr int RB = D * 2;              // bytes per row
     constexpr int CPR = RB / 16;           // 16-byte chunks per row
     constexpr int KSTEPS = D / 16;         // mma k-steps over channels (S) = m-tiles over channels (PV)
     constexpr int STAGE = tc_stage_bytes<D>();
     constexpr int CPL = kTcRows * CPR / 32;  // chunks per lane per K (or V) stage
     const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
-    const int nstages = (wr1 - wr0 + kTcRows - 1) / kTcRows;
 
     auto issue = [&](int sg) {
-        if (sg < nstages) {
+        int r0 = 0;
+        const int nr = gran(sg, r0);
+        if (nr > 0) {
             const uint32_t kdst = ring + (uint32_t)(sg % NST) * 2 * STAGE;
             const uint32_t vdst = kdst + STAGE;
-            const int r0 = wr0 + sg * kTcRows;
-            const int nr = min(kTcRows, wr1 - r0);
             int tok = 0;
             if constexpr (GATHER) {
                 if (lane < nr) tok = tok_of(r0 + lane);
@@ -144,13 +153,15 @@ __device__ __forceinline__ void tc_stream_rows(const uint32_t (&qb)[D / 16][2], 
     const int src0 = 8 * t + (g >> 1), src1 = src0 + 4;
     const bool odd = g & 1;
 
-    for (int sg = 0; sg < nstages; ++sg) {
+    for (int sg = 0;; ++sg) {
+        int r0 = 0;
+        const int nr = gran(sg, r0);
+        if (nr <= 0) break;
         issue(sg + NST - 1);
         asm volatile("cp.async.wait_group %0;" ::"n"(NST - 1) : "memory");
         __syncwarp();
         const uint32_t kst = ring + (uint32_t)(sg % NST) * 2 * STAGE;
         const uint32_t vst = kst + STAGE;
-        const int nr = min(kTcRows, wr1 - (wr0 + sg * kTcRows));
 
         // ---- S^T = K q^T: 16 tokens x 8 heads ----
         float s[4] = {0.f, 0.f, 0.f, 0.f};
@@ -216,6 +227,20 @@ __device__ __forceinline__ void tc_stream_rows(const uint32_t (&qb)[D / 16][2], 
         st.l[e] += __shfl_xor_sync(0xffffffffu, st.l[e], 8);
         st.l[e] += __shfl_xor_sync(0xffffffffu, st.l[e], 16);
     }
+}
+
+// Rows [wr0, wr1) in granules of kTcRows.
+template <typename T, int D, bool GATHER, int NST, typename TokOf>
+__device__ __forceinline__ void tc_stream_rows(const uint32_t (&qb)[D / 16][2], const T* Kseq, const T* Vseq,
+                                               int wr0, int wr1, uint32_t ring, float scale_log2, TokOf&& tok_of,
+                                               TcState<D>& st) {
+    tc_stream_granules<T, D, GATHER, NST>(
+        qb, Kseq, Vseq, ring, scale_log2,
+        [wr0, wr1](int sg, int& r0) {
+            r0 = wr0 + sg * kTcRows;
+            return min(kTcRows, wr1 - r0);
+        },
+        tok_of, st);
 }
 
 // Warp state -> wr[h][D + 2] (o[0..D), m, l) for heads h < HPG.

@@ -12,11 +12,25 @@ namespace fier_cuda {
 
 constexpr int kNibTableBytes = 32 * 16 * 4;  // one table: 32 nibble positions x 16 fp32 entries
 
+#ifndef FIER_NO_EVICT_FIRST
+__device__ __forceinline__ uint64_t l2_evict_first_policy() {
+    uint64_t pol;
+    asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+#endif
+
 __device__ __forceinline__ uint4 ld_cg16(const void* p) {
     uint4 v;
+#ifndef FIER_NO_EVICT_FIRST
+    asm volatile("ld.global.cg.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "l"(p), "l"(l2_evict_first_policy()));
+#else
     asm volatile("ld.global.cg.v4.u32 {%0,%1,%2,%3}, [%4];"
                  : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
                  : "l"(p));
+#endif
     return v;
 }
 

@@ -131,9 +131,18 @@ __device__ __forceinline__ void t2_for_keys(const Keys& keys, F&& f) {
     }
 }
 
+// Barriers of a thread group: the whole CTA, or the first N threads (named barrier ID).
+struct CtaBar {
+    __device__ static __forceinline__ void sync() { __syncthreads(); }
+};
+template <int ID, int N>
+struct NamedBar {
+    __device__ static __forceinline__ void sync() { asm volatile("bar.sync %0, %1;" ::"n"(ID), "n"(N) : "memory"); }
+};
+
 // Over bins held in cnt[0..kT2Bins) (smem), find b with above(b) < krem <= above(b) + cnt[b],
 // above(b) = sum of bins > b.  Writes (b, above) to res[0..1] (res[0] = ~0u if none).
-template <int NT, int BINS = kT2Bins, typename SH = T2Shared>
+template <int NT, int BINS = kT2Bins, typename SH = T2Shared, typename Bar = CtaBar>
 __device__ __forceinline__ void t2_find_bin(const uint32_t* cnt, uint32_t krem, SH& S) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     constexpr int BPT = BINS >= NT ? BINS / NT : 1;  // bins per thread
@@ -152,7 +161,7 @@ __device__ __forceinline__ void t2_find_bin(const uint32_t* cnt, uint32_t krem, 
         if (lane + o < 32) s += y;
     }
     if (lane == 0) S.wsum[warp] = s;
-    __syncthreads();
+    Bar::sync();
     if (warp == 0) {  // exclusive suffix scan of the warp totals
         const uint32_t v = lane < NT / 32 ? S.wsum[lane] : 0u;
         uint32_t t = v;
@@ -163,7 +172,7 @@ __device__ __forceinline__ void t2_find_bin(const uint32_t* cnt, uint32_t krem, 
         }
         if (lane < NT / 32) S.wsuf[lane] = t - v;
     }
-    __syncthreads();
+    Bar::sync();
     uint32_t a = S.wsuf[warp] + s - c;  // count above this thread's highest bin
 #pragma unroll
     for (int i = BPT - 1; i >= 0; --i) {
@@ -173,7 +182,7 @@ __device__ __forceinline__ void t2_find_bin(const uint32_t* cnt, uint32_t krem, 
         }
         a += cb[i];
     }
-    __syncthreads();
+    Bar::sync();
 }
 
 // tot[i] = sum over the cluster's CTAs of hist[i]: 16-byte DSMEM loads

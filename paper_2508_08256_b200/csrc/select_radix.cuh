@@ -43,10 +43,10 @@ struct RxPublished {
     int32_t cidx[kRxCtaCand];
 };
 
+// hist and coarse come last: they are dead after the second cluster barrier, so the
+// fused step overlays its attention rings on them (step_fused.cu).
 struct RxShared {
-    alignas(16) uint32_t hist[kRxBins + 4];  // digit-1 histogram (scoring; read remotely); [kRxBins] = trash
     alignas(16) uint32_t tot[kT2Bins];       // refinement histograms (8-bit digits); fallback merges
-    alignas(16) uint32_t coarse[64];         // sums of 64 consecutive digit-1 bins (read remotely)
     uint32_t mkey[3][kRxCand];  // [0] all candidates of the row (kept), [1], [2] refinement
     int32_t midx[3][kRxCand];
     uint32_t cn[kT2MaxCluster], ca[kT2MaxCluster];     // every CTA's published pair
@@ -56,6 +56,9 @@ struct RxShared {
     uint32_t wg[kT2Warps], we[kT2Warps];               // (fallback compaction)
     uint32_t cgt[kT2MaxCluster], ceq[kT2MaxCluster];
     uint32_t res[8];
+    uint32_t over, nabove, nkept;  // split variant: overflow flag, gather-list lengths
+    alignas(256) uint32_t hist[kRxBins + 4];  // digit-1 histogram (scoring; read remotely); [kRxBins] = trash
+    alignas(16) uint32_t coarse[64];          // sums of 64 consecutive digit-1 bins (read remotely)
 };
 
 // The scorer's contribution: count key kj (0 = empty -> trash bin).
@@ -71,19 +74,19 @@ __device__ __forceinline__ void rx_clear(RxShared& S) {
 
 // Refine list `src` (n entries) to the entries of the bin holding the krem-th
 // largest of digit(value) (BINS bins); returns the survivors' count (in `dst`).
-template <int NT, int BINS, typename Digit, typename SH>
+template <int NT, int BINS, typename Bar = CtaBar, typename Digit, typename SH>
 __device__ __forceinline__ uint32_t rx_refine(SH& S, const uint32_t* sk, const int32_t* si, uint32_t n,
                                               uint32_t* dk, int32_t* di, uint32_t& krem, Digit&& digit) {
     const int tid = threadIdx.x, lane = tid & 31;
     for (int i = tid; i < BINS; i += NT) S.tot[i] = 0u;
-    __syncthreads();
+    Bar::sync();
     for (uint32_t i = tid; i < n; i += NT) atomicAdd(&S.tot[digit(sk[i], si[i])], 1u);
-    __syncthreads();
-    t2_find_bin<NT, BINS>(S.tot, krem, S);
+    Bar::sync();
+    t2_find_bin<NT, BINS, SH, Bar>(S.tot, krem, S);
     const uint32_t b = S.res[0];
     krem -= S.res[1];
     if (tid == 0) S.res[2] = 0;
-    __syncthreads();
+    Bar::sync();
     for (uint32_t i0 = 0; i0 < n; i0 += NT) {
         const uint32_t i = i0 + tid;
         const bool c = i < n && digit(sk[i], si[i]) == b;
@@ -99,12 +102,12 @@ __device__ __forceinline__ uint32_t rx_refine(SH& S, const uint32_t* sk, const i
             }
         }
     }
-    __syncthreads();
+    Bar::sync();
     return S.res[2];
 }
 
 // Exact rank of <= 32 (key, index) pairs by (key desc, index asc): the krem-th -> (T, idx_T).
-template <typename SH>
+template <typename Bar = CtaBar, typename SH>
 __device__ __forceinline__ void rx_rank32(SH& S, const uint32_t* mk, const int32_t* mi, uint32_t n,
                                           uint32_t krem) {
     const int lane = threadIdx.x & 31;
@@ -128,7 +131,7 @@ __device__ __forceinline__ void rx_rank32(SH& S, const uint32_t* mk, const int32
             __shfl_sync(0xffffffffu, ii, src);
         }
     }
-    __syncthreads();
+    Bar::sync();
 }
 
 // One warp, 64 bins held 2 per lane (bin 2l -> c0, 2l+1 -> c1): the bin b with
@@ -387,6 +390,291 @@ __device__ __forceinline__ void rx_emit(const Keys& keys, const RxResult& R, int
         const uint32_t m = __ballot_sync(0xffffffffu, kb);
         if (kb) emit(run + __popc(m & lt), j);
         run += __popc(m);
+    }
+}
+
+// ---- split variant (the fused decode step) -----------------------------------------
+// After the second cluster barrier the CTA splits in two: the gather warps start the
+// attention over the keys above b1 -- certainly kept, since fewer than k keys of the
+// row lie above bin b1 -- while the select warps resolve the candidates (digit 1 ==
+// b1), append this CTA's kept candidates to the gather list and write the selection
+// from per-(warp, slot) lane masks.  Candidate overflow is decided before the split,
+// from the merged and the per-CTA counts of bin b1 (cluster-uniform), and then the
+// exact MSD path of select.cuh runs instead, with every warp.
+
+struct RxFind {
+    uint32_t b1, krem;
+    bool over;
+};
+
+// Sum and per-element max over the cluster's CTAs of two consecutive u32 words.
+__device__ __forceinline__ uint2 rx_cluster_sum2_max(uint32_t a, int nct, uint2* mx) {
+    uint2 t = make_uint2(0u, 0u), m = make_uint2(0u, 0u);
+    for (int r0 = 0; r0 < nct; r0 += 4) {
+        uint2 v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            v[u] = make_uint2(0u, 0u);
+            if (r0 + u < nct) {
+                uint32_t ra;
+                asm("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(a), "r"(r0 + u));
+                asm volatile("ld.shared::cluster.v2.u32 {%0,%1}, [%2];" : "=r"(v[u].x), "=r"(v[u].y) : "r"(ra));
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            t.x += v[u].x;
+            t.y += v[u].y;
+            m.x = max(m.x, v[u].x);
+            m.y = max(m.y, v[u].y);
+        }
+    }
+    *mx = m;
+    return t;
+}
+
+// All NT threads: cluster barrier 1, then bin b1 of digit 1 holding the k-th largest,
+// krem = its rank inside b1, and the overflow decision.
+template <int NT>
+__device__ __forceinline__ RxFind rx_find(int nct, int k, RxShared& S, RxPublished& P) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    __syncthreads();  // this CTA's histogram is complete
+    for (int c = warp; c < 64; c += NT / 32) {  // coarse bins: 64 fine bins each, two per lane
+        const uint2 v = reinterpret_cast<const uint2*>(S.hist + 64 * c)[lane];
+        uint32_t x = v.x + v.y;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+        if (lane == 0) S.coarse[c] = x;
+    }
+    asm volatile("barrier.cluster.arrive.release;\n\tbarrier.cluster.wait.acquire;" ::: "memory");
+    T2_MARK(8);
+    if (tid < kT2MaxCluster) S.ck[tid] = 0u;
+    if (tid == 32) {
+        P.pub[0] = 0u;
+        S.nkept = 0u;
+    }
+    if (warp == 0) {
+        uint32_t ab = 0, kr = (uint32_t)k;
+        int b = -1;
+        bool over = true;
+        const uint2 cc = rx_cluster_sum2(smem_u32(S.coarse) + 8u * lane, nct);
+        const int cb = rx_warp_find64(cc.x, cc.y, kr, &ab);
+        if (cb >= 0) {
+            kr -= ab;
+            uint2 mx;
+            const uint2 ff = rx_cluster_sum2_max(smem_u32(S.hist + 64 * cb) + 8u * lane, nct, &mx);
+            const int fb = rx_warp_find64(ff.x, ff.y, kr, &ab);
+            if (fb >= 0) {  // warp-uniform
+                b = 64 * cb + fb;
+                kr -= ab;
+                const uint32_t n = __shfl_sync(0xffffffffu, (fb & 1) ? ff.y : ff.x, fb >> 1);
+                const uint32_t m = __shfl_sync(0xffffffffu, (fb & 1) ? mx.y : mx.x, fb >> 1);
+                over = n > (uint32_t)kRxCand || m > (uint32_t)kRxCtaCand;  // = rx_threshold's test
+            }
+        }
+        if (lane == 0) {
+            S.res[0] = (uint32_t)b;
+            S.res[1] = kr;
+            S.over = over ? 1u : 0u;
+        }
+    }
+    __syncthreads();
+    T2_MARK(14);
+    return RxFind{S.res[0], S.res[1], S.over != 0u};
+}
+
+// All NT threads, one pass over the keys: candidates -> P (published); keys above b1 ->
+// lane masks amask[warp * kpt + j] and this CTA's gather list alist[0 .. nabove) in index
+// order; kmask zeroed; P.pub[1] = S.nabove.  The caller's cluster barrier 2 follows.
+template <int NT, typename Keys>
+__device__ __forceinline__ void rx_partition(const Keys& keys, int s0, int wbase, uint32_t b1, RxShared& S,
+                                             RxPublished& P, uint32_t* amask, uint32_t* kmask, uint16_t* alist) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int kpt = keys.count();
+    uint32_t mine = 0, above = 0, myw = 0;  // lane j keeps the above-mask of slot j
+    t2_for_keys(keys, [&](int j, uint32_t kj) {
+        const uint32_t d = kj ? kj >> 20 : 0u;  // empty slots: never above, never candidates
+        mine |= (uint32_t)(kj != 0u && d == b1) << j;
+        const uint32_t m = __ballot_sync(0xffffffffu, kj != 0u && d > b1);
+        myw = lane == j ? m : myw;
+        above += __popc(m);
+    });
+    if (lane < kpt) {
+        amask[warp * kpt + lane] = myw;
+        kmask[warp * kpt + lane] = 0u;
+    }
+    {
+        const uint32_t c = __popc(mine);
+        uint32_t pre = c;  // inclusive prefix over lanes
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, pre, o);
+            if (lane >= o) pre += y;
+        }
+        const uint32_t total = __shfl_sync(0xffffffffu, pre, 31);
+        uint32_t base = 0;
+        if (lane == 0) {
+            S.wab[warp] = above;
+            if (total) base = atomicAdd(&P.pub[0], total);
+        }
+        uint32_t slot = __shfl_sync(0xffffffffu, base, 0) + pre - c;
+        for (uint32_t m = mine; m; m &= m - 1, ++slot) {
+            const int j = __ffs(m) - 1;
+            if (slot < kRxCtaCand) {
+                P.ckey[slot] = keys(j);
+                P.cidx[slot] = s0 + wbase + 32 * j + lane;
+            }
+        }
+    }
+    __syncthreads();
+    uint32_t run = 0;
+    for (int w = 0; w < warp; ++w) run += S.wab[w];
+    const uint32_t lt = t2_lanemask_lt();
+    for (int j = 0; j < kpt; ++j) {
+        const uint32_t m = __shfl_sync(0xffffffffu, myw, j);
+        if ((m >> lane) & 1u) alist[run + __popc(m & lt)] = (uint16_t)(wbase + 32 * j + lane);
+        run += __popc(m);
+    }
+    if (tid == NT - 1) {  // the last warp's running count is the CTA's total
+        P.pub[1] = run;
+        S.nabove = run;
+    }
+}
+
+// The select warps (NT threads, barrier Bar), after cluster barrier 2: all candidates of
+// the row -> (T, idx_T) -> kept counts per CTA; this CTA's kept candidates -> kmask bits
+// and klist[0 .. S.nkept) (any order).
+template <int NT, typename Bar>
+__device__ __forceinline__ RxResult rx_resolve(cg::cluster_group& cluster, int s0, int slice, uint32_t krem,
+                                               RxShared& S, RxPublished& P, uint32_t* kmask, uint16_t* klist) {
+    const int nct = (int)cluster.num_blocks();
+    const int rank = (int)cluster.block_rank();
+    const int tid = threadIdx.x, lane = tid & 31;
+    RxResult R = {false, 0u, 0, 0u, 0u};
+    if (tid < nct) {
+        const uint32_t* pp = cluster.map_shared_rank(P.pub, tid);
+        S.cn[tid] = pp[0];
+        S.ca[tid] = pp[1];
+    }
+    Bar::sync();
+    uint32_t n = 0, off = 0;
+    for (int r = 0; r < nct; ++r) {
+        if (r == rank) off = n;
+        n += S.cn[r];
+    }
+    const uint32_t n0 = n, nmine = S.cn[rank];
+    for (uint32_t i = tid; i < n; i += NT) {  // all candidates of the row, rank-ordered
+        int r = 0;
+        uint32_t base = 0;
+        while (i >= base + S.cn[r]) base += S.cn[r++];
+        S.mkey[0][i] = cluster.map_shared_rank(P.ckey, r)[i - base];
+        S.midx[0][i] = cluster.map_shared_rank(P.cidx, r)[i - base];
+    }
+    Bar::sync();
+    T2_MARK(12);
+    const uint32_t* ck = S.mkey[0];
+    const int32_t* ci = S.midx[0];
+    int buf = 1;
+#pragma unroll 1
+    for (int lvl = 0; lvl < 3 && n > 32u; ++lvl) {  // key bits 19..12, 11..4, 3..0
+        const int sh = lvl == 0 ? 12 : (lvl == 1 ? 4 : 0);
+        const uint32_t msk = lvl == 2 ? 0xFu : 0xFFu;
+        n = rx_refine<NT, 256, Bar>(S, ck, ci, n, S.mkey[buf], S.midx[buf], krem,
+                                    [sh, msk](uint32_t kk, int32_t) { return (kk >> sh) & msk; });
+        ck = S.mkey[buf];
+        ci = S.midx[buf];
+        buf ^= 3;
+    }
+    if (n > 32u) {  // > 32 keys all equal to T: the krem lowest indices (digits of ~idx)
+        const uint32_t T = ck[0];
+#pragma unroll 1
+        for (int lvl = 0; lvl < 4 && n > 1u; ++lvl) {
+            const int sh = 24 - 8 * lvl;
+            n = rx_refine<NT, 256, Bar>(S, ck, ci, n, S.mkey[buf], S.midx[buf], krem,
+                                        [sh](uint32_t, int32_t ii) { return (~(uint32_t)ii >> sh) & 0xFFu; });
+            ck = S.mkey[buf];
+            ci = S.midx[buf];
+            buf ^= 3;
+        }
+        if (tid == 0) {
+            S.res[4] = T;
+            S.res[5] = (uint32_t)ci[0];
+        }
+        Bar::sync();
+    } else {
+        rx_rank32<Bar>(S, ck, ci, n, krem);
+    }
+    const uint32_t T = S.res[4];
+    const int32_t idxT = (int32_t)S.res[5];
+    R.T = T;
+    R.idxT = idxT;
+    T2_MARK(13);
+    for (uint32_t i = tid; i < n0; i += NT) {
+        const uint32_t kk = S.mkey[0][i];
+        const int32_t ii = S.midx[0][i];
+        if (kk > T || (kk == T && ii <= idxT)) atomicAdd(&S.ck[ii / slice], 1u);
+    }
+    const uint32_t lt = t2_lanemask_lt();
+    for (uint32_t i0 = 0; i0 < nmine; i0 += NT) {
+        const uint32_t i = i0 + tid;
+        bool kp = false;
+        int local = 0;
+        if (i < nmine) {
+            const uint32_t kk = S.mkey[0][off + i];
+            const int32_t ii = S.midx[0][off + i];
+            kp = kk > T || (kk == T && ii <= idxT);
+            local = ii - s0;
+        }
+        const uint32_t m = __ballot_sync(0xffffffffu, kp);
+        if (m) {
+            const int src = __ffs(m) - 1;
+            uint32_t base = 0;
+            if (lane == src) base = atomicAdd(&S.nkept, (uint32_t)__popc(m));
+            base = __shfl_sync(0xffffffffu, base, src);
+            if (kp) {
+                klist[base + __popc(m & lt)] = (uint16_t)local;
+                atomicOr(&kmask[local >> 5], 1u << (local & 31));
+            }
+        }
+    }
+    Bar::sync();
+    uint32_t cb = 0;
+    for (int r = 0; r < rank; ++r) cb += S.ca[r] + S.ck[r];
+    R.cta_base = cb;
+    R.cta_count = S.ca[rank] + S.ck[rank];
+    return R;
+}
+
+// The select warps: emit(slot, kw, j) for every kept key (key-warp kw < KW, slot j, this
+// lane) from amask | kmask, slots ascending with the index.
+template <int NT, int KW, typename Bar, typename Emit>
+__device__ __forceinline__ void rx_emit_masks(const RxResult& R, int kpt, const uint32_t* amask,
+                                              const uint32_t* kmask, RxShared& S, Emit&& emit) {
+    static_assert(KW <= 32, "");
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (warp == 0) {
+        uint32_t c = 0;
+        if (lane < KW) {
+            c = S.wab[lane];
+            for (int j = 0; j < kpt; ++j) c += __popc(kmask[lane * kpt + j]);
+        }
+        uint32_t pre = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, pre, o);
+            if (lane >= o) pre += y;
+        }
+        if (lane < KW) S.wsum[lane] = pre - c;
+    }
+    Bar::sync();
+    const uint32_t lt = t2_lanemask_lt();
+    for (int kw = warp; kw < KW; kw += NT / 32) {
+        uint32_t run = R.cta_base + S.wsum[kw];
+        for (int j = 0; j < kpt; ++j) {
+            const uint32_t m = amask[kw * kpt + j] | kmask[kw * kpt + j];
+            if ((m >> lane) & 1u) emit(run + __popc(m & lt), kw, j);
+            run += __popc(m);
+        }
     }
 }
 

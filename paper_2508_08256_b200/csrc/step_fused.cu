@@ -47,22 +47,24 @@
 // debug build only (build.py --trace): globaltimer at the phase boundaries, per CTA
 namespace fier_cuda {
 constexpr int kFsTraceCtas = 4096;
-__device__ unsigned long long g_fs_trace[kFsTraceCtas][16];
+constexpr int kFsTraceMarks = 24;
+__device__ unsigned long long g_fs_trace[kFsTraceCtas][kFsTraceMarks];
 }  // namespace fier_cuda
-#define FS_MARK(i)                                                                            \
+#define FS_MARK_T(i, thr)                                                                     \
     do {                                                                                      \
-        if (threadIdx.x == 0) {                                                               \
+        if (threadIdx.x == (thr)) {                                                           \
             const int cta_ = blockIdx.y * gridDim.x + blockIdx.x;                             \
             unsigned long long t_;                                                            \
-            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                            \
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_)::"memory");                            \
             if (cta_ < ::fier_cuda::kFsTraceCtas) ::fier_cuda::g_fs_trace[cta_][i] = t_;                                \
         }                                                                                     \
     } while (0)
 #else
-#define FS_MARK(i) \
-    do {           \
+#define FS_MARK_T(i, thr) \
+    do {                  \
     } while (0)
 #endif
+#define FS_MARK(i) FS_MARK_T(i, 0)
 #define T2_MARK(i) FS_MARK(i)
 
 #include "attn_tc.cuh"
@@ -76,26 +78,39 @@ namespace fier_cuda {
 constexpr int kFsThreads = 512;  // 16 warps: ALU/LDS latency in the scorer needs the warps
 constexpr int kFsWarps = kFsThreads / 32;
 constexpr int kFsD = 128;
-constexpr int kFsGatherWarps = 8;
-constexpr int kFsNst = 3;
+#ifndef FIER_FS_GATHER_WARPS
+#define FIER_FS_GATHER_WARPS 8
+#endif
+#ifndef FIER_FS_NST
+#define FIER_FS_NST 2
+#endif
+constexpr int kFsGatherWarps = FIER_FS_GATHER_WARPS;  // phase D: the last warps attend (tensor cores, cp.async rings),
+constexpr int kFsSelWarps = kFsWarps - kFsGatherWarps;  // the first resolve the candidates and write the selection
+constexpr int kFsSelThreads = kFsSelWarps * 32;
+constexpr int kFsNst = FIER_FS_NST;
 constexpr int kFsMaxKpt = 16;  // slice <= 8192 tokens (u16 slots in sidx)
 constexpr int kFsAppendSlabs = 5;  // sealed slabs the append warps hand to the others (~ the append's time)
 constexpr int kFsLutBytes = kNibTableBytes;
-// shared memory map (bytes from a 256-aligned base)
-constexpr int kFsRing = kFsGatherWarps * kFsNst * 2 * tc_stage_bytes<kFsD>();  // phase D rings
-constexpr int kFsLut = 0;                                                    // phase B (inside the ring area)
-constexpr int kFsKeys = kFsLut + kFsWarps * 2 * kFsLutBytes;                 // phase B/C keys (ditto)
-constexpr int kFsRx = kFsKeys + kFsThreads * kFsMaxKpt * 4;                  // phase B/C RxShared (ditto)
-constexpr int kFsSidx = kFsRing;                                             // u16 selected slots
-constexpr int kFsPub = kFsSidx + kFsThreads * kFsMaxKpt * 2;                 // RxPublished (read by peers)
-constexpr int kFsWres = kFsPub + ((int)sizeof(RxPublished) + 15) / 16 * 16;  // warp partials
-constexpr int kFsCres = kFsWres + kFsGatherWarps * (kFsD + 2) * 4;           // CTA partials (rank 0)
-constexpr int kFsQrot = kFsCres + kT2MaxCluster * (kFsD + 2) * 4;           // fp32 (rotated) query
-constexpr int kFsSmem = kFsQrot + kFsD * 4 + 256;                            // + base alignment
-static_assert(kFsRx + (int)sizeof(RxShared) <= kFsRing, "LUTs, keys and RxShared must fit in the ring area");
+// Shared memory map (bytes from a 256-aligned base).  RxShared's tail (the digit-1
+// histogram, dead after cluster barrier 2) opens the ring area; the scorer's LUTs and
+// keys (dead after the partition pass) follow it inside the ring area.
+constexpr int cmax(int x, int y) { return x > y ? x : y; }
+constexpr int kFsRx = 0;
+constexpr int kFsRing = kFsRx + (int)offsetof(RxShared, hist);                     // phase D rings
+constexpr int kFsRingBytes = kFsGatherWarps * kFsNst * 2 * tc_stage_bytes<kFsD>();
+constexpr int kFsLut = (kFsRx + (int)sizeof(RxShared) + 255) / 256 * 256;          // phase B (in the ring area)
+constexpr int kFsKeys = kFsLut + kFsWarps * 2 * kFsLutBytes;                      // phase B/C keys (ditto)
+constexpr int kFsRingArea = cmax(kFsRingBytes, kFsKeys + kFsThreads * kFsMaxKpt * 4 - kFsRing);
+constexpr int kFsSidx = kFsRing + kFsRingArea;                                    // u16 gather list
+constexpr int kFsMasks = kFsSidx + kFsThreads * kFsMaxKpt * 2;                    // amask, kmask
+constexpr int kFsPub = kFsMasks + 2 * kFsWarps * kFsMaxKpt * 4;                   // RxPublished (read by peers)
+constexpr int kFsWres = kFsPub + ((int)sizeof(RxPublished) + 15) / 16 * 16;        // warp partials
+constexpr int kFsCres = kFsWres + kFsGatherWarps * (kFsD + 2) * 4;                // CTA partials (rank 0)
+constexpr int kFsQrot = kFsCres + kT2MaxCluster * (kFsD + 2) * 4;                 // fp32 (rotated) query
+constexpr int kFsSmem = kFsQrot + kFsD * 4 + 256;                                 // + base alignment
+static_assert(kFsRing % 256 == 0, "");
 static_assert(sizeof(T2Shared) <= sizeof(RxShared), "");
 static_assert(kFsSmem <= 227 * 1024, "fused step exceeds shared memory");
-
 
 struct FsArgs {
     const void* q;
@@ -192,8 +207,8 @@ __global__ void __launch_bounds__(kFsThreads, 1) step_fused_kernel(const FsArgs 
     // Scoring is assigned per slab (32 tokens), independently of which warp owns the
     // slab's keys in phase C (keys are stored token-ordered: slab sl -> keys_s[32 sl ..]).
     // Sealed slabs are split into contiguous per-warp ranges; in the appending CTA the
-    // four append warps take kFsAppendSlabs fewer.  Open (and empty) slabs are scored
-    // after the barrier that publishes the re-packed group.
+    // four append warps take kFsAppendSlabs fewer and also score the open (and empty)
+    // slabs, right after the named barrier that publishes the re-packed group.
     const int nsl = slice / 32;
     const int ntok = max(0, min(a.tokens, s0 + slice) - s0);
     const int nsealed = appender ? (open_lo - s0) / 32 : (ntok + 31) / 32;
@@ -237,6 +252,16 @@ __global__ void __launch_bounds__(kFsThreads, 1) step_fused_kernel(const FsArgs 
             if (t0 + lane < a.tokens) bw = ld_cg16(bseq + (int64_t)(t0 + lane) * 4);
         }
     };
+    if (appender && warp < 4) {
+        // the append warps re-packed the open group: a named barrier over those four
+        // warps publishes it, and they score the open (and empty) slabs first
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        for (int sl = nsealed + warp; sl < nsl; sl += 4) {
+            uint4 p, bw;
+            load(sl, p, bw);
+            score_slab(sl, sl, p, bw);
+        }
+    }
     uint4 pb[PF], bb[PF];  // register ring: (s, z) and bit rows of the next PF slabs
 #pragma unroll
     for (int u = 0; u < PF; ++u)
@@ -252,50 +277,79 @@ __global__ void __launch_bounds__(kFsThreads, 1) step_fused_kernel(const FsArgs 
             }
         }
     }
-    if (appender) {
-        __syncthreads();  // the re-packed open group is visible to every warp of this CTA
-        for (int sl = nsealed + warp; sl < nsl; sl += kFsWarps) {
-            uint4 p, bw;
-            load(sl, p, bw);
-            score_slab(sl, sl, p, bw);
-        }
-    }
 
-    // ---- phase C: cluster Top-k, compaction to sel (global) and sidx (this CTA) ----
+    // ---- phase C: digit-1 bin over the cluster, partition of this CTA's keys ----
     FS_MARK(2);
     const SmemKeys keys{keys_s + wbase, kpt};  // phase C ownership: warp w, slot j, lane L
-    const RxResult rx = rx_threshold<kFsThreads>(cluster, keys, s0, wbase, slice, a.k, S, P);
-    FS_MARK(3);
+    uint32_t* amask = reinterpret_cast<uint32_t*>(smem + kFsMasks);
+    uint32_t* kmask = amask + kFsWarps * kFsMaxKpt;
     int32_t* selrow = a.sel + (int64_t)row * a.k;
-    uint32_t cbase = rx.cta_base, ccount = rx.cta_count;
-    auto emit = [&](uint32_t slot, int j) {
-        const int local = wbase + 32 * j + lane;
-        selrow[slot] = s0 + local;
-        sidx[slot - cbase] = (uint16_t)local;
-    };
-    if (!rx.fallback) {
-        rx_emit<kFsThreads>(keys, rx, s0, wbase, S, emit);
-    } else {  // candidate overflow (very narrow score range): exact MSD radix select
+    const RxFind f = rx_find<kFsThreads>(nct, a.k, S, P);
+    int nlist;  // gather-list rows known to every warp at the split
+    if (!f.over) {
+        rx_partition<kFsThreads>(keys, s0, wbase, f.b1, S, P, amask, kmask, sidx);
+        T2_MARK(10);
+        asm volatile("barrier.cluster.arrive.release;\n\tbarrier.cluster.wait.acquire;" ::: "memory");
+        T2_MARK(11);
+        nlist = (int)S.nabove;
+    } else {  // candidate overflow (very narrow score range): exact MSD radix select, all warps
+        uint32_t cbase = 0, ccount = 0;
         fused_fallback_select(cluster, keys, a.k, S, selrow, sidx, s0, wbase, &cbase, &ccount);
+        __syncthreads();
+        nlist = (int)ccount;
     }
-    __syncthreads();  // sidx complete; RxShared (inside the ring area) no longer read
-    FS_MARK(4);
 
-    // ---- phase D: attention over this CTA's selected rows ----
-    if (warp < kFsGatherWarps) {
+    // ---- phase D: the gather warps attend over the keys above b1 while the select warps
+    // resolve the candidates, append the kept ones to the list and write the selection ----
+    if (warp >= kFsSelWarps) {
+        const int gw = warp - kFsSelWarps;
         uint32_t qb[D / 16][2];
         tc_load_q_f32<T, D, 1>(qrot, qb);
         TcState<D> st;
         st.init();
-        const int cnt = (int)ccount;
-        const int rpw = ((cnt + kFsGatherWarps - 1) / kFsGatherWarps + kTcRows - 1) / kTcRows * kTcRows;
-        const int wr0 = min(warp * rpw, cnt), wr1 = min(wr0 + rpw, cnt);
-        const uint32_t ring = base + (uint32_t)warp * kFsNst * 2 * tc_stage_bytes<D>();
-        tc_stream_rows<T, D, true, kFsNst>(qb, Kseq, Vseq, wr0, wr1, ring, a.scale_log2,
-                                           [&](int r) { return s0 + (int)sidx[r]; }, st);
-        tc_store_state<D, 1>(st, wres + warp * (D + 2));
+        const uint32_t ring = base + kFsRing + (uint32_t)gw * kFsNst * 2 * tc_stage_bytes<D>();
+        auto tok = [&](int r) { return s0 + (int)sidx[r]; };
+        auto share = [&](int r0, int r1, int& w0, int& w1) {  // 16-row granules per warp
+            const int rpw = ((r1 - r0 + kFsGatherWarps - 1) / kFsGatherWarps + kTcRows - 1) / kTcRows * kTcRows;
+            w0 = min(r0 + gw * rpw, r1);
+            w1 = min(w0 + rpw, r1);
+        };
+        int w0, w1, c0 = 0, c1 = 0;
+        share(0, nlist, w0, w1);
+        const int nga = (w1 - w0 + kTcRows - 1) / kTcRows;  // granules above b1, then the kept candidates
+        bool listed = false;
+        auto gran = [&](int sg, int& r0) {
+            if (sg < nga) {
+                r0 = w0 + sg * kTcRows;
+                return min(kTcRows, w1 - r0);
+            }
+            if (!listed) {  // first call past the above rows: wait for the select warps' list
+                int nk = 0;
+                if (!f.over) {
+                    asm volatile("bar.sync 3, %0;" ::"n"(kFsThreads) : "memory");
+                    nk = (int)S.nkept;
+                }
+                share(nlist, nlist + nk, c0, c1);
+                listed = true;
+                FS_MARK_T(15, kFsSelThreads);
+            }
+            r0 = c0 + (sg - nga) * kTcRows;
+            return min(kTcRows, c1 - r0);
+        };
+        tc_stream_granules<T, D, true, kFsNst>(qb, Kseq, Vseq, ring, a.scale_log2, gran, tok, st);
+        tc_store_state<D, 1>(st, wres + gw * (D + 2));
+        FS_MARK_T(5, kFsSelThreads);
+    } else if (!f.over) {
+        using SelBar = NamedBar<2, kFsSelThreads>;
+        const RxResult rx = rx_resolve<kFsSelThreads, SelBar>(cluster, s0, slice, f.krem, S, P, kmask, sidx + nlist);
+        FS_MARK(3);
+        __threadfence_block();
+        asm volatile("bar.arrive 3, %0;" ::"n"(kFsThreads) : "memory");
+        rx_emit_masks<kFsSelThreads, kFsWarps, SelBar>(rx, kpt, amask, kmask, S, [&](uint32_t slot, int kw, int j) {
+            selrow[slot] = s0 + kw * 32 * kpt + 32 * j + lane;
+        });
+        FS_MARK(4);
     }
-    FS_MARK(5);
     __syncthreads();
     // CTA partial -> rank 0's cres[rank] over DSMEM
     float* dst = cluster.map_shared_rank(cres, 0) + rank * (D + 2);
@@ -457,13 +511,13 @@ extern "C" FIER_API int fier_debug_step_occupancy(int cluster) {
 }
 
 extern "C" FIER_API int fier_debug_step_trace_clear(void) {
-    static unsigned long long zeros[fier_cuda::kFsTraceCtas][16];
+    static unsigned long long zeros[fier_cuda::kFsTraceCtas][fier_cuda::kFsTraceMarks];
     return cudaMemcpyToSymbol(fier_cuda::g_fs_trace, zeros, sizeof(zeros)) == cudaSuccess ? 0 : 3;
 }
 
 extern "C" FIER_API int fier_debug_step_trace(unsigned long long* host, int ctas) {
     const int n = ctas < fier_cuda::kFsTraceCtas ? ctas : fier_cuda::kFsTraceCtas;
-    return cudaMemcpyFromSymbol(host, fier_cuda::g_fs_trace, (size_t)n * 16 * sizeof(unsigned long long)) ==
+    return cudaMemcpyFromSymbol(host, fier_cuda::g_fs_trace, (size_t)n * fier_cuda::kFsTraceMarks * sizeof(unsigned long long)) ==
                    cudaSuccess
                ? 0
                : 3;

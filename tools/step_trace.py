@@ -22,8 +22,9 @@ import bench  # noqa: E402
 import paper_2508_08256_b200 as F  # noqa: E402
 from paper_2508_08256_b200 import _lib  # noqa: E402
 
-NAMES = ["start", "append", "score", "threshold", "compact", "gather", "merge_sync", "out",
-         "t:hist_sync", "t:find_bin", "t:cand_local", "t:cand_sync", "t:cand_gather", "t:rank", "t:merged", "-"]
+NAMES = ["start", "append", "score", "resolve", "emit", "gather", "merge_sync", "out",
+         "t:hist_sync", "t:find_bin", "t:partition", "t:cand_sync", "t:cand_gather", "t:rank", "t:merged", "g:above_done",
+         "-", "-", "-", "-", "-", "-", "-", "-"]
 
 
 def main():
@@ -31,6 +32,8 @@ def main():
     ap.add_argument("--config", default="c2")
     ap.add_argument("--layers", type=int, default=4)
     ap.add_argument("--reps", type=int, default=8)
+    ap.add_argument("--pairs", type=lambda x: [tuple(map(int, p.split(":"))) for p in x.split(",")], default=[],
+                    help="mark pairs i:j to print per-CTA interval percentiles for, e.g. 16:17,18:19")
     a = ap.parse_args()
     assert os.environ.get("FIER_LIB", "").endswith("_trace.so"), "set FIER_LIB to the trace build"
     cfg = bench.CONFIGS[a.config]
@@ -49,7 +52,7 @@ def main():
         lay = F.DecodeLayer(B, Hq, Hkv, L, d, g, dtype=K.dtype, device=dev, K=K, V=V)
         lay.prefill(pos)
         layers.append((lay, q, kn, vn))
-    buf = np.zeros((4096, 16), dtype=np.uint64)
+    buf = np.zeros((4096, len(NAMES)), dtype=np.uint64)
     rows = []
     for r in range(a.reps):
         lay, q, kn, vn = layers[r % len(layers)]
@@ -79,6 +82,12 @@ def main():
         v = v[v < 10**7]
         if len(v):
             print(f"  {i} {nm:11s} median {np.median(v) / 1e3:8.2f}  max {v.max() / 1e3:8.2f}")
+    for i, j in a.pairs:  # per-CTA interval between two marks (timer resolution check)
+        d = t[:, j] - t[:, i]  # the per-step offset cancels (also for clock64 marks)
+        d = d[(d > 0) & (d < 10**8)]
+        if len(d):
+            print(f"  {NAMES[i]} -> {NAMES[j]}: ns percentiles 10/50/90 {np.percentile(d, [10, 50, 90])}, "
+                  f"distinct values {len(np.unique(d))}, smallest {np.unique(d)[:6]}")
 
 
 if __name__ == "__main__":
