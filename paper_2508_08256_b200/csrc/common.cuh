@@ -103,6 +103,17 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
     while (!mbar_try_wait(bar, phase)) {
     }
 }
+// Cluster signalling through mbarriers: one arrive (release, cluster scope) on the
+// barrier at local shared address `bar` of CTA `rank`.  The waiter uses mbar_wait (CTA
+// scope): what it then reads is peer shared memory, which L1 does not cache -- a
+// cluster-scope acquire would invalidate L1 (CCTL.IVALL) and slow the SM's MIO pipe
+// for microseconds.
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t bar, uint32_t rank) {
+    uint32_t ra;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(bar), "r"(rank));
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(ra) : "memory");
+}
+
 // cp.async.bulk global -> shared, completion counted on an mbarrier (bytes % 16 == 0).
 __device__ __forceinline__ void bulk_g2s(void* smem_dst, const void* gmem_src, uint32_t bytes,
                                          uint64_t* bar) {

@@ -435,8 +435,10 @@ __device__ __forceinline__ uint2 rx_cluster_sum2_max(uint32_t a, int nct, uint2*
 
 // All NT threads: cluster barrier 1, then bin b1 of digit 1 holding the k-th largest,
 // krem = its rank inside b1, and the overflow decision.
+// Cluster barrier 1 is the mbarrier `cbar` of every CTA (nct arrivals, phase 0): warp 0
+// arrives on all of them and waits on its own; the other warps follow at CTA scope.
 template <int NT>
-__device__ __forceinline__ RxFind rx_find(int nct, int k, RxShared& S, RxPublished& P) {
+__device__ __forceinline__ RxFind rx_find(int nct, int k, RxShared& S, RxPublished& P, uint64_t* cbar) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     __syncthreads();  // this CTA's histogram is complete
     for (int c = warp; c < 64; c += NT / 32) {  // coarse bins: 64 fine bins each, two per lane
@@ -446,7 +448,11 @@ __device__ __forceinline__ RxFind rx_find(int nct, int k, RxShared& S, RxPublish
         for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
         if (lane == 0) S.coarse[c] = x;
     }
-    asm volatile("barrier.cluster.arrive.release;\n\tbarrier.cluster.wait.acquire;" ::: "memory");
+    __syncthreads();
+    if (warp == 0) {
+        if (lane < nct) mbar_arrive_remote(smem_u32(cbar), lane);
+        mbar_wait(cbar, 0);
+    }
     T2_MARK(8);
     if (tid < kT2MaxCluster) S.ck[tid] = 0u;
     if (tid == 32) {

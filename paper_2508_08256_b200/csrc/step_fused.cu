@@ -107,7 +107,8 @@ constexpr int kFsPub = kFsMasks + 2 * kFsWarps * kFsMaxKpt * 4;                 
 constexpr int kFsWres = kFsPub + ((int)sizeof(RxPublished) + 15) / 16 * 16;        // warp partials
 constexpr int kFsCres = kFsWres + kFsGatherWarps * (kFsD + 2) * 4;                // CTA partials (rank 0)
 constexpr int kFsQrot = kFsCres + kT2MaxCluster * (kFsD + 2) * 4;                 // fp32 (rotated) query
-constexpr int kFsSmem = kFsQrot + kFsD * 4 + 256;                                 // + base alignment
+constexpr int kFsCbar = kFsQrot + kFsD * 4;                                       // 3 cluster mbarriers
+constexpr int kFsSmem = kFsCbar + 3 * 8 + 256;                                    // + base alignment
 static_assert(kFsRing % 256 == 0, "");
 static_assert(sizeof(T2Shared) <= sizeof(RxShared), "");
 static_assert(kFsSmem <= 227 * 1024, "fused step exceeds shared memory");
@@ -171,6 +172,14 @@ __global__ void __launch_bounds__(kFsThreads, 1) step_fused_kernel(const FsArgs 
     float* cres = reinterpret_cast<float*>(smem + kFsCres);
     uint32_t* keys_s = reinterpret_cast<uint32_t*>(smem + kFsKeys);
 
+    // Cluster barriers of phases C and D: one mbarrier each per CTA (nct arrivals).  The
+    // launch-phase cluster barrier makes every CTA's initialisation visible before the
+    // first remote arrive; only warp 0 waits on it (the others never use barrier.cluster
+    // again, except on the degenerate-row path).
+    uint64_t* cbar = reinterpret_cast<uint64_t*>(smem + kFsCbar);
+    if (tid == 0) {
+        for (int i = 0; i < 3; ++i) mbar_init(cbar + i, (uint32_t)nct);
+    }
     rx_clear<kFsThreads>(S);  // the scorer counts every key into the digit-1 histogram
     float* qrot = reinterpret_cast<float*>(smem + kFsQrot);  // this head's query, rotated (RoPE)
     if (tid < kFsD) {
@@ -179,6 +188,8 @@ __global__ void __launch_bounds__(kFsThreads, 1) step_fused_kernel(const FsArgs 
         qrot[tid] = to_f32(T(rope_channel(a.rope, tid, [&](int j) { return to_f32(qh[j]); })));
     }
     __syncthreads();
+    asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+    if (warp == 0) asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
     FS_MARK(0);
 
     T* Kseq = static_cast<T*>(a.K) + seq * a.cap * D;
@@ -284,15 +295,21 @@ __global__ void __launch_bounds__(kFsThreads, 1) step_fused_kernel(const FsArgs 
     uint32_t* amask = reinterpret_cast<uint32_t*>(smem + kFsMasks);
     uint32_t* kmask = amask + kFsWarps * kFsMaxKpt;
     int32_t* selrow = a.sel + (int64_t)row * a.k;
-    const RxFind f = rx_find<kFsThreads>(nct, a.k, S, P);
+    const RxFind f = rx_find<kFsThreads>(nct, a.k, S, P, cbar);
     int nlist;  // gather-list rows known to every warp at the split
     if (!f.over) {
         rx_partition<kFsThreads>(keys, s0, wbase, f.b1, S, P, amask, kmask, sidx);
         T2_MARK(10);
-        asm volatile("barrier.cluster.arrive.release;\n\tbarrier.cluster.wait.acquire;" ::: "memory");
+        __syncthreads();  // P complete: cluster barrier 2 (as in rx_find)
+        if (warp == 0) {
+            if (lane < nct) mbar_arrive_remote(smem_u32(cbar + 1), lane);
+            mbar_wait(cbar + 1, 0);
+        }
+        __syncthreads();
         T2_MARK(11);
         nlist = (int)S.nabove;
     } else {  // candidate overflow (very narrow score range): exact MSD radix select, all warps
+        if (warp != 0) asm volatile("barrier.cluster.wait.aligned;" ::: "memory");  // (its cluster.sync)
         uint32_t cbase = 0, ccount = 0;
         fused_fallback_select(cluster, keys, a.k, S, selrow, sidx, s0, wbase, &cbase, &ccount);
         __syncthreads();
@@ -371,9 +388,15 @@ __global__ void __launch_bounds__(kFsThreads, 1) step_fused_kernel(const FsArgs 
             dst[D + 1] = L;
         }
     }
-    cluster.sync();
+    __syncthreads();  // partial written: cluster barrier 3, after which no CTA reads a peer
+    if (warp == 0) {
+        if (lane < nct) mbar_arrive_remote(smem_u32(cbar + 2), lane);
+        mbar_wait(cbar + 2, 0);
+    }
     FS_MARK(6);
-    if (rank != 0 || tid >= D) return;
+    if (rank != 0) return;
+    __syncthreads();  // rank 0: every partial is in cres
+    if (tid >= D) return;
     float M = -INFINITY;
     for (int r = 0; r < nct; ++r) M = fmaxf(M, cres[r * (D + 2) + D]);
     float oo = 0.f, L = 0.f;

@@ -34,6 +34,8 @@ def main():
     ap.add_argument("--reps", type=int, default=8)
     ap.add_argument("--pairs", type=lambda x: [tuple(map(int, p.split(":"))) for p in x.split(",")], default=[],
                     help="mark pairs i:j to print per-CTA interval percentiles for, e.g. 16:17,18:19")
+    ap.add_argument("--raw", type=lambda x: [int(v) for v in x.split(",")], default=[],
+                    help="slots to print raw (probe builds: cycles), e.g. 16,17,18")
     a = ap.parse_args()
     assert os.environ.get("FIER_LIB", "").endswith("_trace.so"), "set FIER_LIB to the trace build"
     cfg = bench.CONFIGS[a.config]
@@ -53,7 +55,7 @@ def main():
         lay.prefill(pos)
         layers.append((lay, q, kn, vn))
     buf = np.zeros((4096, len(NAMES)), dtype=np.uint64)
-    rows = []
+    rows, raws = [], []
     for r in range(a.reps):
         lay, q, kn, vn = layers[r % len(layers)]
         torch.cuda.synchronize()
@@ -68,6 +70,7 @@ def main():
         buf[:] = 0
         t0 = t[:, 0].min()
         rows.append(t - t0)
+        raws.append(t.copy())
     nct = rows[0].shape[0] // (B * Hq)  # CTAs per cluster (grid = cluster x rows)
     if nct > 1:
         by_rank = np.stack([r[:B * Hq * nct, 2].reshape(B * Hq, nct) for r in rows])  # score end
@@ -82,6 +85,13 @@ def main():
         v = v[v < 10**7]
         if len(v):
             print(f"  {i} {nm:11s} median {np.median(v) / 1e3:8.2f}  max {v.max() / 1e3:8.2f}")
+    if a.raw:  # probe slots (cycles), not timestamps
+        r = np.concatenate(raws)
+        for i in a.raw:
+            v = r[:, i]
+            v = v[(v > 0) & (v < 10**7)]
+            if len(v):
+                print(f"  raw slot {i}: percentiles 10/50/90 {np.percentile(v, [10, 50, 90])}")
     for i, j in a.pairs:  # per-CTA interval between two marks (timer resolution check)
         d = t[:, j] - t[:, i]  # the per-step offset cancels (also for clock64 marks)
         d = d[(d > 0) & (d < 10**8)]
