@@ -26,7 +26,7 @@ namespace fier_cuda {
 constexpr int kTcRows = 16;  // rows per stage
 
 __device__ __forceinline__ void cp_async16_tc(uint32_t smem, const void* gmem) {
-#ifndef FIER_NO_EVICT_FIRST
+#if !defined(FIER_NO_EVICT_FIRST) && !defined(FIER_NO_EVICT_FIRST_KV)
     uint64_t pol;
     asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
     asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(smem), "l"(gmem), "l"(pol)
@@ -116,10 +116,9 @@ __device__ __forceinline__ void tc_stream_granules(const uint32_t (&qb)[D / 16][
         if (nr > 0) {
             const uint32_t kdst = ring + (uint32_t)(sg % NST) * 2 * STAGE;
             const uint32_t vdst = kdst + STAGE;
+            // rows past the end of a short granule repeat its last row: finite K/V, p = 0 there
             int tok = 0;
-            if constexpr (GATHER) {
-                if (lane < nr) tok = tok_of(r0 + lane);
-            }
+            if constexpr (GATHER) tok = tok_of(r0 + min(lane, nr - 1));
 #pragma unroll
             for (int i = 0; i < CPL; ++i) {
                 const int chunk = lane + 32 * i;
@@ -128,16 +127,11 @@ __device__ __forceinline__ void tc_stream_granules(const uint32_t (&qb)[D / 16][
                 if constexpr (GATHER) {
                     tk = __shfl_sync(0xffffffffu, tok, rr);
                 } else {
-                    tk = r0 + rr;  // contiguous rows (K0)
+                    tk = r0 + min(rr, nr - 1);  // contiguous rows (K0)
                 }
                 const uint32_t off = swz<RB>(rr, c);
-                if (rr < nr) {
-                    cp_async16_tc(kdst + off, Kseq + (int64_t)tk * D + c * 8);
-                    cp_async16_tc(vdst + off, Vseq + (int64_t)tk * D + c * 8);
-                } else {  // rows past the end: V must be finite zeros (p = 0 there)
-                    asm volatile("st.shared.v4.u32 [%0], {%1,%1,%1,%1};" ::"r"(vdst + off), "r"(0u) : "memory");
-                    asm volatile("st.shared.v4.u32 [%0], {%1,%1,%1,%1};" ::"r"(kdst + off), "r"(0u) : "memory");
-                }
+                cp_async16_tc(kdst + off, Kseq + (int64_t)tk * D + c * 8);
+                cp_async16_tc(vdst + off, Vseq + (int64_t)tk * D + c * 8);
             }
         }
         asm volatile("cp.async.commit_group;" ::: "memory");
