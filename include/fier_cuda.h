@@ -198,6 +198,29 @@ FIER_API int fier_fier_to_index(const uint8_t* buf, size_t len, int32_t* tokens,
                        int32_t* group, uint32_t* bits, size_t bits_cap, uint16_t* params,
                        size_t params_cap);
 
+/* ---- device-side FIER / KVD1 byte streams --------------------- */
+/* serialize_packed_keys (io.hpp:197-225) of one (sequence, kv head) index, written by
+ * kernels into the DEVICE buffer out (18 + fier_payload_bytes(tokens, d, g) bytes):
+ * bits = that head's [>= tokens][ceil(d/32)] words, params = its [ceil(tokens/g)][d]
+ * (s, z) binary16 pairs.  Byte-identical to fier_index_to_fier. */
+FIER_API int fier_index_export(const uint32_t* bits, const void* params, int32_t tokens, int32_t dim,
+                      int32_t group, uint8_t* out, size_t out_bytes, void* stream);
+/* parse_packed_keys (io.hpp:227-277) of a FIER stream in DEVICE memory into a device
+ * index (bits_words >= l * ceil(d/32), param_pairs >= ceil(l/g) * d).  The 18-byte
+ * header is read back (stream-synchronous) and checked with the reference's
+ * diagnostics (FIER_EDATA); NULL bits/params = size query. */
+FIER_API int fier_index_import(const uint8_t* in, size_t in_bytes, int32_t* tokens, int32_t* dim, int32_t* group,
+                      uint32_t* bits, int64_t bits_words, void* params, int64_t param_pairs, void* stream);
+/* parse_cache_dump (io.hpp:140-185) of a KVD1 stream in DEVICE memory into fp32 device
+ * values [K (l x d) | V (l x d) | queries (nq x d)] (exact for both payload dtypes);
+ * dtype = 0 (f16) or 1 (f32).  NULL values = size query. */
+FIER_API int fier_kvd1_load(const uint8_t* in, size_t in_bytes, int32_t* tokens, int32_t* dim, int32_t* queries,
+                   int32_t* dtype, float* values, int64_t values_cap, void* stream);
+/* serialize_cache_dump (io.hpp:110-137) of device fp32 values laid out as above into the
+ * DEVICE buffer out (20 + (2l + nq) * d * (dtype ? 4 : 2) bytes); f16 rounds to nearest even. */
+FIER_API int fier_kvd1_store(const float* values, int32_t tokens, int32_t dim, int32_t queries, int32_t dtype,
+                    uint8_t* out, size_t out_bytes, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -18,11 +18,14 @@ from .api import (  # noqa: F401
     fier_select,
     full_attention,
     gather_attention,
+    load_cache_dump,
     quantize,
+    save_cache_dump,
     topk_oracle,
 )
 
 __all__ = [
     "DecodeLayer", "PackedKeys", "RetrievalResult", "alloc_index", "append_token", "approx_scores",
-    "fier_attend", "fier_select", "full_attention", "gather_attention", "quantize", "topk_oracle",
+    "fier_attend", "fier_select", "full_attention", "gather_attention", "load_cache_dump", "quantize",
+    "save_cache_dump", "topk_oracle",
 ]

@@ -24,6 +24,7 @@ EXPORTS = (
     "fier_decode_step_launches", "fier_decode_step_ex",
     "fier_index_to_fier", "fier_fier_to_index", "fier_sparse_attention_ragged", "fier_shard_bounds",
     "fier_shard_candidates", "fier_shard_merge_workspace", "fier_shard_merge", "fier_lse_merge",
+    "fier_index_export", "fier_index_import", "fier_kvd1_load", "fier_kvd1_store",
 )
 
 
@@ -85,6 +86,12 @@ _SIGS = {
     "fier_index_to_fier": ([_vp, _vp, _i32, _i32, _i32, _vp, _sz], C.c_int),
     "fier_fier_to_index": ([_vp, _sz, C.POINTER(_i32), C.POINTER(_i32), C.POINTER(_i32), _vp, _sz, _vp,
                             _sz], C.c_int),
+    "fier_index_export": ([_vp, _vp, _i32, _i32, _i32, _vp, _sz, _vp], C.c_int),
+    "fier_index_import": ([_vp, _sz, C.POINTER(_i32), C.POINTER(_i32), C.POINTER(_i32), _vp, _i64, _vp, _i64,
+                           _vp], C.c_int),
+    "fier_kvd1_load": ([_vp, _sz, C.POINTER(_i32), C.POINTER(_i32), C.POINTER(_i32), C.POINTER(_i32), _vp, _i64,
+                        _vp], C.c_int),
+    "fier_kvd1_store": ([_vp, _i32, _i32, _i32, _i32, _vp, _sz, _vp], C.c_int),
 }
 
 _lib = None

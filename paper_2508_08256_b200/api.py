@@ -146,6 +146,36 @@ class PackedKeys:
                           single=True)
 
 
+    def to_fier_device(self, b: int = 0, h: int = 0) -> torch.Tensor:
+        """serialize_packed_keys (io.hpp:197-225) of sequence b, kv head h into a CUDA uint8
+        tensor, written by kernels (fier_index_export): persist it with one D2H copy."""
+        _require(self.bits.is_cuda, "to_fier_device: the index is not on a GPU")
+        out = torch.empty(18 + self.payload_bytes(), dtype=torch.uint8, device=self.bits.device)
+        check(_lib.load().fier_index_export(_p(self.bits[b, h]), _p(self.params[b, h]), self.tokens, self.dim,
+                                            self.group_size, _p(out), out.numel(), _stream()))
+        return out
+
+    @staticmethod
+    def from_fier_device(buf: torch.Tensor, capacity: Optional[int] = None) -> "PackedKeys":
+        """parse_packed_keys (io.hpp:227-277) of a FIER stream held in a CUDA uint8 tensor,
+        decoded on the device (fier_index_import)."""
+        _require(isinstance(buf, torch.Tensor) and buf.is_cuda and buf.dtype == torch.uint8,
+                 "from_fier_device: expected a CUDA uint8 tensor")
+        lib = _lib.load()
+        buf = buf.contiguous()
+        l, d, g = C.c_int32(), C.c_int32(), C.c_int32()
+        check(lib.fier_index_import(_p(buf), buf.numel(), C.byref(l), C.byref(d), C.byref(g), None, 0, None, 0,
+                                    _stream()))
+        l, d, g = l.value, d.value, g.value
+        cap = capacity or l
+        _require(cap >= l, "from_fier_device: capacity below the stored token count")
+        pk = alloc_index(1, 1, cap, d, g, buf.device)
+        check(lib.fier_index_import(_p(buf), buf.numel(), None, None, None, _p(pk.bits), pk.bits.numel(),
+                                    _p(pk.params), pk.params.numel() // 2, _stream()))
+        pk.tokens, pk.single = l, True
+        return pk
+
+
 def alloc_index(batch, kv_heads, capacity, dim, group, device="cuda") -> PackedKeys:
     W, G = (dim + 31) // 32, (capacity + group - 1) // group
     bits = torch.zeros((batch, kv_heads, capacity, W), dtype=torch.int32, device=device)
@@ -377,3 +407,39 @@ class DecodeLayer:
         check(lib.fier_full_attention(C.byref(self.shape), _p(q), _p(self.K), _p(self.V), tokens, scale,
                                       _p(out), _p(ws), ws.numel(), _stream()))
         return out
+
+
+# ---- KVD1 cache dumps straight to/from the device (io.hpp:110-185) -----------------
+
+def load_cache_dump(buf, device="cuda") -> Tuple[torch.Tensor, torch.Tensor, torch.Tensor]:
+    """parse_cache_dump (io.hpp:140-185) decoded on the GPU (fier_kvd1_load).  buf: bytes or a
+    CUDA uint8 tensor.  Returns fp32 CUDA tensors K [l, d], V [l, d], queries [nq, d] (exact)."""
+    if not isinstance(buf, torch.Tensor):
+        buf = torch.from_numpy(np.frombuffer(bytes(buf), np.uint8).copy()).to(device)
+    _require(buf.is_cuda and buf.dtype == torch.uint8, "load_cache_dump: expected bytes or a CUDA uint8 tensor")
+    buf = buf.contiguous()
+    lib = _lib.load()
+    l, d, nq, dt = C.c_int32(), C.c_int32(), C.c_int32(), C.c_int32()
+    check(lib.fier_kvd1_load(_p(buf), buf.numel(), C.byref(l), C.byref(d), C.byref(nq), C.byref(dt), None, 0,
+                             _stream()))
+    l, d, nq = l.value, d.value, nq.value
+    vals = torch.empty((2 * l + nq) * d, dtype=torch.float32, device=buf.device)
+    check(lib.fier_kvd1_load(_p(buf), buf.numel(), None, None, None, None, _p(vals), vals.numel(), _stream()))
+    vals = vals.view(2 * l + nq, d)
+    return vals[:l], vals[l:2 * l], vals[2 * l:]
+
+
+def save_cache_dump(K: torch.Tensor, V: torch.Tensor, queries: Optional[torch.Tensor] = None,
+                    dtype: str = "f16") -> torch.Tensor:
+    """serialize_cache_dump (io.hpp:110-137) encoded on the GPU (fier_kvd1_store) into a CUDA
+    uint8 tensor.  K, V: [l, d]; queries: [nq, d]; dtype "f16" (round to nearest even) or "f32"."""
+    _require(K.dim() == 2 and K.shape == V.shape, "serialize_cache_dump: K and V shapes differ")
+    l, d = K.shape
+    Q = queries if queries is not None else K.new_zeros((0, d))
+    _require(Q.dim() == 2 and Q.shape[1] == d, "serialize_cache_dump: query length does not match dim")
+    _require(dtype in ("f16", "f32"), "serialize_cache_dump: dtype must be f16 or f32")
+    vals = torch.cat([_cuda(K, "K").float(), _cuda(V, "V").float(), _cuda(Q, "queries").float()]).contiguous()
+    code = 0 if dtype == "f16" else 1
+    out = torch.empty(20 + vals.numel() * (2 if code == 0 else 4), dtype=torch.uint8, device=vals.device)
+    check(_lib.load().fier_kvd1_store(_p(vals), l, d, Q.shape[0], code, _p(out), out.numel(), _stream()))
+    return out
