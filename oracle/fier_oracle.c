@@ -310,3 +310,78 @@ int fo_fier_attend(const double* q, const double* K, const double* V, size_t l, 
     free(est);
     return rc;
 }
+
+/* ---- Quest page retrieval (baselines.hpp), SURVEY 8(f) row 2 ------------------- */
+
+/* build_page_summaries (baselines.hpp:34-56): per page, channel-wise min / max of the
+ * page's actual members (the last page may be short).  kmax/kmin: [ceil(l/L)][d]. */
+int fo_page_summaries(const double* K, size_t l, size_t d, size_t L, double* kmax, double* kmin) {
+    if (L < 1) return FO_EINVAL; /* :35 */
+    const size_t pages = (l + L - 1) / L;
+    for (size_t p = 0; p < pages; ++p) {
+        const size_t t0 = p * L, t1 = t0 + L < l ? t0 + L : l;
+        for (size_t j = 0; j < d; ++j) {
+            double mn = K[t0 * d + j], mx = mn;
+            for (size_t t = t0 + 1; t < t1; ++t) {
+                const double v = K[t * d + j];
+                mn = v < mn ? v : mn; /* std::min / std::max: first-seen on ties */
+                mx = mx < v ? v : mx;
+            }
+            kmax[p * d + j] = mx;
+            kmin[p * d + j] = mn;
+        }
+    }
+    return FO_OK;
+}
+
+/* quest_page_scores (baselines.hpp:60-79): term_j = max(q_j kmax_j, q_j kmin_j);
+ * variant 1 = sum over channels, 0 = max over channels. */
+int fo_quest_page_scores(const double* q, const double* kmax, const double* kmin, size_t pages, size_t d,
+                         int variant, double* out) {
+    for (size_t p = 0; p < pages; ++p) {
+        double acc = 0.0, best = -INFINITY;
+        for (size_t j = 0; j < d; ++j) {
+            const double hi = q[j] * kmax[p * d + j], lo = q[j] * kmin[p * d + j];
+            const double term = hi < lo ? lo : hi; /* std::max(hi, lo) */
+            acc += term;
+            best = best < term ? term : best;
+        }
+        out[p] = variant == 1 ? acc : best;
+    }
+    return FO_OK;
+}
+
+/* quest_select_quantized page scores (baselines.hpp:131-139): mean of the members'
+ * estimated scores, summed in token order. */
+int fo_page_mean(const double* est, size_t l, size_t L, double* out) {
+    if (L < 1) return FO_EINVAL; /* :122 */
+    const size_t pages = (l + L - 1) / L;
+    for (size_t p = 0; p < pages; ++p) {
+        const size_t t0 = p * L, t1 = t0 + L < l ? t0 + L : l;
+        double acc = 0.0;
+        for (size_t t = t0; t < t1; ++t) acc += est[t];
+        out[p] = acc / (double)(t1 - t0);
+    }
+    return FO_OK;
+}
+
+/* detail::select_by_page_scores (baselines.hpp:85-111): pages ranked by (score desc,
+ * index asc); whole pages while they fit, then the next page's lowest indices; the
+ * n indices ascending. */
+int fo_select_by_page_scores(const double* ps, size_t l, size_t L, size_t n, int64_t* out) {
+    if (n < 1 || n > l || L < 1) return FO_EINVAL; /* :87 */
+    const size_t pages = (l + L - 1) / L;
+    int64_t* order = (int64_t*)malloc(pages * sizeof(int64_t));
+    if (!order) return FO_EINVAL;
+    for (size_t i = 0; i < pages; ++i) order[i] = (int64_t)i;
+    qsort_r(order, pages, sizeof(int64_t), cmp_desc, (void*)ps);
+    size_t taken = 0;
+    for (size_t r = 0; r < pages && taken < n; ++r) {
+        const size_t t0 = (size_t)order[r] * L, t1 = t0 + L < l ? t0 + L : l;
+        const size_t take = taken + (t1 - t0) <= n ? t1 - t0 : n - taken;
+        for (size_t t = t0; t < t0 + take; ++t) out[taken++] = (int64_t)t;
+    }
+    qsort(out, n, sizeof(int64_t), cmp_asc);
+    free(order);
+    return FO_OK;
+}

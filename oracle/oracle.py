@@ -70,6 +70,10 @@ class Port:
         L.fo_relative_l2_error.argtypes = [_dp, _dp, _sz]
         L.fo_relative_l2_error.restype = C.c_double
         L.fo_fier_attend.argtypes = [_dp, _dp, _dp, _sz, _sz, _sz, _u64p, _dp, _dp, _sz, _i64p, _dp]
+        L.fo_page_summaries.argtypes = [_dp, _sz, _sz, _sz, _dp, _dp]
+        L.fo_quest_page_scores.argtypes = [_dp, _dp, _dp, _sz, _sz, C.c_int, _dp]
+        L.fo_page_mean.argtypes = [_dp, _sz, _sz, _dp]
+        L.fo_select_by_page_scores.argtypes = [_dp, _sz, _sz, _sz, _i64p]
 
     # half.hpp
     def double_to_half(self, x: float) -> int:
@@ -166,6 +170,44 @@ class Port:
         return sel, out
 
 
+    # baselines.hpp (Quest page retrieval)
+    def page_summaries(self, K, L: int):
+        """build_page_summaries (baselines.hpp:34): (kmax, kmin) [ceil(l/L), d]."""
+        K = _c64(K)
+        l, d = K.shape
+        P = (l + L - 1) // L
+        kmax, kmin = np.zeros((P, d)), np.zeros((P, d))
+        if self.lib.fo_page_summaries(K, l, d, L, kmax, kmin):
+            raise OracleError("build_page_summaries: page size must be >= 1")
+        return kmax, kmin
+
+    def quest_page_scores(self, q, kmax, kmin, variant: str = "sum") -> np.ndarray:
+        """quest_page_scores (baselines.hpp:60); variant "sum" or "max" over channels."""
+        kmax, kmin = _c64(kmax), _c64(kmin)
+        out = np.zeros(kmax.shape[0])
+        self.lib.fo_quest_page_scores(_c64(q), kmax, kmin, kmax.shape[0], kmax.shape[1], int(variant == "sum"), out)
+        return out
+
+    def page_mean(self, est, L: int) -> np.ndarray:
+        """quest_select_quantized's page scores (baselines.hpp:131-139)."""
+        est = _c64(est)
+        out = np.zeros((est.size + L - 1) // L)
+        if self.lib.fo_page_mean(est, est.size, L, out):
+            raise OracleError("quest_select_quantized: page size must be >= 1")
+        return out
+
+    def select_by_page_scores(self, page_scores, l: int, L: int, n: int) -> np.ndarray:
+        """detail::select_by_page_scores (baselines.hpp:85)."""
+        out = np.zeros(n, np.int64)
+        if self.lib.fo_select_by_page_scores(_c64(page_scores), l, L, n, out):
+            raise OracleError("page selection: budget out of range")
+        return out
+
+    def quest_select(self, q, K, L: int, n: int, variant: str = "sum") -> np.ndarray:
+        kmax, kmin = self.page_summaries(K, L)
+        return self.select_by_page_scores(self.quest_page_scores(q, kmax, kmin, variant), len(K), L, n)
+
+
 class Ref:
     """The reference's own functions (oracle/_ref/libfier_ref.so)."""
 
@@ -192,6 +234,11 @@ class Ref:
         L.ref_layer_free.argtypes = [C.c_void_p]
         L.ref_layer_step.argtypes = [C.c_void_p, _fp, _sz, _sz, _sz, _sz, _sz, C.c_void_p, C.c_void_p]
         L.ref_layer_step.restype = C.c_double
+        L.ref_page_summaries.argtypes = [_dp, _sz, _sz, _sz, _dp, _dp]
+        L.ref_quest_page_scores.argtypes = [_dp, _dp, _sz, _sz, _sz, C.c_int, _dp]
+        L.ref_quest_select.argtypes = [_dp, _dp, _sz, _sz, _sz, _sz, C.c_int, _i64p]
+        L.ref_quest_select_quantized.argtypes = [_dp, _u8p, _sz, _sz, _sz, _i64p]
+        L.ref_select_by_page_scores.argtypes = [_dp, _sz, _sz, _sz, _i64p]
 
     def _check(self, rc: int):
         if rc:
@@ -260,6 +307,39 @@ class Ref:
         self._check(self.lib.ref_fier_attend_fier(_c64(q), K, V, l, d, b, len(b), n, sel, out, est,
                                                   C.byref(nbytes)))
         return sel, out, est, int(nbytes.value)
+
+    def page_summaries(self, K, L: int):
+        K = _c64(K)
+        l, d = K.shape
+        P = (l + L - 1) // L
+        kmax, kmin = np.zeros((P, d)), np.zeros((P, d))
+        self._check(self.lib.ref_page_summaries(K, l, d, L, kmax, kmin))
+        return kmax, kmin
+
+    def quest_page_scores(self, q, K, L: int, variant: str = "sum") -> np.ndarray:
+        K = _c64(K)
+        out = np.zeros((K.shape[0] + L - 1) // L)
+        self._check(self.lib.ref_quest_page_scores(_c64(q), K, K.shape[0], K.shape[1], L, int(variant == "sum"),
+                                                   out))
+        return out
+
+    def quest_select(self, q, K, L: int, n: int, variant: str = "sum") -> np.ndarray:
+        K = _c64(K)
+        out = np.zeros(n, np.int64)
+        self._check(self.lib.ref_quest_select(_c64(q), K, K.shape[0], K.shape[1], L, n, int(variant == "sum"),
+                                              out))
+        return out
+
+    def quest_select_quantized(self, q, buf: bytes, L: int, n: int) -> np.ndarray:
+        b = np.frombuffer(buf, np.uint8).copy()
+        out = np.zeros(n, np.int64)
+        self._check(self.lib.ref_quest_select_quantized(_c64(q), b, len(b), L, n, out))
+        return out
+
+    def select_by_page_scores(self, page_scores, l: int, L: int, n: int) -> np.ndarray:
+        out = np.zeros(n, np.int64)
+        self._check(self.lib.ref_select_by_page_scores(_c64(page_scores), l, L, n, out))
+        return out
 
     def generate(self, l, d, planted=False, spike_count=4, spike_gain=1e3, seed=0, query_count=1):
         K = np.zeros((l, d))

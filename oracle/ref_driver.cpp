@@ -19,6 +19,7 @@
 #include <thread>
 #include <vector>
 
+#include "fier/baselines.hpp"
 #include "fier/core.hpp"
 #include "fier/half.hpp"
 #include "fier/io.hpp"
@@ -258,6 +259,68 @@ double ref_layer_step(void* p, const float* Q, size_t hq, size_t h0, size_t h1, 
     auto t1 = std::chrono::steady_clock::now();
     if (failed) return -1.0;
     return std::chrono::duration<double>(t1 - t0).count();
+}
+
+// ---- Quest page retrieval (baselines.hpp), SURVEY 8(f) row 2 ----
+
+// build_page_summaries (baselines.hpp:34)
+int ref_page_summaries(const double* K, size_t l, size_t d, size_t L, double* kmax, double* kmin) {
+    return guard([&] {
+        const fier::PageSummaries ps = fier::build_page_summaries(key_cache(K, l, d), L);
+        std::memcpy(kmax, ps.max_vecs.data().data(), ps.page_count() * d * sizeof(double));
+        std::memcpy(kmin, ps.min_vecs.data().data(), ps.page_count() * d * sizeof(double));
+    });
+}
+
+// quest_page_scores (baselines.hpp:60) over build_page_summaries; variant 1 = sum, 0 = max
+int ref_quest_page_scores(const double* q, const double* K, size_t l, size_t d, size_t L, int variant,
+                          double* out) {
+    return guard([&] {
+        const fier::PageSummaries ps = fier::build_page_summaries(key_cache(K, l, d), L);
+        const std::vector<double> s = fier::quest_page_scores(
+            fier::QueryVector(q, q + d), ps,
+            variant ? fier::QuestVariant::sum_over_channels : fier::QuestVariant::max_over_channels);
+        std::memcpy(out, s.data(), s.size() * sizeof(double));
+    });
+}
+
+// quest_select (baselines.hpp:113)
+int ref_quest_select(const double* q, const double* K, size_t l, size_t d, size_t L, size_t n, int variant,
+                     int64_t* out) {
+    return guard([&] {
+        const fier::KeyCache kc = key_cache(K, l, d);
+        const fier::PageSummaries ps = fier::build_page_summaries(kc, L);
+        const fier::Selection sel = fier::quest_select(
+            fier::QueryVector(q, q + d), kc, ps, n,
+            variant ? fier::QuestVariant::sum_over_channels : fier::QuestVariant::max_over_channels);
+        for (size_t i = 0; i < sel.indices.size(); ++i) out[i] = static_cast<int64_t>(sel.indices[i]);
+    });
+}
+
+// quest_select_quantized (baselines.hpp:120) over parse_packed_keys (io.hpp:227)
+int ref_quest_select_quantized(const double* q, const unsigned char* fier_bytes, size_t len, size_t L, size_t n,
+                               int64_t* out) {
+    return guard([&] {
+        const fier::PackedKeys pk =
+            fier::parse_packed_keys(std::string(reinterpret_cast<const char*>(fier_bytes), len));
+        const fier::Selection sel = fier::quest_select_quantized(fier::QueryVector(q, q + pk.dim), pk, L, n);
+        for (size_t i = 0; i < sel.indices.size(); ++i) out[i] = static_cast<int64_t>(sel.indices[i]);
+    });
+}
+
+// detail::select_by_page_scores (baselines.hpp:85) on given page scores (geometry only)
+int ref_select_by_page_scores(const double* page_scores, size_t l, size_t L, size_t n, int64_t* out) {
+    return guard([&] {
+        fier::PageSummaries layout;
+        layout.page_size = L;
+        layout.tokens = l;
+        const size_t pages = (l + L - 1) / L;
+        layout.max_vecs = fier::Matrix(pages, 0);
+        layout.min_vecs = fier::Matrix(pages, 0);
+        const fier::Selection sel =
+            fier::detail::select_by_page_scores(std::vector<double>(page_scores, page_scores + pages), layout, n);
+        for (size_t i = 0; i < sel.indices.size(); ++i) out[i] = static_cast<int64_t>(sel.indices[i]);
+    });
 }
 
 }  // extern "C"
