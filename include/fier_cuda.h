@@ -221,6 +221,28 @@ FIER_API int fier_kvd1_load(const uint8_t* in, size_t in_bytes, int32_t* tokens,
 FIER_API int fier_kvd1_store(const float* values, int32_t tokens, int32_t dim, int32_t queries, int32_t dtype,
                     uint8_t* out, size_t out_bytes, void* stream);
 
+/* ---- Quest page retrieval (baselines.hpp) ------------------------ */
+/* build_page_summaries (baselines.hpp:34-56): K [B][Hkv][capacity][d] (s->dtype) ->
+ * kmax, kmin [B][Hkv][ceil(tokens/L)][d] fp32 (exact channel-wise extrema). */
+FIER_API int fier_quest_summaries(const fier_shape* s, const void* K, int32_t tokens, int32_t page_size,
+                         float* kmax, float* kmin, void* stream);
+/* quest_page_scores (baselines.hpp:60-79) for q [B][Hq][d] (q head h reads kv head
+ * h / (Hq/Hkv)): page_scores[B*Hq][pld], variant 1 = sum over channels, 0 = max;
+ * evaluated in fp64, stored fp32. */
+FIER_API int fier_quest_page_scores(const fier_shape* s, const void* q, const float* kmax, const float* kmin,
+                           int32_t tokens, int32_t page_size, int32_t variant, float* page_scores,
+                           int64_t pld, void* stream);
+/* quest_select_quantized's page scores (baselines.hpp:131-139): the mean of each page's
+ * approx_scores (K2 output scores[rows][ld]) -> page_scores[rows][pld]. */
+FIER_API int fier_page_mean(const float* scores, int32_t rows, int32_t tokens, int64_t ld, int32_t page_size,
+                   float* page_scores, int64_t pld, void* stream);
+/* detail::select_by_page_scores (baselines.hpp:85-111): rank pages by (score desc, index
+ * asc), take whole pages while they fit, then the next page's lowest indices:
+ * sel[rows][n] ascending.  Workspace from fier_page_select_workspace (required). */
+FIER_API size_t fier_page_select_workspace(int32_t rows, int32_t tokens, int32_t page_size, int32_t n);
+FIER_API int fier_page_select(const float* page_scores, int32_t rows, int32_t tokens, int64_t pld, int32_t page_size,
+                     int32_t n, int32_t* sel, void* workspace, size_t workspace_bytes, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

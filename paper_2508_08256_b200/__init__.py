@@ -13,19 +13,26 @@ from .api import (  # noqa: F401
     RetrievalResult,
     alloc_index,
     append_token,
+    PageSummaries,
     approx_scores,
+    build_page_summaries,
     fier_attend,
     fier_select,
     full_attention,
     gather_attention,
     load_cache_dump,
     quantize,
+    quest_page_scores,
+    quest_select,
+    quest_select_quantized,
     save_cache_dump,
+    select_by_page_scores,
     topk_oracle,
 )
 
 __all__ = [
     "DecodeLayer", "PackedKeys", "RetrievalResult", "alloc_index", "append_token", "approx_scores",
     "fier_attend", "fier_select", "full_attention", "gather_attention", "load_cache_dump", "quantize",
-    "save_cache_dump", "topk_oracle",
+    "save_cache_dump", "topk_oracle", "PageSummaries", "build_page_summaries", "quest_page_scores",
+    "quest_select", "quest_select_quantized", "select_by_page_scores",
 ]

@@ -25,6 +25,8 @@ EXPORTS = (
     "fier_index_to_fier", "fier_fier_to_index", "fier_sparse_attention_ragged", "fier_shard_bounds",
     "fier_shard_candidates", "fier_shard_merge_workspace", "fier_shard_merge", "fier_lse_merge",
     "fier_index_export", "fier_index_import", "fier_kvd1_load", "fier_kvd1_store",
+    "fier_quest_summaries", "fier_quest_page_scores", "fier_page_mean", "fier_page_select_workspace",
+    "fier_page_select",
 )
 
 
@@ -92,6 +94,11 @@ _SIGS = {
     "fier_kvd1_load": ([_vp, _sz, C.POINTER(_i32), C.POINTER(_i32), C.POINTER(_i32), C.POINTER(_i32), _vp, _i64,
                         _vp], C.c_int),
     "fier_kvd1_store": ([_vp, _i32, _i32, _i32, _i32, _vp, _sz, _vp], C.c_int),
+    "fier_quest_summaries": ([C.POINTER(FierShape), _vp, _i32, _i32, _vp, _vp, _vp], C.c_int),
+    "fier_quest_page_scores": ([C.POINTER(FierShape), _vp, _vp, _vp, _i32, _i32, _i32, _vp, _i64, _vp], C.c_int),
+    "fier_page_mean": ([_vp, _i32, _i32, _i64, _i32, _vp, _i64, _vp], C.c_int),
+    "fier_page_select_workspace": ([_i32, _i32, _i32, _i32], _sz),
+    "fier_page_select": ([_vp, _i32, _i32, _i64, _i32, _i32, _vp, _vp, _sz, _vp], C.c_int),
 }
 
 _lib = None

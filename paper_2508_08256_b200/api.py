@@ -443,3 +443,91 @@ def save_cache_dump(K: torch.Tensor, V: torch.Tensor, queries: Optional[torch.Te
     out = torch.empty(20 + vals.numel() * (2 if code == 0 else 4), dtype=torch.uint8, device=vals.device)
     check(_lib.load().fier_kvd1_store(_p(vals), l, d, Q.shape[0], code, _p(out), out.numel(), _stream()))
     return out
+
+
+# ---- Quest page retrieval (baselines.hpp) ------------------------
+
+_VARIANTS = {"sum": 1, "sum_over_channels": 1, "max": 0, "max_over_channels": 0}
+
+
+@dataclass
+class PageSummaries:
+    """build_page_summaries (baselines.hpp:16-56) on the device: fp32 [B, Hkv, P, d]."""
+    max_vecs: torch.Tensor
+    min_vecs: torch.Tensor
+    page_size: int
+    tokens: int
+    dim: int
+    single: bool = False
+
+    def page_count(self) -> int:
+        return self.max_vecs.shape[-2]
+
+
+def build_page_summaries(K: torch.Tensor, page_size: int = 16, tokens: Optional[int] = None) -> PageSummaries:
+    """build_page_summaries (baselines.hpp:34-56).  K: [l, d] or [B, Hkv, cap, d]."""
+    _require(page_size >= 1, "build_page_summaries: page size must be >= 1")
+    single = K.dim() == 2
+    K4 = _as4(_cuda(K, "build_page_summaries"))
+    B, H, cap, d = K4.shape
+    tokens = cap if tokens is None else tokens
+    _require(1 <= tokens <= cap, "build_page_summaries: empty key cache")
+    P = (tokens + page_size - 1) // page_size
+    kmax = torch.empty((B, H, P, d), dtype=torch.float32, device=K4.device)
+    kmin = torch.empty_like(kmax)
+    shape = make_shape(B, H, H, cap, d, 1, _dtype_code(K4))
+    check(_lib.load().fier_quest_summaries(C.byref(shape), _p(K4), tokens, page_size, _p(kmax), _p(kmin),
+                                           _stream()))
+    return PageSummaries(kmax, kmin, page_size, tokens, d, single)
+
+
+def quest_page_scores(q: torch.Tensor, ps: PageSummaries, variant: str = "sum") -> torch.Tensor:
+    """quest_page_scores (baselines.hpp:60-79): fp32 [P] or [B, Hq, P] (fp64 evaluation)."""
+    _require(variant in _VARIANTS, "quest_page_scores: variant must be sum or max")
+    _require(q.shape[-1] == ps.dim, "quest_page_scores: query length does not match dim")
+    single = q.dim() == 1
+    q3 = _as3(_cuda(q, "quest_page_scores"))
+    B, Hq, d = q3.shape
+    Hkv = ps.max_vecs.shape[1]
+    _require(B == ps.max_vecs.shape[0] and Hq % Hkv == 0, "quest_page_scores: query heads do not match")
+    P = ps.page_count()
+    out = torch.empty((B, Hq, P), dtype=torch.float32, device=q3.device)
+    shape = make_shape(B, Hq, Hkv, max(ps.tokens, 1), d, 1, _dtype_code(q3))
+    check(_lib.load().fier_quest_page_scores(C.byref(shape), _p(q3), _p(ps.max_vecs), _p(ps.min_vecs), ps.tokens,
+                                             ps.page_size, _VARIANTS[variant], _p(out), P, _stream()))
+    return out.view(-1) if single else out
+
+
+def select_by_page_scores(page_scores: torch.Tensor, tokens: int, page_size: int, n: int) -> torch.Tensor:
+    """detail::select_by_page_scores (baselines.hpp:85-111): int32 ascending [n] or [..., n]."""
+    s = _cuda(page_scores, "page selection")
+    _require(s.dtype == torch.float32, "page selection: page scores must be float32")
+    _require(1 <= n <= tokens, "page selection: budget out of range")
+    P = s.shape[-1]
+    _require(P == (tokens + page_size - 1) // page_size, "page selection: page count does not match tokens")
+    rows = s.numel() // P
+    lib = _lib.load()
+    ws = torch.empty(max(1, lib.fier_page_select_workspace(rows, tokens, page_size, n)), dtype=torch.uint8,
+                     device=s.device)
+    sel = torch.empty(s.shape[:-1] + (n,), dtype=torch.int32, device=s.device)
+    check(lib.fier_page_select(_p(s), rows, tokens, P, page_size, n, _p(sel), _p(ws), ws.numel(), _stream()))
+    return sel
+
+
+def quest_select(q: torch.Tensor, K: torch.Tensor, ps: PageSummaries, n: int, variant: str = "sum") -> torch.Tensor:
+    """quest_select (baselines.hpp:113-118)."""
+    _require(K.shape[-2] >= ps.tokens and K.shape[-1] == ps.dim, "quest_select: summaries do not match cache")
+    return select_by_page_scores(quest_page_scores(q, ps, variant), ps.tokens, ps.page_size, n)
+
+
+def quest_select_quantized(q: torch.Tensor, pk: PackedKeys, page_size: int, n: int) -> torch.Tensor:
+    """quest_select_quantized (baselines.hpp:120-140): pages scored by the mean of the
+    members' approx_scores (K2 on the GPU), ranked and filled like quest_select."""
+    _require(page_size >= 1, "quest_select_quantized: page size must be >= 1")
+    est = approx_scores(q, pk)
+    rows, l = est.numel() // pk.tokens, pk.tokens
+    P = (l + page_size - 1) // page_size
+    pscores = torch.empty(est.shape[:-1] + (P,), dtype=torch.float32, device=est.device)
+    check(_lib.load().fier_page_mean(_p(est), rows, l, l, page_size, _p(pscores), P, _stream()))
+    return select_by_page_scores(pscores, l, page_size, n)
+
