@@ -243,6 +243,22 @@ FIER_API size_t fier_page_select_workspace(int32_t rows, int32_t tokens, int32_t
 FIER_API int fier_page_select(const float* page_scores, int32_t rows, int32_t tokens, int64_t pld, int32_t page_size,
                      int32_t n, int32_t* sel, void* workspace, size_t workspace_bytes, void* stream);
 
+/* ---- recall / margin sweep diagnostics (evalharness.hpp) --------- */
+/* exact_scores (core.hpp:98-112): scores[B*Hq][ld] = q . k_i in fp64 (scaled: / sqrt(d)),
+ * GQA as above; scores32 (may be NULL) receives the same rounded to fp32. */
+FIER_API int fier_exact_scores(const fier_shape* s, const void* q, const void* K, int32_t tokens, int32_t scaled,
+                      double* scores, float* scores32, int64_t ld, void* stream);
+/* margin_and_errors (evalharness.hpp:63-83) per row: report[rows][5] = (margin, max_err,
+ * l2_loss, hinge_loss, hinge_loss_symmetric) of err = exact - est; the order statistics
+ * come from K3 on exact32 (exact unless fp32 rounding ties the boundary scores). */
+FIER_API size_t fier_margin_errors_workspace(int32_t rows, int32_t k);
+FIER_API int fier_margin_errors(const double* exact, const float* exact32, const float* est, int32_t rows,
+                       int32_t tokens, int64_t ld, int32_t k, double* report, void* workspace,
+                       size_t workspace_bytes, void* stream);
+/* overlap_fraction (evalharness.hpp:40-48) per row of ascending lists: out[rows]. */
+FIER_API int fier_overlap(const int32_t* sel, int32_t n, const int32_t* oracle, int32_t no, int32_t rows, double* out,
+                 void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -239,6 +239,8 @@ class Ref:
         L.ref_quest_select.argtypes = [_dp, _dp, _sz, _sz, _sz, _sz, C.c_int, _i64p]
         L.ref_quest_select_quantized.argtypes = [_dp, _u8p, _sz, _sz, _sz, _i64p]
         L.ref_select_by_page_scores.argtypes = [_dp, _sz, _sz, _sz, _i64p]
+        L.ref_margin_and_errors.argtypes = [_dp, _dp, _sz, _sz, _u8p, _sz, _sz, _dp]
+        L.ref_run_trial.argtypes = [_dp, _dp, _sz, _sz, _dp, _sz, _sz, _sz, C.c_int, C.POINTER(_sz), _sz, _dp, _dp]
 
     def _check(self, rc: int):
         if rc:
@@ -340,6 +342,26 @@ class Ref:
         out = np.zeros(n, np.int64)
         self._check(self.lib.ref_select_by_page_scores(_c64(page_scores), l, L, n, out))
         return out
+
+    def margin_and_errors(self, q, K, buf: bytes, k: int) -> np.ndarray:
+        """evalharness.hpp:63 -> (margin, max_err, l2_loss, hinge_loss, hinge_loss_symmetric)."""
+        K = _c64(K)
+        b = np.frombuffer(buf, np.uint8).copy()
+        out = np.zeros(5)
+        self._check(self.lib.ref_margin_and_errors(_c64(q), K, K.shape[0], K.shape[1], b, len(b), k, out))
+        return out
+
+    def run_trial(self, K, V, Q, g: int, L: int, budgets, variant: str = "sum"):
+        """run_trial (evalharness.hpp:184), policies fier, quest, quest_quant, oracle, full:
+        cells [5, len(budgets), 3] = (recall, out_err, max_err), margins [len(budgets)]."""
+        K, V, Q = _c64(K), _c64(V), _c64(np.atleast_2d(Q))
+        nb = len(budgets)
+        bud = (_sz * nb)(*budgets)
+        cells = np.zeros((5, nb, 3))
+        margins = np.zeros(nb)
+        self._check(self.lib.ref_run_trial(K, V, K.shape[0], K.shape[1], Q, Q.shape[0], g, L, int(variant == "sum"),
+                                           bud, nb, cells, margins))
+        return cells, margins
 
     def generate(self, l, d, planted=False, spike_count=4, spike_gain=1e3, seed=0, query_count=1):
         K = np.zeros((l, d))

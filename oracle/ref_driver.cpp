@@ -21,6 +21,9 @@
 
 #include "fier/baselines.hpp"
 #include "fier/core.hpp"
+#ifdef FIER_REF_HARNESS
+#include "fier/evalharness.hpp"
+#endif
 #include "fier/half.hpp"
 #include "fier/io.hpp"
 #include "fier/quant1bit.hpp"
@@ -322,5 +325,57 @@ int ref_select_by_page_scores(const double* page_scores, size_t l, size_t L, siz
         for (size_t i = 0; i < sel.indices.size(); ++i) out[i] = static_cast<int64_t>(sel.indices[i]);
     });
 }
+
+// ---- evaluation harness (evalharness.hpp), SURVEY 8(f) row 4 ----
+#ifdef FIER_REF_HARNESS
+
+// margin_and_errors (evalharness.hpp:63) over parse_packed_keys (io.hpp:227); out =
+// (margin, max_err, l2_loss, hinge_loss, hinge_loss_symmetric)
+int ref_margin_and_errors(const double* q, const double* K, size_t l, size_t d, const unsigned char* fier_bytes,
+                          size_t len, size_t k, double* out) {
+    return guard([&] {
+        const fier::PackedKeys pk =
+            fier::parse_packed_keys(std::string(reinterpret_cast<const char*>(fier_bytes), len));
+        const fier::MarginReport r = fier::margin_and_errors(fier::QueryVector(q, q + d), key_cache(K, l, d), pk, k);
+        out[0] = r.margin;
+        out[1] = r.max_err;
+        out[2] = r.l2_loss;
+        out[3] = r.hinge_loss;
+        out[4] = r.hinge_loss_symmetric;
+    });
+}
+
+// run_trial (evalharness.hpp:184) on a fixed workload with the policies fier(g),
+// quest(L, variant), quest_quant(g, L), oracle, full (in that order); cells[p][b] =
+// (recall, out_err, max_err), margins[b].
+int ref_run_trial(const double* K, const double* V, size_t l, size_t d, const double* Q, size_t nq, size_t g,
+                  size_t L, int variant, const size_t* budgets, size_t nb, double* cells, double* margins) {
+    return guard([&] {
+        fier::WorkloadInstance w;
+        w.keys = key_cache(K, l, d);
+        w.values = value_cache(V, l, d);
+        for (size_t i = 0; i < nq; ++i) w.queries.emplace_back(Q + i * d, Q + (i + 1) * d);
+        std::vector<fier::BudgetPolicy> pol(5);
+        const fier::PolicyKind kinds[5] = {fier::PolicyKind::fier, fier::PolicyKind::quest,
+                                           fier::PolicyKind::quest_quant, fier::PolicyKind::oracle,
+                                           fier::PolicyKind::full};
+        for (int i = 0; i < 5; ++i) {
+            pol[i].kind = kinds[i];
+            pol[i].group_size = g;
+            pol[i].page_size = L;
+            pol[i].variant = variant ? fier::QuestVariant::sum_over_channels : fier::QuestVariant::max_over_channels;
+        }
+        const fier::detail::TrialData t =
+            fier::detail::run_trial(fier::WorkloadSpec{}, 0, pol, std::vector<size_t>(budgets, budgets + nb), &w);
+        for (size_t i = 0; i < t.cells.size(); ++i) {
+            cells[3 * i] = t.cells[i].recall;
+            cells[3 * i + 1] = t.cells[i].out_err;
+            cells[3 * i + 2] = t.cells[i].has_max_err ? t.cells[i].max_err : -1.0;
+        }
+        for (size_t b = 0; b < nb; ++b) margins[b] = t.margins[b];
+    });
+}
+
+#endif  // FIER_REF_HARNESS
 
 }  // extern "C"

@@ -26,7 +26,7 @@ EXPORTS = (
     "fier_shard_candidates", "fier_shard_merge_workspace", "fier_shard_merge", "fier_lse_merge",
     "fier_index_export", "fier_index_import", "fier_kvd1_load", "fier_kvd1_store",
     "fier_quest_summaries", "fier_quest_page_scores", "fier_page_mean", "fier_page_select_workspace",
-    "fier_page_select",
+    "fier_page_select", "fier_exact_scores", "fier_margin_errors_workspace", "fier_margin_errors", "fier_overlap",
 )
 
 
@@ -99,6 +99,10 @@ _SIGS = {
     "fier_page_mean": ([_vp, _i32, _i32, _i64, _i32, _vp, _i64, _vp], C.c_int),
     "fier_page_select_workspace": ([_i32, _i32, _i32, _i32], _sz),
     "fier_page_select": ([_vp, _i32, _i32, _i64, _i32, _i32, _vp, _vp, _sz, _vp], C.c_int),
+    "fier_exact_scores": ([C.POINTER(FierShape), _vp, _vp, _i32, _i32, _vp, _vp, _i64, _vp], C.c_int),
+    "fier_margin_errors_workspace": ([_i32, _i32], _sz),
+    "fier_margin_errors": ([_vp, _vp, _vp, _i32, _i32, _i64, _i32, _vp, _vp, _sz, _vp], C.c_int),
+    "fier_overlap": ([_vp, _i32, _vp, _i32, _i32, _vp, _vp], C.c_int),
 }
 
 _lib = None
