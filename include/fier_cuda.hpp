@@ -12,6 +12,9 @@
 //   fier::cuda::gather_attention(q, K, V, sel)  gather_attention  core.hpp:152-179
 //   fier::cuda::fier_select(q, pk, n)           fier_select       retrieval.hpp:130-133
 //   fier::cuda::fier_attend(q, K, V, pk, n)     fier_attend       retrieval.hpp:136-146
+//   fier::cuda::build_page_summaries(K, L)      build_page_summaries baselines.hpp:34-56
+//   fier::cuda::quest_select(q, K, ps, n, v)    quest_select      baselines.hpp:113-118
+//   fier::cuda::quest_select_quantized(q, pk, L, n) quest_select_quantized baselines.hpp:120-140
 //
 // The functions are templates over the cache / index / result types and only use
 // the reference's member names (K.tokens(), K.dim(), K.data.data(), pk.code_words,
@@ -85,6 +88,12 @@ struct RetrievalResult {
     std::vector<double> output;
     ScoreVector est_scores;
     uint64_t bytes_loaded_for_estimation = 0;
+};
+enum class QuestVariant { max_over_channels, sum_over_channels };  // baselines.hpp:28-31
+struct PageSummaries {  // baselines.hpp:16-29
+    std::size_t page_size = 16, tokens = 0, dim = 0;
+    Matrix max_vecs, min_vecs;
+    std::size_t page_count() const { return max_vecs.rows(); }
 };
 }  // namespace types
 
@@ -295,6 +304,88 @@ RR fier_attend(const Q& q, const KC& K, const VC& V, const PK& pk, std::size_t n
     r.output = gather_attention<decltype(r.output)>(q, K, V, r.selection);
     r.bytes_loaded_for_estimation = pk.payload_bytes();
     return r;
+}
+
+// ---- Quest page retrieval (baselines.hpp) ----
+
+namespace detail {
+// detail::select_by_page_scores (baselines.hpp:85-111) of device page scores
+template <typename SEL>
+SEL page_select(const Dev<float>& dp, std::size_t tokens, std::size_t page_size, std::size_t n) {
+    if (n < 1 || n > tokens) throw std::invalid_argument("page selection: budget out of range");
+    const std::size_t P = (tokens + page_size - 1) / page_size;
+    const std::size_t wsb = fier_page_select_workspace(1, (int32_t)tokens, (int32_t)page_size, (int32_t)n);
+    Dev<uint8_t> ws(wsb);
+    Dev<int32_t> dsel(n);
+    check(fier_page_select(dp.p, 1, (int32_t)tokens, (int64_t)P, (int32_t)page_size, (int32_t)n, dsel.p, ws.p, wsb,
+                           nullptr));
+    const std::vector<int32_t> idx = dsel.host();
+    SEL sel;
+    sel.indices.assign(idx.begin(), idx.end());
+    sel.budget = n;
+    return sel;
+}
+}  // namespace detail
+
+// build_page_summaries (baselines.hpp:34-56): channel-wise page extrema on the device
+template <typename PS = types::PageSummaries, typename KC>
+PS build_page_summaries(const KC& K, std::size_t page_size) {
+    if (page_size < 1) throw std::invalid_argument("build_page_summaries: page size must be >= 1");
+    const std::size_t l = K.tokens(), d = K.dim(), P = (l + page_size - 1) / page_size;
+    const std::vector<float> kf = detail::to_f32(detail::mat_data(K), l * d);
+    detail::Dev<float> dk(kf.data(), kf.size()), mx(P * d), mn(P * d);
+    fier_shape s = detail::shape(1, 1, 1, (int)l, (int)d, 1);
+    detail::check(fier_quest_summaries(&s, dk.p, (int32_t)l, (int32_t)page_size, mx.p, mn.p, nullptr));
+    const std::vector<float> hx = mx.host(), hn = mn.host();
+    PS ps;
+    ps.page_size = page_size;
+    ps.tokens = l;
+    ps.dim = d;
+    ps.max_vecs = decltype(ps.max_vecs)(P, d);
+    ps.min_vecs = decltype(ps.min_vecs)(P, d);
+    for (std::size_t p = 0; p < P; ++p)
+        for (std::size_t j = 0; j < d; ++j) {
+            ps.max_vecs.row(p)[j] = hx[p * d + j];
+            ps.min_vecs.row(p)[j] = hn[p * d + j];
+        }
+    return ps;
+}
+
+// quest_select (baselines.hpp:113-118); variant: the reference's QuestVariant (max = 0, sum = 1)
+template <typename SEL = types::Selection, typename Q, typename KC, typename PS, typename VAR>
+SEL quest_select(const Q& q, const KC& K, const PS& ps, std::size_t n, VAR variant) {
+    if (K.tokens() != ps.tokens || K.dim() != ps.dim)
+        throw std::invalid_argument("quest_select: summaries do not match cache");
+    if (q.size() != ps.dim) throw std::invalid_argument("quest_page_scores: query length does not match dim");
+    const std::size_t P = ps.page_count(), d = ps.dim;
+    std::vector<float> hx(P * d), hn(P * d);
+    for (std::size_t p = 0; p < P; ++p)
+        for (std::size_t j = 0; j < d; ++j) {
+            hx[p * d + j] = static_cast<float>(ps.max_vecs.row(p)[j]);
+            hn[p * d + j] = static_cast<float>(ps.min_vecs.row(p)[j]);
+        }
+    const std::vector<float> qf = detail::to_f32(q.data(), d);
+    detail::Dev<float> mx(hx.data(), hx.size()), mn(hn.data(), hn.size()), dq(qf.data(), d), dp(P);
+    fier_shape s = detail::shape(1, 1, 1, (int)ps.tokens, (int)d, 1);
+    detail::check(fier_quest_page_scores(&s, dq.p, mx.p, mn.p, (int32_t)ps.tokens, (int32_t)ps.page_size,
+                                         static_cast<int>(variant) == 1 ? 1 : 0, dp.p, (int64_t)P, nullptr));
+    return detail::page_select<SEL>(dp, ps.tokens, ps.page_size, n);
+}
+
+// quest_select_quantized (baselines.hpp:120-140): pages scored by the mean 1-bit estimate
+template <typename SEL = types::Selection, typename Q, typename PK>
+SEL quest_select_quantized(const Q& q, const PK& pk, std::size_t page_size, std::size_t n) {
+    if (page_size < 1) throw std::invalid_argument("quest_select_quantized: page size must be >= 1");
+    if (q.size() != pk.dim) throw std::invalid_argument("approx_scores: query length does not match key dim");
+    const std::size_t l = pk.tokens, P = (l + page_size - 1) / page_size;
+    detail::DevIndex di(l, pk.dim, pk.group_size);
+    detail::upload(pk, di);
+    const std::vector<float> qf = detail::to_f32(q.data(), q.size());
+    detail::Dev<float> dq(qf.data(), qf.size()), ds(l), dp(P);
+    fier_shape s = detail::shape(1, 1, 1, (int)l, (int)pk.dim, (int)pk.group_size);
+    detail::check(fier_score(&s, dq.p, di.bits.p, di.params.p, (int32_t)l, ds.p, (int64_t)l, nullptr));
+    detail::check(fier_page_mean(ds.p, 1, (int32_t)l, (int64_t)l, (int32_t)page_size, dp.p, (int64_t)P, nullptr));
+    return detail::page_select<SEL>(dp, l, page_size, n);
 }
 
 }  // namespace cuda

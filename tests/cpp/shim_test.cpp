@@ -56,6 +56,20 @@ int main(int argc, char** argv) {
     } catch (const std::invalid_argument& e) {
         e2 = e.what();
     }
+    // Quest (baselines.hpp): planted pages well above the rest, so the fp32 page scores rank
+    // exactly like the reference's fp64 ones
+    fc::types::KeyCache KQ;
+    KQ.data = fc::types::Matrix(4096, d);
+    for (auto& x : KQ.data.v) x = (double)(float)next_gauss();
+    for (std::size_t p = 0; p < 4096 / 16; p += 7)
+        for (std::size_t j = 0; j < d; ++j) {  // keep the entries fp32-representable
+            double& x = KQ.data.row(p * 16 + 3)[j];
+            x = (double)(float)(x + 4.0 * (q[j] > 0 ? 1 : -1));
+        }
+    const auto ps = fc::build_page_summaries(KQ, 16);
+    const auto qs = fc::quest_select(q, KQ, ps, 300, fc::types::QuestVariant::sum_over_channels);
+    const auto pkq = fc::quantize(KQ, fc::types::GroupSpec{g});
+    const auto qq = fc::quest_select_quantized(q, pkq, 16, 300);
     std::ofstream f(argv[1], std::ios::binary);
     put(f, K.data.v);
     put(f, V.data.v);
@@ -72,6 +86,11 @@ int main(int argc, char** argv) {
     put(f, rr.output);
     put(f, std::vector<char>(e1.begin(), e1.end()));
     put(f, std::vector<char>(e2.begin(), e2.end()));
+    put(f, KQ.data.v);
+    put(f, ps.max_vecs.v);
+    put(f, ps.min_vecs.v);
+    put(f, std::vector<int64_t>(qs.indices.begin(), qs.indices.end()));
+    put(f, std::vector<int64_t>(qq.indices.begin(), qq.indices.end()));
     std::printf("shim ok: payload %zu bytes\n", (size_t)rr.bytes_loaded_for_estimation);
     return 0;
 }

@@ -158,7 +158,8 @@ def _read_blobs(path):
         data = f.read()
     off = 0
     dtypes = [np.float64, np.float64, np.float64, np.uint64, np.float64, np.float64, np.float64, np.int64,
-              np.float64, np.int64, np.float64, np.uint8, np.uint8]
+              np.float64, np.int64, np.float64, np.uint8, np.uint8,
+              np.float64, np.float64, np.float64, np.int64, np.int64]  # + Quest: K, kmax, kmin, sel, sel_q
     for dt in dtypes:
         n = int(np.frombuffer(data[off:off + 8], np.uint64)[0])
         off += 8
@@ -171,7 +172,8 @@ def _read_blobs(path):
 @pytest.mark.gpu
 def test_cpp_shim_matches_oracle(cuda, port, tmp_path):
     """Host C++ through include/fier_cuda.hpp (fier::cuda::quantize / approx_scores /
-    topk_oracle / gather_attention / fier_select / fier_attend) against the oracle."""
+    topk_oracle / gather_attention / fier_select / fier_attend / build_page_summaries /
+    quest_select / quest_select_quantized) against the oracle."""
     import subprocess
     from paper_2508_08256_b200 import build as b
     exe = b.SHIM_BIN
@@ -180,7 +182,7 @@ def test_cpp_shim_matches_oracle(cuda, port, tmp_path):
     res = str(tmp_path / "shim.bin")
     r = subprocess.run([exe, res], capture_output=True, text=True, timeout=120)
     assert r.returncode == 0, r.stderr
-    K, V, q, cw, s, z, est, sel, out, sel2, out2, e1, e2 = _read_blobs(res)
+    K, V, q, cw, s, z, est, sel, out, sel2, out2, e1, e2, KQ, qmax, qmin, qs, qq = _read_blobs(res)
     l, d, g, n = 1000, 128, 32, 77
     K, V = K.reshape(l, d), V.reshape(l, d)
     cw_ref, s_ref, z_ref = port.quantize(K, g)
@@ -198,3 +200,11 @@ def test_cpp_shim_matches_oracle(cuda, port, tmp_path):
     assert port.relative_l2_error(out2, want) < 1e-2
     assert bytes(e1).decode() == "topk_oracle: k out of range"
     assert bytes(e2).decode() == "fier_select: budget out of range"
+    # Quest through the shim (baselines.hpp): exact summaries, the oracle's selections
+    KQ = KQ.reshape(4096, d)
+    kmax, kmin = port.page_summaries(KQ, 16)
+    assert np.array_equal(qmax.reshape(kmax.shape), kmax) and np.array_equal(qmin.reshape(kmin.shape), kmin)
+    assert np.array_equal(qs, port.quest_select(q, KQ, 16, 300, "sum"))
+    bufq = port.quantize_fier(KQ, g)
+    est_q = port.approx_scores_fier(q, bufq)
+    assert np.array_equal(qq, port.select_by_page_scores(port.page_mean(est_q, 16), 4096, 16, 300))
