@@ -45,14 +45,14 @@ __global__ void __launch_bounds__(kPackThreads) append_kernel(T* __restrict__ K,
             if (j < zero_n) zero_words[j] = 0;
         }
     }
-    // Thread c writes channel c and is the lane that re-reads it below (warp
-    // (c/32) % 4 owns slice c/32): program order suffices.
+    // The group re-pack takes token pos from k_new; the K/V row stores follow it,
+    // so the group's loads do not queue behind them.
+    pack_group<T>(Kseq, d, W, g, pos / g, pos + 1, bits + seq * cap * W, sz + seq * G * d,
+                  nonfinite, k_new + seq * d, pos);
     for (int c = threadIdx.x; c < d; c += blockDim.x) {
         Kseq[(int64_t)pos * d + c] = k_new[seq * d + c];
         V[seq * cap * d + (int64_t)pos * d + c] = v_new[seq * d + c];
     }
-    pack_group<T>(Kseq, d, W, g, pos / g, pos + 1, bits + seq * cap * W, sz + seq * G * d,
-                  nonfinite);
 }
 
 template <typename T>

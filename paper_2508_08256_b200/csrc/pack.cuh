@@ -10,20 +10,28 @@ constexpr int kPackThreads = 128;  // 4 warps; warp w packs channel slices w, w+
 
 // Values of one 32-token chunk of this lane's channel, loaded together (one
 // memory latency per chunk instead of one per token).  bf16/fp16/fp32 are
-// exact in fp32; they are widened to fp64 for the arithmetic below.
+// exact in fp32; they are widened to fp64 for the arithmetic below.  Token
+// tnew (the row a decode-time append is storing right now) takes the value
+// xnew, read from the appended row itself, so the group's loads do not wait
+// behind the store (the loaded copy of that row is discarded).
 template <typename T>
 __device__ __forceinline__ void load_chunk(const T* Kseq, int d, int c, bool valid,
-                                           int tc, int cnt, float (&v)[32]) {
+                                           int tc, int cnt, float (&v)[32], float xnew, int tnew) {
 #pragma unroll
-    for (int i = 0; i < 32; ++i)
-        v[i] = (valid && i < cnt) ? to_f32(Kseq[(int64_t)(tc + i) * d + c]) : 0.f;
+    for (int i = 0; i < 32; ++i) {
+        // read-only path: the only row this launch writes (tnew) is stored after the
+        // re-pack, and its loaded copy is discarded
+        const float x = (valid && i < cnt) ? to_f32(__ldg(Kseq + (int64_t)(tc + i) * d + c)) : 0.f;
+        v[i] = tc + i == tnew ? xnew : x;
+    }
 }
 
 template <typename T>
 __device__ __forceinline__ void pack_group(const T* Kseq,  // no restrict: append re-reads its own store
                                            int d, int W, int g, int gi,
                                            int t_end, uint32_t* __restrict__ bits_seq,
-                                           __half2* __restrict__ sz_seq, int32_t* nonfinite) {
+                                           __half2* __restrict__ sz_seq, int32_t* nonfinite,
+                                           const T* nrow = nullptr, int tnew = -1) {
     const int lane = threadIdx.x & 31;
     for (int warp = threadIdx.x >> 5; warp < W; warp += blockDim.x >> 5) {
     const int c = warp * 32 + lane;
@@ -31,13 +39,14 @@ __device__ __forceinline__ void pack_group(const T* Kseq,  // no restrict: appen
     const int t0 = gi * g;
     const int t1 = min(t0 + g, t_end);  // short final group (quant1bit.hpp:84)
     float v[32];
+    const float xnew = (nrow && valid) ? to_f32(nrow[c]) : 0.f;
     // min/max on the exact fp32 values (== their fp64 widenings), sequential with
     // std::min/std::max semantics: a tie keeps the first-seen value (+0 vs -0).
     float mn = 0.f, mx = 0.f;
     bool bad = false;
     for (int tc = t0; tc < t1; tc += 32) {
         const int cnt = min(32, t1 - tc);
-        load_chunk<T>(Kseq, d, c, valid, tc, cnt, v);
+        load_chunk<T>(Kseq, d, c, valid, tc, cnt, v, xnew, tnew);
 #pragma unroll
         for (int i = 0; i < 32; ++i) {
             if (i < cnt) {
@@ -65,7 +74,7 @@ __device__ __forceinline__ void pack_group(const T* Kseq,  // no restrict: appen
     // g <= 32 the chunk is still in registers.
     for (int tc = t0; tc < t1; tc += 32) {
         const int cnt = min(32, t1 - tc);
-        if (g > 32) load_chunk<T>(Kseq, d, c, valid, tc, cnt, v);
+        if (g > 32) load_chunk<T>(Kseq, d, c, valid, tc, cnt, v, xnew, tnew);
         uint32_t mine = 0;
 #pragma unroll
         for (int i = 0; i < 32; ++i) {
@@ -82,11 +91,14 @@ __device__ __forceinline__ void pack_group(const T* Kseq,  // no restrict: appen
 // Decode-time re-pack of the open group [gi*g, t_end) (one group per launch, so
 // the code stays small: no divergent unrolled paths).  Threads [0, 32*W) take
 // part, thread c owns channel c; the same rules as pack_group (first-seen
-// min/max, fp64 z/s, cvt.rn.f16.f64, compare against the unrounded z).
+// min/max, fp64 z/s, cvt.rn.f16.f64, compare against the unrounded z).  Token
+// tnew takes the value xnew (this thread's channel of the row being appended,
+// already rounded to T) instead of a load that would wait behind its store.
 template <typename T>
 __device__ __forceinline__ void pack_open_group(const T* Kseq,  // no restrict: re-reads the appended row
                                                 int d, int g, int gi, int t_end, uint32_t* __restrict__ bits_seq,
-                                                __half2* __restrict__ sz_seq) {
+                                                __half2* __restrict__ sz_seq, float xnew = 0.f,
+                                                int tnew = -1) {
     const int W = (d + 31) / 32;
     const int c = threadIdx.x, lane = c & 31, w = c >> 5;
     if (w >= W) return;
@@ -99,7 +111,7 @@ __device__ __forceinline__ void pack_open_group(const T* Kseq,  // no restrict: 
 #pragma unroll
         for (int i = 0; i < 32; ++i) {
             const int t = min(tc + i, t1 - 1);  // past the end: repeat the last token (no effect)
-            v[i] = valid ? to_f32(Kseq[(int64_t)t * d + c]) : 0.f;
+            v[i] = !valid ? 0.f : t == tnew ? xnew : to_f32(Kseq[(int64_t)t * d + c]);
         }
         if (tc == t0) mn = mx = v[0];
 #pragma unroll
@@ -119,7 +131,7 @@ __device__ __forceinline__ void pack_open_group(const T* Kseq,  // no restrict: 
 #pragma unroll
             for (int i = 0; i < 32; ++i) {
                 const int t = min(tc + i, t1 - 1);
-                v[i] = valid ? to_f32(Kseq[(int64_t)t * d + c]) : 0.f;
+                v[i] = !valid ? 0.f : t == tnew ? xnew : to_f32(Kseq[(int64_t)t * d + c]);
             }
         }
         uint32_t mine = 0;

@@ -149,12 +149,21 @@ __global__ void __launch_bounds__(kScoreWarps * 32) score128_kernel(
         }
         T* Kseq = static_cast<T*>(ap.K) + seq * cap * D;
         T* Vseq = static_cast<T*>(ap.V) + seq * cap * D;
-        // thread c writes channel c and re-reads it in pack_group (warp c/32, lane c%32)
-        for (int c = threadIdx.x; c < D; c += blockDim.x) {
-            Kseq[(int64_t)ap.pos * D + c] = static_cast<const T*>(ap.k_new)[seq * D + c];
-            Vseq[(int64_t)ap.pos * D + c] = static_cast<const T*>(ap.v_new)[seq * D + c];
+        // The re-pack takes token pos from k_new; the K/V rows are loaded first and
+        // stored after it, so neither the group's loads nor the stores wait in line.
+        static_assert(D <= kScoreWarps * 32, "one channel per thread");
+        const bool own = threadIdx.x < D;
+        T kr{}, vr{};
+        if (own) {
+            kr = static_cast<const T*>(ap.k_new)[seq * D + threadIdx.x];
+            vr = static_cast<const T*>(ap.v_new)[seq * D + threadIdx.x];
         }
-        pack_group<T>(Kseq, D, 4, g, ap.pos / g, ap.pos + 1, bseq, zseq, nullptr);
+        pack_group<T>(Kseq, D, 4, g, ap.pos / g, ap.pos + 1, bseq, zseq, nullptr,
+                      static_cast<const T*>(ap.k_new) + seq * D, ap.pos);
+        if (own) {
+            Kseq[(int64_t)ap.pos * D + threadIdx.x] = kr;
+            Vseq[(int64_t)ap.pos * D + threadIdx.x] = vr;
+        }
         __syncthreads();  // the re-packed group is visible to every warp of this CTA
         for (int slab = open0 + warp; slab < nslabs; slab += kScoreWarps) {
             const int t = slab * 32 + lane;

@@ -291,12 +291,20 @@ __global__ void __launch_bounds__(kMmaWarps * 32) score_mma_kernel(const T* __re
             T* Vseq = static_cast<T*>(ap.V) + (int64_t)seq * cap * 128;
             uint32_t* bseq = bits + (int64_t)seq * cap * 4;
             __half2* zseq = sz + (int64_t)seq * G * 128;
-            for (int c = threadIdx.x; c < 128; c += blockDim.x) {
-                Kseq[(int64_t)ap.pos * 128 + c] = static_cast<const T*>(ap.k_new)[(int64_t)seq * 128 + c];
-                Vseq[(int64_t)ap.pos * 128 + c] = static_cast<const T*>(ap.v_new)[(int64_t)seq * 128 + c];
+            // token pos comes from k_new; the K/V rows are loaded first and stored after
+            // the re-pack, so neither the group's loads nor the stores wait in line
+            const bool own = threadIdx.x < 128;
+            T kr{}, vr{};
+            if (own) {
+                kr = static_cast<const T*>(ap.k_new)[(int64_t)seq * 128 + threadIdx.x];
+                vr = static_cast<const T*>(ap.v_new)[(int64_t)seq * 128 + threadIdx.x];
             }
-            __syncthreads();
-            pack_group<T>(Kseq, 128, 4, g, ap.pos >> (5 + lg), ap.pos + 1, bseq, zseq, nullptr);
+            pack_group<T>(Kseq, 128, 4, g, ap.pos >> (5 + lg), ap.pos + 1, bseq, zseq, nullptr,
+                          static_cast<const T*>(ap.k_new) + (int64_t)seq * 128, ap.pos);
+            if (own) {
+                Kseq[(int64_t)ap.pos * 128 + threadIdx.x] = kr;
+                Vseq[(int64_t)ap.pos * 128 + threadIdx.x] = vr;
+            }
             __syncthreads();
             lane_q<T, HPG>(q + ((int64_t)b * hq + h * HPG) * 128, L.ch, dn, L);
             for (int slab = open0 + warp; slab < nslabs; slab += kMmaWarps) {

@@ -203,9 +203,11 @@ __global__ void __launch_bounds__(kFsThreads, 1) step_fused_kernel(const FsArgs 
     const int open_lo = appender ? (a.pos / a.g) * a.g : INT_MAX;  // first token of the open group
     if (appender && tid < D) {
         const T* kn = static_cast<const T*>(a.k_new) + seq * D;
-        Kseq[(int64_t)a.pos * D + tid] = T(rope_channel(a.rope, tid, [&](int j) { return to_f32(kn[j]); }));
-        Vseq[(int64_t)a.pos * D + tid] = static_cast<const T*>(a.v_new)[seq * D + tid];
-        pack_open_group<T>(Kseq, D, a.g, a.pos / a.g, a.pos + 1, bseq, zseq);
+        const T kv = T(rope_channel(a.rope, tid, [&](int j) { return to_f32(kn[j]); }));
+        const T vv = static_cast<const T*>(a.v_new)[seq * D + tid];
+        pack_open_group<T>(Kseq, D, a.g, a.pos / a.g, a.pos + 1, bseq, zseq, to_f32(kv), a.pos);
+        Kseq[(int64_t)a.pos * D + tid] = kv;  // after the re-pack: its loads do not queue behind this store
+        Vseq[(int64_t)a.pos * D + tid] = vv;
     }
 
     FS_MARK(1);
