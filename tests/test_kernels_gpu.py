@@ -399,3 +399,31 @@ def test_topk_long_rows(cuda, port, l, k):
     sel = F.topk_oracle(s.to(cuda), k).cpu().numpy()
     for r in range(3):
         np.testing.assert_array_equal(sel[r], port.topk(s[r].double().numpy(), k))
+
+
+@pytest.mark.parametrize("hq,hkv,dtype,g,pos", [
+    (8, 8, torch.bfloat16, 32, 4127),   # MHA: one-launch step (the appending CTA re-packs, then stores)
+    (8, 8, torch.float32, 32, 4096),    # fp32 MHA: append fused into score128
+    (8, 2, torch.bfloat16, 32, 4131),   # GQA: append fused into the tensor-core scorer
+    (8, 2, torch.bfloat16, 64, 0),      # first token of an empty cache
+])
+def test_step_writes_kv_rows_and_open_group(cuda, port, hq, hkv, dtype, g, pos):
+    """Every step path stores the new k / v rows exactly (the re-pack reads token pos from
+    k_new and the row stores come after it) and leaves the index == quantize(K[0:pos+1])."""
+    F = fier()
+    torch.manual_seed(pos + hq + hkv)
+    B, d, cap, n = 1, 128, 4200, 1
+    layer = F.DecodeLayer(B, hq, hkv, cap, d, g, dtype=dtype, device=cuda)
+    layer.K.copy_(torch.randn(B, hkv, cap, d, device=cuda).to(dtype))
+    layer.V.copy_(torch.randn(B, hkv, cap, d, device=cuda).to(dtype))
+    if pos > 0:
+        layer.prefill(pos)
+    q = torch.randn(B, hq, d, device=cuda).to(dtype)
+    kn = (torch.randn(B, hkv, d, device=cuda) * 4).to(dtype)  # likely a new group min/max
+    vn = torch.randn(B, hkv, d, device=cuda).to(dtype)
+    layer.step(q, kn, vn, pos, n)
+    torch.cuda.synchronize()
+    assert torch.equal(layer.K[:, :, pos], kn)
+    assert torch.equal(layer.V[:, :, pos], vn)
+    for kv in range(hkv):
+        assert layer.pk.to_fier(0, kv) == port.quantize_fier(layer.K[0, kv, :pos + 1].double().cpu().numpy(), g)
