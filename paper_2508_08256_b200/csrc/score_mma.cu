@@ -53,7 +53,17 @@ struct AppendArgs2 {  // K == nullptr: no fused append
     int pos;
     int* zero_words;
     int zero_n;
+    int rebalance;  // sealed slabs fewer per warp of an appending CTA
 };
+
+// FIER_MMA_REBALANCE overrides the default (measurement knob)
+static int mma_rebalance() {
+    static const int v = [] {
+        const char* e = getenv("FIER_MMA_REBALANCE");
+        return e ? atoi(e) : 6;
+    }();
+    return v;
+}
 
 // k-slot (0..127, = 16 * k-step + k) -> channel and exponent of its A value
 __host__ __device__ constexpr int kslot_i(int ks) { return 2 * (ks >> 4) + ((ks & 15) >= 8 ? 1 : 0); }
@@ -328,8 +338,17 @@ __global__ void __launch_bounds__(kMmaWarps * 32) score_mma_kernel(const T* __re
     const int64_t total = (int64_t)open0 * nseq;
     const int64_t nwarps = (int64_t)gridDim.x * kMmaWarps;
     const int64_t gw = (int64_t)blockIdx.x * kMmaWarps + warp;
-    const int64_t per = (total + nwarps - 1) / nwarps;
-    const int64_t w0 = min(total, gw * per), w1 = min(total, w0 + per);
+    // The warps of the CTAs that ran the fused append start late: they take `ra` slabs fewer
+    // (when every appending CTA appended once, nseq <= gridDim.x).
+    const int64_t na = (ap.K && nseq <= (int)gridDim.x) ? (int64_t)nseq * kMmaWarps : 0;
+    int64_t per = (total + nwarps - 1) / nwarps, ra = 0;
+    if (na > 0) {
+        ra = min((int64_t)ap.rebalance, per);
+        per = (total + na * ra + nwarps - 1) / nwarps;
+        ra = min(ra, per);
+    }
+    const int64_t w0 = min(total, gw < na ? gw * (per - ra) : na * (per - ra) + (gw - na) * per);
+    const int64_t w1 = min(total, w0 + (gw < na ? per - ra : per));
     if (w0 >= w1) return;
     if (lane == 0) {
         for (int s = 0; s < kMmaStages; ++s) mbar_init(&full[s], 1);
@@ -427,7 +446,7 @@ static int mma_typed(const fier_shape* s, const void* q, const uint32_t* bits, c
 int score_mma_dispatch(const fier_shape* s, const void* q, const uint32_t* bits, const void* params, int tokens,
                        float* scores, int64_t ld, void* K, void* V, const void* k_new, const void* v_new, int pos,
                        int* zero_words, int zero_n, cudaStream_t st) {
-    const AppendArgs2 ap = {K, V, k_new, v_new, pos, zero_words, zero_n};
+    const AppendArgs2 ap = {K, V, k_new, v_new, pos, zero_words, zero_n, mma_rebalance()};
     switch (s->dtype) {
         case FIER_F32: return mma_typed<float>(s, q, bits, params, tokens, scores, ld, ap, st);
         case FIER_F16: return mma_typed<__half>(s, q, bits, params, tokens, scores, ld, ap, st);
