@@ -173,8 +173,12 @@ __global__ void __launch_bounds__(kScoreWarps * 32) score128_kernel(
         }
     }
 
-    const int stride = gridDim.x * kScoreWarps;
-    int slab = blockIdx.x * kScoreWarps + warp;
+    // With a fused append, CTA 0 (which re-packed and scored the open group) takes no sealed
+    // slabs: the launch has one CTA more for them (launch_fast).
+    const int skip = (ap.K && gridDim.x > 1) ? 1 : 0;
+    if ((int)blockIdx.x < skip) return;
+    const int stride = (gridDim.x - skip) * kScoreWarps;
+    int slab = (blockIdx.x - skip) * kScoreWarps + warp;
     if (slab >= open0) return;
     // register double buffer: parameters + bit row of the next slab
     uint4 p_cur = sz4[(int64_t)((slab * 32) / g) * 32 + lane];
@@ -228,7 +232,7 @@ static int launch_fast(const fier_shape* s, const void* q, const uint32_t* bits,
     static const int per_sm = ctas_per_sm(score128_kernel<T, HPG>, kScoreWarps * 32, 0);
     const int64_t units = (int64_t)s->kv_heads * s->batch;
     int gx = (int)std::max<int64_t>(1, (int64_t)per_sm * num_sms() / units);
-    gx = (int)std::min<int64_t>(gx, ceil_div(nslabs, kScoreWarps));
+    gx = (int)std::min<int64_t>(gx, ceil_div(nslabs, kScoreWarps) + (ap.K ? 1 : 0));
     dim3 grid(gx, s->kv_heads, s->batch);
     score128_kernel<T, HPG><<<grid, kScoreWarps * 32, 0, st>>>(
         static_cast<const T*>(q), const_cast<uint32_t*>(bits),
