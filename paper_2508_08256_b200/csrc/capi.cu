@@ -188,9 +188,37 @@ int fier_full_attention(const fier_shape* s, const void* q, const void* K, const
 
 int64_t fier_step_scores_ld(int32_t tokens) { return ceil_div(tokens, 32) * 32; }
 
-// workspace: [scores][attention partials + counters][top-k][rotated q, k_new (RoPE, separate kernels)]
+// workspace: [scores][attention partials + counters][top-k][q, k_new, v_new: rotated (RoPE) or
+// staged from host memory (separate kernels)]
 static size_t rope_bytes(const fier_shape* s) {
-    return align_up((size_t)s->batch * (s->q_heads + s->kv_heads) * s->dim * elem_size(s->dtype));
+    return align_up((size_t)s->batch * (s->q_heads + 2 * s->kv_heads) * s->dim * elem_size(s->dtype));
+}
+
+static bool host_resident(const void* p) {
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeHost;
+}
+
+// One launch copies the step's inputs out of (pinned, mapped) host memory, so the separate
+// kernels' CTAs read them from HBM instead of each paying its own PCIe round trips.
+__global__ void stage_inputs_kernel(const uint8_t* a, uint8_t* da, int64_t na, const uint8_t* b, uint8_t* db,
+                                    int64_t nb, const uint8_t* c, uint8_t* dc, int64_t nc) {
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, nt = (int64_t)gridDim.x * blockDim.x;
+    auto copy = [&](const uint8_t* src, uint8_t* dst, int64_t n) {
+        if ((((uintptr_t)src | (uintptr_t)dst | (uintptr_t)n) & 15) == 0) {
+            for (int64_t i = tid; i < n / 16; i += nt)
+                reinterpret_cast<uint4*>(dst)[i] = reinterpret_cast<const uint4*>(src)[i];
+        } else {
+            for (int64_t i = tid; i < n; i += nt) dst[i] = src[i];
+        }
+    };
+    copy(a, da, na);
+    copy(b, db, nb);
+    copy(c, dc, nc);
 }
 
 size_t fier_decode_workspace(const fier_shape* s, int32_t tokens, int32_t n) {
@@ -235,11 +263,25 @@ int fier_decode_step_ex(const fier_shape* s, const void* q, const void* k_new, c
     float* scores = scores_out ? scores_out : reinterpret_cast<float*>(ws);
     uint8_t* attn_ws = ws + align_up((size_t)s->batch * s->q_heads * ld * sizeof(float));
     int* counters = reinterpret_cast<int*>(attn_ws + sparse_counter_offset(s, n));
+    uint8_t* rws = attn_ws + align_up(sparse_workspace(s, n)) +
+                   align_up(topk_workspace(s->batch * s->q_heads, tokens, n));
+    const size_t qb = (size_t)s->batch * s->q_heads * s->dim * elem_size(s->dtype);
+    const size_t kb = (size_t)s->batch * s->kv_heads * s->dim * elem_size(s->dtype);
+    // (with RoPE the rope kernel already moves q / k_new out of host memory once)
+    if (!rope && (host_resident(q) || host_resident(k_new) || host_resident(v_new))) {
+        const int64_t words = (int64_t)(qb + 2 * kb) / 16;
+        const int blocks = (int)std::min<int64_t>(num_sms(), std::max<int64_t>(1, ceil_div(words, 256)));
+        stage_inputs_kernel<<<blocks, 256, 0, st>>>(static_cast<const uint8_t*>(q), rws, (int64_t)qb,
+                                                    static_cast<const uint8_t*>(k_new), rws + qb, (int64_t)kb,
+                                                    static_cast<const uint8_t*>(v_new), rws + qb + kb, (int64_t)kb);
+        if (int rc = check_launch("fier_decode_step (staging)")) return rc;
+        q = rws;
+        k_new = rws + qb;
+        v_new = rws + qb + kb;
+    }
     if (rope) {  // rotated copies of q and k_new for the separate kernels
-        uint8_t* rws = attn_ws + align_up(sparse_workspace(s, n)) +
-                       align_up(topk_workspace(s->batch * s->q_heads, tokens, n));
         void* q_rot = rws;
-        void* k_rot = rws + (size_t)s->batch * s->q_heads * s->dim * elem_size(s->dtype);
+        void* k_rot = rws + qb;
         if (int rc = rope_dispatch(s, q, k_new, pos, rope, q_rot, k_rot, st)) return rc;
         q = q_rot;
         k_new = k_rot;

@@ -427,3 +427,37 @@ def test_step_writes_kv_rows_and_open_group(cuda, port, hq, hkv, dtype, g, pos):
     assert torch.equal(layer.V[:, :, pos], vn)
     for kv in range(hkv):
         assert layer.pk.to_fier(0, kv) == port.quantize_fier(layer.K[0, kv, :pos + 1].double().cpu().numpy(), g)
+
+
+@pytest.mark.parametrize("hq,hkv,dtype,rope", [
+    (8, 2, torch.bfloat16, None),                 # GQA: inputs staged from host memory, then 3 launches
+    (8, 8, torch.float32, None),                  # fp32 MHA
+    (8, 2, torch.bfloat16, (10000.0, 128, False)),  # RoPE: the rope kernel reads host q / k_new itself
+])
+def test_step_with_host_resident_inputs(cuda, hq, hkv, dtype, rope):
+    """fier_decode_step on pinned host q / k_new / v_new / out (the zero-copy public-API path)
+    gives bit-identical results to the same step on device buffers."""
+    F = fier()
+    B, d, cap, pos, n = 2, 128, 3000, 2500, 300
+    torch.manual_seed(11)
+    K0 = torch.randn(B, hkv, cap, d, device=cuda).to(dtype)
+    V0 = torch.randn(B, hkv, cap, d, device=cuda).to(dtype)
+    q = torch.randn(B, hq, d, device=cuda).to(dtype)
+    kn = torch.randn(B, hkv, d, device=cuda).to(dtype)
+    vn = torch.randn(B, hkv, d, device=cuda).to(dtype)
+    outs = []
+    for host in (False, True):
+        layer = F.DecodeLayer(B, hq, hkv, cap, d, 32, dtype=dtype, device=cuda)
+        layer.K.copy_(K0)
+        layer.V.copy_(V0)
+        layer.prefill(pos)
+        if host:
+            qa, ka, va = (x.cpu().pin_memory() for x in (q, kn, vn))
+            out = torch.empty(B, hq, d, dtype=torch.float32).pin_memory()
+        else:
+            qa, ka, va, out = q, kn, vn, None
+        o, sel = layer.step(qa, ka, va, pos, n, out=out, rope=rope)
+        torch.cuda.synchronize()
+        outs.append((o.cpu().clone(), sel.cpu().clone(), layer.K[:, :, pos].cpu(), layer.V[:, :, pos].cpu()))
+    for a, b in zip(*outs):
+        assert torch.equal(a, b)
