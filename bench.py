@@ -316,7 +316,7 @@ def run_ours(args, cfg, world, rank, local):
         return statistics.median(best)
 
     kreps = max(4 * n_layers, 40)
-    launches = lib.fier_decode_step_launches(C.byref(layers[0].shape), pos + 1, n)
+    launches = layers[0].launches(pos + 1, n)
     fused_us = graph_time(step, kreps) if launches == 1 else None  # the one-launch step kernel alone
     for li in range(n_layers):  # scores/selections of every layer for the isolated K3/K4 runs
         k_score(li)
@@ -386,7 +386,7 @@ def run_ours(args, cfg, world, rank, local):
 
     def zc_step(li):
         q_, kn_, vn_ = hin[li]
-        layers[li].step(q_, kn_, vn_, pos, n, out=hout[li], sel=sels[li])
+        layers[li].step(q_, kn_, vn_, pos, n, out=hout[li], sel=sels[li], host_inputs=True)
 
     zgraphs = []
     for li in range(n_layers):
@@ -474,8 +474,11 @@ def run_ours(args, cfg, world, rank, local):
                     "speedup_fier_vs_full": round(full_us / us_per_step, 3)},
         "e2e": {"value": round(e2e_us, 3), "unit": UNIT, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h,
-                "how": "fier_decode_step on pinned host buffers: the step kernel reads q/k_new/v_new from host "
-                       "memory and writes the output to host memory (zero-copy), one CUDA graph per layer rotation",
+                "how": "fier_decode_step_ex(FIER_STEP_HOST_INPUTS) on pinned host buffers: the one-launch step "
+                       "kernel reads q/k_new/v_new from host memory itself; the separate-kernel path first stages "
+                       "them into the workspace with one extra launch; the output is written to host memory "
+                       "(zero-copy); one CUDA graph per layer rotation",
+                "launches_per_step": layers[0].launches(pos + 1, n, host_inputs=True),
                 "dma_variant_us": round(e2e_dma_us, 3)},
         "clocks": sampler.summary(),
         "n_layers": n_layers,

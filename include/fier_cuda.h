@@ -48,7 +48,10 @@ extern "C" {
 #endif
 
 enum fier_status { FIER_OK = 0, FIER_EINVAL = 1, FIER_EDATA = 2, FIER_ECUDA = 3 };
-enum fier_dtype { FIER_F32 = 0, FIER_F16 = 1, FIER_BF16 = 2 };
+/* FIER_F64: the reference's own key type (KeyCache is an fp64 Matrix, core.hpp:24-68);
+ * accepted by fier_pack_keys, fier_append (bit-exact quantize of fp64 keys) and
+ * fier_exact_scores (the C++ drop-in's oracle / full policies) only. */
+enum fier_dtype { FIER_F32 = 0, FIER_F16 = 1, FIER_BF16 = 2, FIER_F64 = 3 };
 
 /* Shape of one layer's cache.  All fields are plain integers. */
 typedef struct fier_shape {
@@ -70,6 +73,12 @@ FIER_API size_t fier_params_bytes(const fier_shape* s);
 /* Exact accounted payload of one (sequence, kv head) index at `tokens`
  * (PackedKeys::payload_bytes, quant1bit.hpp:60-62). */
 FIER_API size_t fier_payload_bytes(int32_t tokens, int32_t dim, int32_t group);
+/* load_ratio_fier (quant1bit.hpp:176-184): exact estimation cost per channel against a
+ * 16-bit key cache, l code bits + ceil(l/g) * 2 * 16 parameter bits over l * 16 bits,
+ * as the unreduced bit counts of LoadRatio (numerator_bits, denominator_bits) and
+ * formula = (g divides l).  Reduce with gcd for LoadRatio::ratio().  Host-only. */
+FIER_API int fier_load_ratio_fier(int64_t tokens, int64_t group, int64_t* numerator_bits,
+                                  int64_t* denominator_bits, int32_t* formula);
 
 /* ---- K1: 1-bit key packer ---------------------------------------------------- */
 /* quantize (quant1bit.hpp:65-103) of tokens [0, tokens) of every (b, kv head).
@@ -98,6 +107,13 @@ FIER_API int fier_score(const fier_shape* s, const void* q, const uint32_t* bits
 FIER_API size_t fier_topk_workspace(int32_t rows, int32_t tokens, int32_t k);
 FIER_API int fier_topk(const float* scores, int32_t rows, int32_t tokens, int64_t ld, int32_t k,
               int32_t* sel, void* workspace, size_t workspace_bytes, void* stream);
+
+/* topk_oracle on fp64 scores (the reference's own ScoreVector type, core.hpp:75-79):
+ * exact on doubles that would tie after rounding to fp32.  One CTA per row, an exact
+ * radix select on order-preserving u64 keys; not a decode-path kernel (the C++
+ * drop-in's fp64 inputs).  Same tie rule and ascending output as fier_topk. */
+FIER_API int fier_topk_f64(const double* scores, int32_t rows, int32_t tokens, int64_t ld, int32_t k,
+                           int32_t* sel, void* stream);
 
 /* ---- K4: sparse attention over the selected rows ------------------------------ */
 /* gather_attention (core.hpp:152-179): out[b][h] = softmax(scale * q K[sel]^T) V[sel]
@@ -135,8 +151,11 @@ FIER_API int fier_full_attention(const fier_shape* s, const void* q, const void*
  * other shapes as append+score, Top-k and sparse-attention launches. */
 FIER_API size_t fier_decode_workspace(const fier_shape* s, int32_t tokens, int32_t n);
 FIER_API int64_t fier_step_scores_ld(int32_t tokens);
-/* Kernel launches fier_decode_step issues for this shape (1 = the fused kernel). */
-FIER_API int32_t fier_decode_step_launches(const fier_shape* s, int32_t tokens, int32_t n);
+/* Kernel launches fier_decode_step_ex issues for this shape and flags (1 = the fused
+ * kernel; the separate-kernel path adds one launch for FIER_STEP_HOST_INPUTS staging and
+ * one for RoPE when with_rope != 0).  fier_decode_step = flags 0, no rope. */
+FIER_API int32_t fier_decode_step_launches(const fier_shape* s, int32_t tokens, int32_t n, uint32_t flags,
+                                           int32_t with_rope);
 
 /* Rotary position embedding fused into the step (the KV write +
  * RoPE + append-pack that precedes scoring in a decode loop).  q (every q head) and
@@ -151,11 +170,27 @@ typedef struct fier_rope {
     int32_t rotary_dim;  /* rd: even, 2 <= rd <= min(dim, 128) */
     int32_t interleaved;
 } fier_rope;
-/* fier_decode_step with an optional rope (NULL: none); same workspace. */
+/* Flags of fier_decode_step_ex.
+ *  FIER_STEP_HOST_INPUTS: q / k_new / v_new live in pinned, mapped HOST memory.  The
+ *  separate-kernel path then stages them into the workspace with one launch first (one
+ *  PCIe round trip instead of one per CTA); the one-launch path reads them directly.
+ *  The caller states residency once (no per-step pointer queries, and the choice is
+ *  what a captured graph replays).
+ *  FIER_STEP_SEPARATE: run the separate-kernel path even where the one-launch cluster
+ *  kernel applies (same results; for A/B comparisons and tests). */
+enum fier_step_flags { FIER_STEP_HOST_INPUTS = 1, FIER_STEP_SEPARATE = 2 };
+/* Non-finite inputs of a step, OR-ed into *nonfinite (a device int the caller zeroes):
+ *  FIER_NONFINITE_KEY   -- the appended key row (after RoPE) or its open group holds a
+ *                          non-finite entry: "quantize: non-finite key entry" (quant1bit.hpp:68)
+ *  FIER_NONFINITE_QUERY -- the query does: its logits cannot be finite,
+ *                          "softmax: non-finite logit" (core.hpp:122). */
+enum fier_nonfinite { FIER_NONFINITE_KEY = 1, FIER_NONFINITE_QUERY = 2 };
+/* fier_decode_step with an optional rope (NULL: none), flags (fier_step_flags) and an
+ * optional device status word nonfinite (NULL: not checked); same workspace. */
 FIER_API int fier_decode_step_ex(const fier_shape* s, const void* q, const void* k_new, const void* v_new,
                         int32_t pos, void* K, void* V, uint32_t* bits, void* params, int32_t n,
-                        float scale, const fier_rope* rope, float* out, int32_t* sel, float* scores_out,
-                        void* workspace, size_t workspace_bytes, void* stream);
+                        float scale, const fier_rope* rope, uint32_t flags, int32_t* nonfinite, float* out,
+                        int32_t* sel, float* scores_out, void* workspace, size_t workspace_bytes, void* stream);
 FIER_API int fier_decode_step(const fier_shape* s, const void* q, const void* k_new, const void* v_new,
                      int32_t pos, void* K, void* V, uint32_t* bits, void* params, int32_t n,
                      float scale, float* out, int32_t* sel, float* scores_out, void* workspace,
@@ -245,7 +280,9 @@ FIER_API int fier_page_select(const float* page_scores, int32_t rows, int32_t to
 
 /* ---- recall / margin sweep diagnostics (evalharness.hpp) --------- */
 /* exact_scores (core.hpp:98-112): scores[B*Hq][ld] = q . k_i in fp64 (scaled: / sqrt(d)),
- * GQA as above; scores32 (may be NULL) receives the same rounded to fp32. */
+ * GQA as above; scores32 (may be NULL) receives the same rounded to fp32.  FIER_F64
+ * q and K (the reference's own types) are summed in the reference's channel order with
+ * unfused products: bit-identical to exact_scores. */
 FIER_API int fier_exact_scores(const fier_shape* s, const void* q, const void* K, int32_t tokens, int32_t scaled,
                       double* scores, float* scores32, int64_t ld, void* stream);
 /* margin_and_errors (evalharness.hpp:63-83) per row: report[rows][5] = (margin, max_err,

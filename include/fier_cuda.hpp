@@ -15,6 +15,10 @@
 //   fier::cuda::build_page_summaries(K, L)      build_page_summaries baselines.hpp:34-56
 //   fier::cuda::quest_select(q, K, ps, n, v)    quest_select      baselines.hpp:113-118
 //   fier::cuda::quest_select_quantized(q, pk, L, n) quest_select_quantized baselines.hpp:120-140
+//   fier::cuda::exact_scores(q, K, scaled)      exact_scores      core.hpp:98-112
+//   fier::cuda::select_for_policy(p, q, K, st)  select_for_policy retrieval.hpp:155-221
+//   fier::cuda::run_policy(p, q, K, V, st)      run_policy        retrieval.hpp:223-233
+//   fier::cuda::load_ratio_fier(l, g)           load_ratio_fier   quant1bit.hpp:176-184
 //
 // The functions are templates over the cache / index / result types and only use
 // the reference's member names (K.tokens(), K.dim(), K.data.data(), pk.code_words,
@@ -22,11 +26,14 @@
 // fier::cuda::types; next to the reference headers a caller names the reference's
 // own types, e.g. `fier::cuda::quantize<fier::PackedKeys>(K, fier::GroupSpec{32})`.
 //
-// Precision: the device path computes in fp32 on fp32 copies of the fp64 inputs
-// (exact for fp32-representable data) and keeps (s, z) as binary16, the on-disk
-// precision of the FIER format (io.hpp:205-211); the returned PackedKeys holds
-// those half-rounded values, so serialize_packed_keys() of it is byte-identical to
-// serialize_packed_keys(quantize(K)) of the reference.  Top-k ranks fp32 scores.
+// Precision: quantize packs the fp64 keys themselves on the device (FIER_F64: fp64
+// min/max/midpoint, bits against the unrounded fp64 z) and keeps (s, z) as binary16,
+// the on-disk precision of the FIER format (io.hpp:205-211); the returned PackedKeys
+// holds those half-rounded values, so serialize_packed_keys() of it is byte-identical
+// to serialize_packed_keys(quantize(K)) of the reference for any fp64 K.  topk_oracle
+// and exact_scores run in fp64 (bit-identical selections / scores).  approx_scores and
+// gather_attention compute in fp32 on fp32 copies of q, K, V (the decode path's
+// arithmetic): within 1e-3 / 1e-2 of the reference (BASELINE.json north star).
 #ifndef FIER_CUDA_HPP_
 #define FIER_CUDA_HPP_
 
@@ -90,10 +97,42 @@ struct RetrievalResult {
     uint64_t bytes_loaded_for_estimation = 0;
 };
 enum class QuestVariant { max_over_channels, sum_over_channels };  // baselines.hpp:28-31
+// retrieval.hpp:20 (same enumerator order: the drop-in reads the reference's enum by value)
+enum class PolicyKind { full, oracle, fier, quest, quest_quant, streaming_llm, h2o };
+struct BudgetPolicy {  // retrieval.hpp:36-45 (the fields the device policies read)
+    PolicyKind kind = PolicyKind::full;
+    std::size_t budget = 0;
+    std::size_t group_size = 32;
+    std::size_t page_size = 16;
+    QuestVariant variant = QuestVariant::sum_over_channels;
+};
+struct PolicySelection {  // retrieval.hpp:147-151
+    Selection selection;
+    ScoreVector est_scores;
+    uint64_t bytes_loaded = 0;
+};
+struct LoadRatio {  // quant1bit.hpp:162-171
+    long long numerator_bits = 0, denominator_bits = 1;
+    bool formula = true;
+};
 struct PageSummaries {  // baselines.hpp:16-29
     std::size_t page_size = 16, tokens = 0, dim = 0;
     Matrix max_vecs, min_vecs;
     std::size_t page_count() const { return max_vecs.rows(); }
+};
+struct SideState {  // retrieval.hpp:88-103: the side state select_for_policy reads
+    std::vector<std::pair<std::size_t, PackedKeys>> packed_by_group;
+    std::vector<std::pair<std::size_t, PageSummaries>> pages_by_size;
+    const PackedKeys& packed(std::size_t g) const {
+        for (const auto& e : packed_by_group)
+            if (e.first == g) return e.second;
+        throw std::invalid_argument("run_policy: missing packed keys in side state");
+    }
+    const PageSummaries& pages(std::size_t L) const {
+        for (const auto& e : pages_by_size)
+            if (e.first == L) return e.second;
+        throw std::invalid_argument("run_policy: missing page summaries in side state");
+    }
 };
 }  // namespace types
 
@@ -151,7 +190,7 @@ inline double half_to_double(uint16_t h) {  // exact widening (half.hpp:13-28)
     return sgn * std::ldexp((double)(m | 0x400), e - 25);
 }
 
-inline fier_shape shape(int B, int Hq, int Hkv, int cap, int d, int g) {
+inline fier_shape shape(int B, int Hq, int Hkv, int cap, int d, int g, int dtype = FIER_F32) {
     fier_shape s;
     s.batch = B;
     s.q_heads = Hq;
@@ -159,7 +198,7 @@ inline fier_shape shape(int B, int Hq, int Hkv, int cap, int d, int g) {
     s.capacity = cap;
     s.dim = d;
     s.group = g;
-    s.dtype = FIER_F32;
+    s.dtype = dtype;
     return s;
 }
 
@@ -191,18 +230,17 @@ inline void upload(const PK& pk, DevIndex& di) {  // host PackedKeys -> device l
 
 }  // namespace detail
 
-// quantize (quant1bit.hpp:65-103)
+// quantize (quant1bit.hpp:65-103): the fp64 keys are packed as they are (FIER_F64)
 template <typename PK = types::PackedKeys, typename KC, typename GS>
 PK quantize(const KC& K, const GS& spec) {
     if (spec.group_size < 1) throw std::invalid_argument("quantize: group size must be >= 1");
     if (K.tokens() == 0 || K.dim() == 0) throw std::invalid_argument("quantize: empty key cache");
     const std::size_t l = K.tokens(), d = K.dim(), g = spec.group_size;
-    const std::vector<float> kf = detail::to_f32(detail::mat_data(K), l * d);
-    detail::Dev<float> dk(kf.data(), kf.size());
+    detail::Dev<double> dk(detail::mat_data(K), l * d);
     detail::DevIndex di(l, d, g);
     detail::Dev<int32_t> flag(1);
     detail::cuda_check(cudaMemset(flag.p, 0, 4), "cudaMemset");
-    fier_shape s = detail::shape(1, 1, 1, (int)l, (int)d, (int)g);
+    fier_shape s = detail::shape(1, 1, 1, (int)l, (int)d, (int)g, FIER_F64);
     detail::check(fier_pack_keys(&s, dk.p, (int32_t)l, di.bits.p, di.params.p, flag.p, nullptr));
     detail::cuda_check(cudaDeviceSynchronize(), "quantize");
     if (flag.host()[0]) throw std::invalid_argument("quantize: non-finite key entry");
@@ -244,20 +282,47 @@ SV approx_scores(const Q& q, const PK& pk) {
     return out;
 }
 
-// topk_oracle (core.hpp:134-148): the k largest, ties to the lower index, ascending
+// topk_oracle (core.hpp:134-148): the k largest, ties to the lower index, ascending --
+// ranked on the fp64 scores themselves (fier_topk_f64)
 template <typename SEL = types::Selection, typename SV>
 SEL topk_oracle(const SV& scores, std::size_t k) {
     const std::size_t l = scores.values.size();
     if (k < 1 || k > l) throw std::invalid_argument("topk_oracle: k out of range");
-    const std::vector<float> sf = detail::to_f32(scores.values.data(), l);
-    detail::Dev<float> ds(sf.data(), l);
+    detail::Dev<double> ds(scores.values.data(), l);
     detail::Dev<int32_t> dsel(k);
-    detail::check(fier_topk(ds.p, 1, (int32_t)l, (int64_t)l, (int32_t)k, dsel.p, nullptr, 0, nullptr));
+    detail::check(fier_topk_f64(ds.p, 1, (int32_t)l, (int64_t)l, (int32_t)k, dsel.p, nullptr));
     const std::vector<int32_t> idx = dsel.host();
     SEL sel;
     sel.indices.assign(idx.begin(), idx.end());
     sel.budget = k;
     return sel;
+}
+
+// exact_scores (core.hpp:98-112): fp64 on the device in the reference's term order
+template <typename SV = types::ScoreVector, typename Q, typename KC>
+SV exact_scores(const Q& q, const KC& K, bool scaled = false) {
+    if (q.size() != K.dim()) throw std::invalid_argument("exact_scores: query length does not match key dim");
+    const std::size_t l = K.tokens(), d = K.dim();
+    detail::Dev<double> dk(detail::mat_data(K), l * d), dq(q.data(), d), ds(l);
+    fier_shape s = detail::shape(1, 1, 1, (int)l, (int)d, 1, FIER_F64);
+    detail::check(fier_exact_scores(&s, dq.p, dk.p, (int32_t)l, scaled ? 1 : 0, ds.p, nullptr, (int64_t)l, nullptr));
+    const std::vector<double> v = ds.host();
+    SV out;
+    out.values.assign(v.begin(), v.end());
+    return out;
+}
+
+// load_ratio_fier (quant1bit.hpp:176-184)
+template <typename LR = types::LoadRatio>
+LR load_ratio_fier(std::size_t l, std::size_t g) {
+    int64_t num = 0, den = 1;
+    int32_t formula = 1;
+    detail::check(fier_load_ratio_fier((int64_t)l, (int64_t)g, &num, &den, &formula));
+    LR r;
+    r.numerator_bits = num;
+    r.denominator_bits = den;
+    r.formula = formula != 0;
+    return r;
 }
 
 // gather_attention (core.hpp:152-179)
@@ -290,7 +355,7 @@ OUT gather_attention(const Q& q, const KC& K, const VC& V, const SEL& sel, bool 
 template <typename SEL = types::Selection, typename Q, typename PK>
 SEL fier_select(const Q& q, const PK& pk, std::size_t n) {
     if (n < 1 || n > pk.tokens) throw std::invalid_argument("fier_select: budget out of range");
-    return topk_oracle<SEL>(approx_scores(q, pk), n);
+    return ::fier::cuda::topk_oracle<SEL>(::fier::cuda::approx_scores(q, pk), n);
 }
 
 // fier_attend (retrieval.hpp:136-146)
@@ -299,9 +364,9 @@ RR fier_attend(const Q& q, const KC& K, const VC& V, const PK& pk, std::size_t n
     if (pk.tokens != K.tokens() || pk.dim != K.dim())
         throw std::invalid_argument("fier_attend: packed keys do not match cache");
     RR r;
-    r.est_scores = approx_scores<decltype(r.est_scores)>(q, pk);
-    r.selection = topk_oracle<decltype(r.selection)>(r.est_scores, n);
-    r.output = gather_attention<decltype(r.output)>(q, K, V, r.selection);
+    r.est_scores = ::fier::cuda::approx_scores<decltype(r.est_scores)>(q, pk);
+    r.selection = ::fier::cuda::topk_oracle<decltype(r.selection)>(r.est_scores, n);
+    r.output = ::fier::cuda::gather_attention<decltype(r.output)>(q, K, V, r.selection);
     r.bytes_loaded_for_estimation = pk.payload_bytes();
     return r;
 }
@@ -386,6 +451,73 @@ SEL quest_select_quantized(const Q& q, const PK& pk, std::size_t page_size, std:
     detail::check(fier_score(&s, dq.p, di.bits.p, di.params.p, (int32_t)l, ds.p, (int64_t)l, nullptr));
     detail::check(fier_page_mean(ds.p, 1, (int32_t)l, (int64_t)l, (int32_t)page_size, dp.p, (int64_t)P, nullptr));
     return detail::page_select<SEL>(dp, l, page_size, n);
+}
+
+// ---- policy dispatch (retrieval.hpp:155-233): the device-side policies ----
+//
+// select_for_policy's branches for the policies on the device path -- full, oracle,
+// fier (retrieval.hpp:177-183: the Fier index from state.packed(policy.group_size),
+// approx_scores -> topk_oracle, bytes = payload_bytes), quest and quest_quant --
+// with the reference's preconditions and messages.  streaming_llm and h2o are not on
+// the Fier path (SURVEY §8 out of scope) and throw.  PS / the policy / the side state
+// may be the reference's own types (PolicySelection, BudgetPolicy, SideState).
+template <typename PS = types::PolicySelection, typename POL, typename Q, typename KC, typename ST>
+PS select_for_policy(const POL& policy, const Q& q, const KC& K, const ST& state) {
+    const std::size_t l = K.tokens();
+    PS r;
+    const int kind = static_cast<int>(policy.kind);  // PolicyKind enumerator order, retrieval.hpp:20
+    if (kind == static_cast<int>(types::PolicyKind::full)) {  // pass-through: budget does not apply
+        r.selection.budget = l;
+        r.selection.indices.resize(l);
+        for (std::size_t i = 0; i < l; ++i) r.selection.indices[i] = i;
+        r.est_scores = ::fier::cuda::exact_scores<decltype(r.est_scores)>(q, K);
+        return r;
+    }
+    const std::size_t n = policy.budget;
+    if (n < 1 || n > l) throw std::invalid_argument("run_policy: budget out of range for cache");
+    switch (static_cast<types::PolicyKind>(kind)) {
+        case types::PolicyKind::oracle:
+            r.est_scores = ::fier::cuda::exact_scores<decltype(r.est_scores)>(q, K);
+            r.selection = ::fier::cuda::topk_oracle<decltype(r.selection)>(r.est_scores, n);
+            r.bytes_loaded = static_cast<uint64_t>(l) * K.dim() * 2;
+            break;
+        case types::PolicyKind::fier: {
+            const auto& pk = state.packed(policy.group_size);
+            r.est_scores = ::fier::cuda::approx_scores<decltype(r.est_scores)>(q, pk);
+            r.selection = ::fier::cuda::topk_oracle<decltype(r.selection)>(r.est_scores, n);
+            r.bytes_loaded = pk.payload_bytes();
+            break;
+        }
+        case types::PolicyKind::quest: {
+            const auto& ps = state.pages(policy.page_size);
+            r.selection = ::fier::cuda::quest_select<decltype(r.selection)>(q, K, ps, n, policy.variant);
+            r.bytes_loaded = static_cast<uint64_t>(ps.page_count()) * ps.dim * 4;
+            break;
+        }
+        case types::PolicyKind::quest_quant: {
+            const auto& pk = state.packed(policy.group_size);
+            r.selection = ::fier::cuda::quest_select_quantized<decltype(r.selection)>(q, pk, policy.page_size, n);
+            r.est_scores = ::fier::cuda::approx_scores<decltype(r.est_scores)>(q, pk);
+            r.bytes_loaded = pk.payload_bytes();
+            break;
+        }
+        default:
+            throw std::invalid_argument("run_policy: policy not on the device path (streaming_llm, h2o)");
+    }
+    return r;
+}
+
+// run_policy (retrieval.hpp:223-233): the selection, then gather_attention on it
+template <typename RR = types::RetrievalResult, typename POL, typename Q, typename KC, typename VC, typename ST>
+RR run_policy(const POL& policy, const Q& q, const KC& K, const VC& V, const ST& state) {
+    auto ps = ::fier::cuda::select_for_policy<types::PolicySelection>(policy, q, K, state);
+    RR r;
+    r.selection.indices = std::move(ps.selection.indices);
+    r.selection.budget = ps.selection.budget;
+    r.est_scores.values = std::move(ps.est_scores.values);
+    r.bytes_loaded_for_estimation = ps.bytes_loaded;
+    r.output = ::fier::cuda::gather_attention<decltype(r.output)>(q, K, V, r.selection);
+    return r;
 }
 
 }  // namespace cuda

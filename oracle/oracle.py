@@ -224,6 +224,8 @@ class Ref:
         L.ref_quantize_inmem.argtypes = [_dp, _sz, _sz, _sz, _u64p, _dp, _dp]
         L.ref_approx_scores_fier.argtypes = [_dp, _u8p, _sz, _dp]
         L.ref_topk.argtypes = [_dp, _sz, _sz, _i64p]
+        L.ref_load_ratio_fier.argtypes = [_sz, _sz, C.POINTER(C.c_longlong), C.POINTER(C.c_longlong),
+                                          C.POINTER(C.c_int)]
         L.ref_gather_attention.argtypes = [_dp, _dp, _dp, _sz, _sz, _i64p, _sz, C.c_int, _dp]
         L.ref_exact_scores.argtypes = [_dp, _dp, _sz, _sz, C.c_int, _dp]
         L.ref_fier_attend_fier.argtypes = [_dp, _dp, _dp, _sz, _sz, _u8p, _sz, _sz, _i64p, _dp, _dp,
@@ -283,6 +285,14 @@ class Ref:
         out = np.zeros(k, np.int64)
         self._check(self.lib.ref_topk(scores, scores.size, k, out))
         return out
+
+    def load_ratio_fier(self, l: int, g: int):
+        """load_ratio_fier (quant1bit.hpp:176-184): ((num_bits, den_bits), (num, den) reduced, formula)."""
+        bits = (C.c_longlong * 2)()
+        ratio = (C.c_longlong * 2)()
+        formula = C.c_int()
+        self._check(self.lib.ref_load_ratio_fier(l, g, bits, ratio, C.byref(formula)))
+        return (bits[0], bits[1]), (ratio[0], ratio[1]), bool(formula.value)
 
     def gather_attention(self, q, K, V, idx, scaled=True) -> np.ndarray:
         K, V = _c64(K), _c64(V)

@@ -75,6 +75,19 @@ extern "C" {
 const char* ref_last_error() { return g_err.c_str(); }
 
 uint16_t ref_double_to_half(double x) { return fier::double_to_half(x); }   // half.hpp:30
+// load_ratio_fier (quant1bit.hpp:176-184): the unreduced bit counts, the reduced ratio
+// (Rational, quant1bit.hpp:143-160) and the formula flag
+int ref_load_ratio_fier(size_t l, size_t g, long long* bits, long long* ratio, int* formula) {
+    return guard([&] {
+        const fier::LoadRatio r = fier::load_ratio_fier(l, g);
+        bits[0] = r.numerator_bits;
+        bits[1] = r.denominator_bits;
+        const fier::Rational q = r.ratio();
+        ratio[0] = q.num;
+        ratio[1] = q.den;
+        *formula = r.formula ? 1 : 0;
+    });
+}
 double ref_half_to_double(uint16_t h) { return fier::half_to_double(h); }   // half.hpp:13
 
 // quantize (quant1bit.hpp:65) -> serialize_packed_keys (io.hpp:197).

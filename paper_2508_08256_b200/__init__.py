@@ -9,6 +9,9 @@ fier_attend) on torch CUDA tensors.
 from . import _lib  # noqa: F401
 from .api import (  # noqa: F401
     DecodeLayer,
+    LoadRatio,
+    load_ratio_fier,
+    raise_nonfinite,
     PackedKeys,
     RetrievalResult,
     alloc_index,
@@ -34,5 +37,5 @@ __all__ = [
     "DecodeLayer", "PackedKeys", "RetrievalResult", "alloc_index", "append_token", "approx_scores",
     "fier_attend", "fier_select", "full_attention", "gather_attention", "load_cache_dump", "quantize",
     "save_cache_dump", "topk_oracle", "PageSummaries", "build_page_summaries", "quest_page_scores",
-    "quest_select", "quest_select_quantized", "select_by_page_scores",
+    "quest_select", "quest_select_quantized", "select_by_page_scores", "LoadRatio", "load_ratio_fier", "raise_nonfinite",
 ]

@@ -13,7 +13,9 @@ import os
 LIB_PATH = os.environ.get("FIER_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libfier_cuda.so")
 
 FIER_OK, FIER_EINVAL, FIER_EDATA, FIER_ECUDA = 0, 1, 2, 3
-FIER_F32, FIER_F16, FIER_BF16 = 0, 1, 2
+FIER_F32, FIER_F16, FIER_BF16, FIER_F64 = 0, 1, 2, 3
+FIER_STEP_HOST_INPUTS, FIER_STEP_SEPARATE = 1, 2
+FIER_NONFINITE_KEY, FIER_NONFINITE_QUERY = 1, 2
 
 # every symbol include/fier_cuda.h declares
 EXPORTS = (
@@ -27,6 +29,7 @@ EXPORTS = (
     "fier_index_export", "fier_index_import", "fier_kvd1_load", "fier_kvd1_store",
     "fier_quest_summaries", "fier_quest_page_scores", "fier_page_mean", "fier_page_select_workspace",
     "fier_page_select", "fier_exact_scores", "fier_margin_errors_workspace", "fier_margin_errors", "fier_overlap",
+    "fier_topk_f64", "fier_load_ratio_fier",
 )
 
 
@@ -65,6 +68,8 @@ _SIGS = {
     "fier_append": ([_SP, _vp, _vp, _vp, _vp, _i32, _vp, _vp, _vp, _vp], C.c_int),
     "fier_score": ([_SP, _vp, _vp, _vp, _i32, _vp, _i64, _vp], C.c_int),
     "fier_topk_workspace": ([_i32, _i32, _i32], _sz),
+    "fier_topk_f64": ([_vp, _i32, _i32, _i64, _i32, _vp, _vp], C.c_int),
+    "fier_load_ratio_fier": ([_i64, _i64, C.POINTER(_i64), C.POINTER(_i64), C.POINTER(_i32)], C.c_int),
     "fier_topk": ([_vp, _i32, _i32, _i64, _i32, _vp, _vp, _sz, _vp], C.c_int),
     "fier_sparse_attention_workspace": ([_SP, _i32], _sz),
     "fier_sparse_attention": ([_SP, _vp, _vp, _vp, _vp, _i32, _i32, C.c_float, _vp, _vp, _sz, _vp],
@@ -73,9 +78,9 @@ _SIGS = {
     "fier_full_attention": ([_SP, _vp, _vp, _vp, _i32, C.c_float, _vp, _vp, _sz, _vp], C.c_int),
     "fier_decode_workspace": ([_SP, _i32, _i32], _sz),
     "fier_step_scores_ld": ([_i32], _i64),
-    "fier_decode_step_launches": ([_SP, _i32, _i32], _i32),
+    "fier_decode_step_launches": ([_SP, _i32, _i32, C.c_uint32, _i32], _i32),
     "fier_decode_step_ex": ([_SP, _vp, _vp, _vp, _i32, _vp, _vp, _vp, _vp, _i32, C.c_float, C.POINTER(FierRope),
-                             _vp, _vp, _vp, _vp, _sz, _vp], C.c_int),
+                             C.c_uint32, _vp, _vp, _vp, _vp, _vp, _sz, _vp], C.c_int),
     "fier_decode_step": ([_SP, _vp, _vp, _vp, _i32, _vp, _vp, _vp, _vp, _i32, C.c_float, _vp, _vp,
                           _vp, _vp, _sz, _vp], C.c_int),
     "fier_sparse_attention_ragged": ([_SP, _vp, _vp, _vp, _vp, _vp, _i32, _i32, C.c_float, _vp, _vp, _vp,

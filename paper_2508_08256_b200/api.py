@@ -37,6 +37,8 @@ from . import _lib
 from ._lib import FierShape, check
 
 _DT = {torch.float32: _lib.FIER_F32, torch.float16: _lib.FIER_F16, torch.bfloat16: _lib.FIER_BF16}
+# fp64 keys (the reference's own KeyCache type) are accepted by quantize / append_token only
+_DT_KEYS = {**_DT, torch.float64: _lib.FIER_F64}
 
 
 def _stream() -> C.c_void_p:
@@ -52,9 +54,11 @@ def _require(ok: bool, msg: str) -> None:
         raise ValueError(msg)
 
 
-def _dtype_code(t: torch.Tensor) -> int:
-    _require(t.dtype in _DT, f"unsupported dtype {t.dtype}: expected float32, float16 or bfloat16")
-    return _DT[t.dtype]
+def _dtype_code(t: torch.Tensor, keys: bool = False) -> int:
+    table = _DT_KEYS if keys else _DT
+    _require(t.dtype in table, f"unsupported dtype {t.dtype}: expected float32, float16 or bfloat16"
+             + (" (or float64 keys)" if keys else ""))
+    return table[t.dtype]
 
 
 def _cuda(t: torch.Tensor, what: str) -> torch.Tensor:
@@ -176,6 +180,30 @@ class PackedKeys:
         return pk
 
 
+@dataclass(frozen=True)
+class LoadRatio:
+    """LoadRatio (quant1bit.hpp:162-171): exact bit counts of estimation vs a 16-bit key cache."""
+    numerator_bits: int
+    denominator_bits: int
+    formula: bool  # False when a short final group forces exact byte accounting
+
+    def ratio(self) -> Tuple[int, int]:
+        """Rational(numerator_bits, denominator_bits) reduced (quant1bit.hpp:143-160)."""
+        g = math.gcd(self.numerator_bits, self.denominator_bits)
+        return self.numerator_bits // g, self.denominator_bits // g
+
+    def value(self) -> float:
+        n, d = self.ratio()
+        return n / d
+
+
+def load_ratio_fier(l: int, g: int) -> LoadRatio:
+    """load_ratio_fier (quant1bit.hpp:176-184) through the C ABI (fier_load_ratio_fier)."""
+    num, den, formula = C.c_int64(), C.c_int64(), C.c_int32()
+    check(_lib.load().fier_load_ratio_fier(l, g, C.byref(num), C.byref(den), C.byref(formula)))
+    return LoadRatio(num.value, den.value, bool(formula.value))
+
+
 def alloc_index(batch, kv_heads, capacity, dim, group, device="cuda") -> PackedKeys:
     W, G = (dim + 31) // 32, (capacity + group - 1) // group
     bits = torch.zeros((batch, kv_heads, capacity, W), dtype=torch.int32, device=device)
@@ -199,7 +227,7 @@ def quantize(K: torch.Tensor, group_size: int = 32, tokens: Optional[int] = None
     _require(1 <= tokens <= cap, "quantize: empty key cache")
     pk = out or alloc_index(B, H, cap, d, group_size, K4.device)
     flag = torch.zeros(1, dtype=torch.int32, device=K4.device)
-    shape = make_shape(B, H, H, cap, d, group_size, _dtype_code(K4))
+    shape = make_shape(B, H, H, cap, d, group_size, _dtype_code(K4, keys=True))
     check(_lib.load().fier_pack_keys(C.byref(shape), _p(K4), tokens, _p(pk.bits), _p(pk.params),
                                      _p(flag), _stream()))
     if int(flag.item()) != 0:
@@ -214,7 +242,7 @@ def append_token(K: torch.Tensor, V: torch.Tensor, k_new: torch.Tensor, v_new: t
     K4, V4 = _as4(K), _as4(V)
     B, H, cap, d = K4.shape
     flag = torch.zeros(1, dtype=torch.int32, device=K4.device) if check_finite else None
-    shape = make_shape(B, H, H, cap, d, pk.group_size, _dtype_code(K4))
+    shape = make_shape(B, H, H, cap, d, pk.group_size, _dtype_code(K4, keys=True))
     check(_lib.load().fier_append(C.byref(shape), _p(K4), _p(V4), _p(k_new.contiguous()),
                                   _p(v_new.contiguous()), pos, _p(pk.bits), _p(pk.params), _p(flag),
                                   _stream()))
@@ -240,14 +268,20 @@ def approx_scores(q: torch.Tensor, pk: PackedKeys) -> torch.Tensor:
 
 
 def topk_oracle(scores: torch.Tensor, k: int) -> torch.Tensor:
-    """topk_oracle (core.hpp:134-148): int32 ascending indices [k] or [..., k]."""
+    """topk_oracle (core.hpp:134-148): int32 ascending indices [k] or [..., k].
+
+    float32 scores take the decode path's cluster select (fier_topk); float64 scores
+    (the reference's own ScoreVector type) the exact fp64 select (fier_topk_f64)."""
     s = _cuda(scores, "topk_oracle")
-    _require(s.dtype == torch.float32, "topk_oracle: scores must be float32")
+    _require(s.dtype in (torch.float32, torch.float64), "topk_oracle: scores must be float32 or float64")
     l = s.shape[-1]
     _require(1 <= k <= l, "topk_oracle: k out of range")
     rows = s.numel() // l
     sel = torch.empty(s.shape[:-1] + (k,), dtype=torch.int32, device=s.device)
-    check(_lib.load().fier_topk(_p(s), rows, l, l, k, _p(sel), None, 0, _stream()))
+    if s.dtype == torch.float64:
+        check(_lib.load().fier_topk_f64(_p(s), rows, l, l, k, _p(sel), _stream()))
+    else:
+        check(_lib.load().fier_topk(_p(s), rows, l, l, k, _p(sel), None, 0, _stream()))
     return sel
 
 
@@ -371,11 +405,17 @@ class DecodeLayer:
         return self._ws
 
     def step(self, q, k_new, v_new, pos: int, n: int, out=None, sel=None, scores_out=None,
-             scale: Optional[float] = None, rope: Optional[Tuple[float, int, bool]] = None):
+             scale: Optional[float] = None, rope: Optional[Tuple[float, int, bool]] = None,
+             host_inputs: bool = False, separate: bool = False,
+             nonfinite: Optional[torch.Tensor] = None):
         """fier_attend for a decode step: append token `pos`, score, select n, attend.
 
         rope = (base, rotary_dim, interleaved): rotate q and k_new by position `pos`
-        inside the step (fier_decode_step_ex; the cache stores the rotated k row)."""
+        inside the step (fier_decode_step_ex; the cache stores the rotated k row).
+        host_inputs: q / k_new / v_new are pinned host tensors (FIER_STEP_HOST_INPUTS).
+        separate: force the separate-kernel path (FIER_STEP_SEPARATE).
+        nonfinite: an int32 device tensor the step ORs FIER_NONFINITE_KEY (1) /
+        FIER_NONFINITE_QUERY (2) into; check it with ``raise_nonfinite``."""
         lib = _lib.load()
         tokens = pos + 1
         ws = self.workspace(tokens, n) if self._ws_key != (tokens, n) else self._ws
@@ -388,12 +428,20 @@ class DecodeLayer:
         if rope is not None:
             base, rd, inter = rope
             rp = C.byref(_lib.FierRope(float(base), int(rd), 1 if inter else 0))
+        flags = (_lib.FIER_STEP_HOST_INPUTS if host_inputs else 0) | (_lib.FIER_STEP_SEPARATE if separate else 0)
         check(lib.fier_decode_step_ex(C.byref(self.shape), _p(q), _p(k_new), _p(v_new), pos, _p(self.K),
-                                      _p(self.V), _p(self.pk.bits), _p(self.pk.params), n, scale, rp, _p(out),
-                                      _p(sel), _p(scores_out), _p(ws), ws.numel(), _stream()))
+                                      _p(self.V), _p(self.pk.bits), _p(self.pk.params), n, scale, rp, flags,
+                                      _p(nonfinite), _p(out), _p(sel), _p(scores_out), _p(ws), ws.numel(),
+                                      _stream()))
         self.pk.tokens = max(self.pk.tokens, tokens)
         self.tokens = max(self.tokens, tokens)
         return out, sel
+
+    def launches(self, tokens: int, n: int, host_inputs: bool = False, rope: bool = False,
+                 separate: bool = False) -> int:
+        """Kernel launches one step issues (fier_decode_step_launches)."""
+        flags = (_lib.FIER_STEP_HOST_INPUTS if host_inputs else 0) | (_lib.FIER_STEP_SEPARATE if separate else 0)
+        return int(_lib.load().fier_decode_step_launches(C.byref(self.shape), tokens, n, flags, 1 if rope else 0))
 
     def full_step(self, q, tokens: int, out=None, ws=None, scale: Optional[float] = None):
         """K0: full-KV decode attention over [0, tokens) (the baseline)."""
@@ -407,6 +455,17 @@ class DecodeLayer:
         check(lib.fier_full_attention(C.byref(self.shape), _p(q), _p(self.K), _p(self.V), tokens, scale,
                                       _p(out), _p(ws), ws.numel(), _stream()))
         return out
+
+
+def raise_nonfinite(flag: torch.Tensor) -> None:
+    """Raise the reference's error for a decode step's non-finite status word (a host sync):
+    "quantize: non-finite key entry" (quant1bit.hpp:68) or "softmax: non-finite logit"
+    (core.hpp:122)."""
+    v = int(flag.item())
+    if v & _lib.FIER_NONFINITE_KEY:
+        raise ValueError("quantize: non-finite key entry")
+    if v & _lib.FIER_NONFINITE_QUERY:
+        raise ValueError("softmax: non-finite logit")
 
 
 # ---- KVD1 cache dumps straight to/from the device (io.hpp:110-185) -----------------

@@ -100,6 +100,28 @@ def build_shim_test() -> str:
     return SHIM_BIN
 
 
+REF_INCLUDE = "/root/reference/proj/include"
+REF_SHIM_SRC = os.path.join(ROOT, "tests", "cpp", "ref_shim_test.cpp")
+REF_SHIM_BIN = os.path.join(ROOT, "tests", "cpp", "ref_shim_test")
+
+
+def build_ref_shim_test() -> str:
+    """The C++ drop-in compiled next to the reference's own headers (test infrastructure:
+    the checker of tests/test_capi.py::test_ref_shim_against_reference).  Built only where
+    /root/reference exists; the binary travels to the GPU box with the snapshot."""
+    build()
+    if not os.path.isdir(os.path.join(REF_INCLUDE, "fier")):
+        return REF_SHIM_BIN if os.path.exists(REF_SHIM_BIN) else ""
+    deps = (REF_SHIM_SRC, OUT, os.path.join(ROOT, "include", "fier_cuda.hpp"), os.path.join(ROOT, "include", "fier_cuda.h"))
+    if os.path.exists(REF_SHIM_BIN) and os.path.getmtime(REF_SHIM_BIN) > max(os.path.getmtime(f) for f in deps):
+        return REF_SHIM_BIN
+    subprocess.run([nvcc(), *ARCH, "-std=c++20", "-O2", "-Xcompiler", "-ffp-contract=off",
+                    "-I" + os.path.join(ROOT, "include"), "-I" + REF_INCLUDE, REF_SHIM_SRC,
+                    "-L" + PKG, "-lfier_cuda", "-Xlinker", "-rpath=$ORIGIN/../../paper_2508_08256_b200",
+                    "-o", REF_SHIM_BIN], check=True)
+    return REF_SHIM_BIN
+
+
 def dump_sass(path: str) -> None:
     cuobjdump = os.path.join(os.path.dirname(nvcc()), "cuobjdump")
     with open(path, "w") as f:

@@ -40,14 +40,15 @@ int full_dispatch(const fier_shape*, const void*, const void*, const void*, int,
                   cudaStream_t);
 size_t sparse_counter_offset(const fier_shape*, int);
 int append_score_dispatch(const fier_shape*, const void*, void*, void*, const void*, const void*, int,
-                          uint32_t*, void*, float*, int64_t, int*, int, cudaStream_t);
+                          uint32_t*, void*, float*, int64_t, int*, int, int32_t*, cudaStream_t);
 int fused_step_dispatch(const fier_shape*, const void*, const void*, const void*, int, void*, void*, uint32_t*,
-                        void*, int, float, const fier_rope*, float*, int32_t*, float*, int64_t, cudaStream_t);
+                        void*, int, float, const fier_rope*, float*, int32_t*, float*, int64_t, int32_t*,
+                        cudaStream_t);
 int rope_dispatch(const fier_shape*, const void*, const void*, int, const fier_rope*, void*, void*, cudaStream_t);
 bool fused_step_applies(const fier_shape*, int tokens);
 bool attn_fused_merge(const fier_shape*);
 
-static int check_shape(const fier_shape* s, const char* fn) {
+static int check_shape(const fier_shape* s, const char* fn, bool allow_f64 = false) {
     const std::string f(fn);
     if (!s) return fail(FIER_EINVAL, f + ": null shape");
     if (s->batch < 1 || s->q_heads < 1 || s->kv_heads < 1 || s->capacity < 1)
@@ -56,14 +57,16 @@ static int check_shape(const fier_shape* s, const char* fn) {
         return fail(FIER_EINVAL, f + ": q_heads must be a multiple of kv_heads");
     if (s->dim < 1 || s->dim > 1024) return fail(FIER_EINVAL, f + ": head dim must be in [1, 1024]");
     if (s->group < 1) return fail(FIER_EINVAL, "quantize: group size must be >= 1");
-    if (s->dtype != FIER_F32 && s->dtype != FIER_F16 && s->dtype != FIER_BF16)
+    if (s->dtype == FIER_F64 && !allow_f64)
+        return fail(FIER_EINVAL, f + ": FIER_F64 keys are accepted by fier_pack_keys / fier_append only");
+    if (s->dtype != FIER_F32 && s->dtype != FIER_F16 && s->dtype != FIER_BF16 && s->dtype != FIER_F64)
         return fail(FIER_EINVAL, f + ": unknown dtype");
     return FIER_OK;
 }
 
 static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
-static size_t elem_size(int dtype) { return dtype == FIER_F32 ? 4 : 2; }
+static size_t elem_size(int dtype) { return dtype == FIER_F64 ? 8 : dtype == FIER_F32 ? 4 : 2; }
 
 static size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
 
@@ -78,12 +81,12 @@ const char* fier_last_error(void) { return g_last_error.c_str(); }
 int fier_version(void) { return 1; }
 
 size_t fier_bits_bytes(const fier_shape* s) {
-    if (check_shape(s, "fier_bits_bytes")) return 0;
+    if (check_shape(s, "fier_bits_bytes", true)) return 0;
     return (size_t)s->batch * s->kv_heads * s->capacity * ((s->dim + 31) / 32) * 4;
 }
 
 size_t fier_params_bytes(const fier_shape* s) {
-    if (check_shape(s, "fier_params_bytes")) return 0;
+    if (check_shape(s, "fier_params_bytes", true)) return 0;
     return (size_t)s->batch * s->kv_heads * ceil_div(s->capacity, s->group) * s->dim * 4;
 }
 
@@ -92,9 +95,20 @@ size_t fier_payload_bytes(int32_t tokens, int32_t dim, int32_t group) {
     return (size_t)tokens * ((dim + 7) / 8) + (size_t)dim * ceil_div(tokens, group) * 4;
 }
 
+int fier_load_ratio_fier(int64_t tokens, int64_t group, int64_t* numerator_bits, int64_t* denominator_bits,
+                         int32_t* formula) {
+    FIER_REQUIRE(tokens >= 1 && group >= 1, "load_ratio_fier: l and g must be >= 1");
+    FIER_REQUIRE(numerator_bits && denominator_bits && formula, "load_ratio_fier: null output");
+    const int64_t groups = (tokens + group - 1) / group;
+    *numerator_bits = tokens + groups * 2 * 16;
+    *denominator_bits = tokens * 16;
+    *formula = tokens % group == 0 ? 1 : 0;
+    return FIER_OK;
+}
+
 int fier_pack_keys(const fier_shape* s, const void* K, int32_t tokens, uint32_t* bits, void* params,
                    int32_t* nonfinite, void* stream) {
-    if (int rc = check_shape(s, "quantize")) return rc;
+    if (int rc = check_shape(s, "quantize", true)) return rc;
     FIER_REQUIRE(tokens >= 1, "quantize: empty key cache");
     FIER_REQUIRE(tokens <= s->capacity, "quantize: tokens exceed cache capacity");
     FIER_REQUIRE(K && bits && params, "quantize: null buffer");
@@ -103,7 +117,7 @@ int fier_pack_keys(const fier_shape* s, const void* K, int32_t tokens, uint32_t*
 
 int fier_append(const fier_shape* s, void* K, void* V, const void* k_new, const void* v_new,
                 int32_t pos, uint32_t* bits, void* params, int32_t* nonfinite, void* stream) {
-    if (int rc = check_shape(s, "fier_append")) return rc;
+    if (int rc = check_shape(s, "fier_append", true)) return rc;
     FIER_REQUIRE(pos >= 0 && pos < s->capacity, "fier_append: position outside cache capacity");
     FIER_REQUIRE(K && V && k_new && v_new && bits && params, "fier_append: null buffer");
     return append_dispatch(s, K, V, k_new, v_new, pos, bits, params, nonfinite, nullptr, 0,
@@ -194,15 +208,6 @@ static size_t rope_bytes(const fier_shape* s) {
     return align_up((size_t)s->batch * (s->q_heads + 2 * s->kv_heads) * s->dim * elem_size(s->dtype));
 }
 
-static bool host_resident(const void* p) {
-    cudaPointerAttributes a;
-    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
-        cudaGetLastError();
-        return false;
-    }
-    return a.type == cudaMemoryTypeHost;
-}
-
 // One launch copies the step's inputs out of (pinned, mapped) host memory, so the separate
 // kernels' CTAs read them from HBM instead of each paying its own PCIe round trips.
 __global__ void stage_inputs_kernel(const uint8_t* a, uint8_t* da, int64_t na, const uint8_t* b, uint8_t* db,
@@ -232,19 +237,24 @@ int fier_decode_step(const fier_shape* s, const void* q, const void* k_new, cons
                      int32_t pos, void* K, void* V, uint32_t* bits, void* params, int32_t n,
                      float scale, float* out, int32_t* sel, float* scores_out, void* workspace,
                      size_t workspace_bytes, void* stream) {
-    return fier_decode_step_ex(s, q, k_new, v_new, pos, K, V, bits, params, n, scale, nullptr, out, sel, scores_out,
-                               workspace, workspace_bytes, stream);
+    return fier_decode_step_ex(s, q, k_new, v_new, pos, K, V, bits, params, n, scale, nullptr, 0u, nullptr, out, sel,
+                               scores_out, workspace, workspace_bytes, stream);
 }
 
 int fier_decode_step_ex(const fier_shape* s, const void* q, const void* k_new, const void* v_new,
                         int32_t pos, void* K, void* V, uint32_t* bits, void* params, int32_t n,
-                        float scale, const fier_rope* rope, float* out, int32_t* sel, float* scores_out,
-                        void* workspace, size_t workspace_bytes, void* stream) {
+                        float scale, const fier_rope* rope, uint32_t flags, int32_t* nonfinite, float* out,
+                        int32_t* sel, float* scores_out, void* workspace, size_t workspace_bytes, void* stream) {
     if (int rc = check_shape(s, "fier_decode_step")) return rc;
     const int32_t tokens = pos + 1;
     FIER_REQUIRE(pos >= 0 && pos < s->capacity, "fier_append: position outside cache capacity");
     FIER_REQUIRE(n >= 1 && n <= tokens, "fier_select: budget out of range");
     FIER_REQUIRE(q && k_new && v_new && K && V && bits && params && out && sel, "fier_decode_step: null buffer");
+    FIER_REQUIRE(aligned16(K) && aligned16(V) && aligned16(bits) && aligned16(params),
+                 "fier_decode_step: K, V and the index buffers must be 16-byte aligned");
+    FIER_REQUIRE((int64_t)s->batch * s->q_heads <= 65535, "fier_decode_step: batch * q_heads exceeds 65535 rows");
+    FIER_REQUIRE((flags & ~(uint32_t)(FIER_STEP_HOST_INPUTS | FIER_STEP_SEPARATE)) == 0,
+                 "fier_decode_step: unknown flags");
     FIER_REQUIRE(workspace && workspace_bytes >= fier_decode_workspace(s, tokens, n),
                  "fier_decode_step: workspace too small");
     if (rope) {
@@ -256,9 +266,11 @@ int fier_decode_step_ex(const fier_shape* s, const void* q, const void* k_new, c
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     const int64_t ld = fier_step_scores_ld(tokens);
     // MHA, d = 128: the whole step (RoPE included) in one cluster launch (step_fused.cu)
-    const int frc = fused_step_dispatch(s, q, k_new, v_new, pos, K, V, bits, params, n, scale, rope, out, sel,
-                                        scores_out, ld, st);
-    if (frc >= 0) return frc;
+    if (!(flags & FIER_STEP_SEPARATE)) {
+        const int frc = fused_step_dispatch(s, q, k_new, v_new, pos, K, V, bits, params, n, scale, rope, out, sel,
+                                            scores_out, ld, nonfinite, st);
+        if (frc >= 0) return frc;
+    }
     uint8_t* ws = static_cast<uint8_t*>(workspace);
     float* scores = scores_out ? scores_out : reinterpret_cast<float*>(ws);
     uint8_t* attn_ws = ws + align_up((size_t)s->batch * s->q_heads * ld * sizeof(float));
@@ -268,7 +280,7 @@ int fier_decode_step_ex(const fier_shape* s, const void* q, const void* k_new, c
     const size_t qb = (size_t)s->batch * s->q_heads * s->dim * elem_size(s->dtype);
     const size_t kb = (size_t)s->batch * s->kv_heads * s->dim * elem_size(s->dtype);
     // (with RoPE the rope kernel already moves q / k_new out of host memory once)
-    if (!rope && (host_resident(q) || host_resident(k_new) || host_resident(v_new))) {
+    if (!rope && (flags & FIER_STEP_HOST_INPUTS)) {
         const int64_t words = (int64_t)(qb + 2 * kb) / 16;
         const int blocks = (int)std::min<int64_t>(num_sms(), std::max<int64_t>(1, ceil_div(words, 256)));
         stage_inputs_kernel<<<blocks, 256, 0, st>>>(static_cast<const uint8_t*>(q), rws, (int64_t)qb,
@@ -287,19 +299,21 @@ int fier_decode_step_ex(const fier_shape* s, const void* q, const void* k_new, c
         k_new = k_rot;
     }
     int rc = append_score_dispatch(s, q, K, V, k_new, v_new, pos, bits, params, scores, ld, counters,
-                                   s->batch * s->q_heads, st);
+                                   s->batch * s->q_heads, nonfinite, st);
     if (rc) return rc;
     rc = topk_dispatch(scores, s->batch * s->q_heads, tokens, ld, n, sel, st);
     if (rc) return rc;
     return sparse_dispatch(s, q, K, V, sel, n, tokens, scale, out, attn_ws, true, st, nullptr, nullptr);
 }
 
-int32_t fier_decode_step_launches(const fier_shape* s, int32_t tokens, int32_t n) {
+int32_t fier_decode_step_launches(const fier_shape* s, int32_t tokens, int32_t n, uint32_t flags,
+                                  int32_t with_rope) {
     if (check_shape(s, "fier_decode_step") || tokens < 1 || n < 1 || n > tokens) return 0;
-    if (fused_step_applies(s, tokens)) return 1;
-    // append+score, Top-k, sparse attention (+ a separate LSE merge on the generic attention path;
-    // + the RoPE kernel when fier_decode_step_ex gets a rope)
-    return attn_fused_merge(s) ? 3 : 4;
+    if (!(flags & FIER_STEP_SEPARATE) && fused_step_applies(s, tokens)) return 1;
+    // append+score, Top-k, sparse attention (+ a separate LSE merge on the generic attention path)
+    int launches = attn_fused_merge(s) ? 3 : 4;
+    if (with_rope) return launches + 1;  // the RoPE kernel (it also reads host-resident inputs once)
+    return launches + ((flags & FIER_STEP_HOST_INPUTS) ? 1 : 0);  // staging of host-resident inputs
 }
 
 // ---- host-side FIER conversion (io.hpp:197-277) ------------------------------------

@@ -70,6 +70,12 @@ __device__ __forceinline__ uint32_t float_key(float f) {
     return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
 }
 
+// Key of a score in a Top-k row: NaN ranks below every number (key 1; key 0 marks an
+// empty slot past the row end), so a row of NaN scores still selects k tokens, the
+// lowest indices first.  (The reference's std::sort on NaN is undefined; the decode step
+// flags a non-finite query separately, FIER_NONFINITE_QUERY.)
+__device__ __forceinline__ uint32_t score_key(float f) { return isnan(f) ? 1u : float_key(f); }
+
 // ---- async bulk copies (TMA bulk engine) + mbarriers ----------------------------
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));

@@ -44,6 +44,25 @@ __global__ void exact_scores_kernel(const T* __restrict__ q, const T* __restrict
     }
 }
 
+// fp64 keys and query (the reference's own types): one thread per token, the reference's
+// sequential channel order with unfused multiply and add (core.hpp:105-109), so the
+// scores are the reference's bit for bit
+__global__ void exact_scores_f64_kernel(const double* __restrict__ q, const double* __restrict__ K, int Hq, int hpg,
+                                        int cap, int d, int tokens, double inv, double* __restrict__ out,
+                                        float* __restrict__ out32, int64_t ld) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    const int qrow = blockIdx.y;
+    if (t >= tokens) return;
+    const int64_t kvrow = (int64_t)(qrow / Hq) * (Hq / hpg) + (qrow % Hq) / hpg;
+    const double* k = K + (kvrow * cap + t) * d;
+    const double* qr = q + (int64_t)qrow * d;
+    double acc = 0.0;
+    for (int j = 0; j < d; ++j) acc = __dadd_rn(acc, __dmul_rn(qr[j], k[j]));
+    const double v = __dmul_rn(acc, inv);
+    out[(int64_t)qrow * ld + t] = v;
+    if (out32) out32[(int64_t)qrow * ld + t] = (float)v;
+}
+
 // per row: margin from the k+1 largest (sel), then the four error sums (block reduction)
 __global__ void margin_errors_kernel(const double* __restrict__ exact, const float* __restrict__ est, int64_t ld,
                                      int tokens, const int32_t* __restrict__ top, int k1,
@@ -160,7 +179,11 @@ int fier_exact_scores(const fier_shape* s, const void* q, const void* K, int32_t
     const double inv = scaled ? 1.0 / std::sqrt((double)s->dim) : 1.0;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     const dim3 grid((unsigned)ceil_div(tokens, 8), (unsigned)rows);
-    if (s->dtype == FIER_BF16)
+    if (s->dtype == FIER_F64)
+        exact_scores_f64_kernel<<<dim3((unsigned)ceil_div(tokens, 128), (unsigned)rows), 128, 0, st>>>(
+            static_cast<const double*>(q), static_cast<const double*>(K), s->q_heads, hpg, s->capacity, s->dim,
+            tokens, inv, scores, scores32, ld);
+    else if (s->dtype == FIER_BF16)
         exact_scores_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(q),
                                                                  static_cast<const __nv_bfloat16*>(K), s->q_heads, hpg,
                                                                  s->capacity, s->dim, tokens, inv, scores, scores32, ld);

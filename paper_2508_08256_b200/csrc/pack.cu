@@ -3,7 +3,8 @@
 // Replaces quantize (reference quant1bit.hpp:65-103).  One CTA per
 // (group, kv head, sequence); warp w owns channels [32w, 32w+32), lane = channel.
 //   * min/max scanned sequentially over the group's tokens in the input dtype
-//     widened exactly to fp64, first-seen wins ties (std::min/std::max at
+//     widened exactly to fp64 (fp64 keys -- the reference's own KeyCache type,
+//     core.hpp:24-68 -- are taken as they are), first-seen wins ties (std::min/std::max at
 //     quant1bit.hpp:85-89 -- matters for the sign of zero),
 //   * z = (mx+mn)/2, s = (mx-mn)/2 in fp64 (:90-93), stored RNE to binary16
 //     with cvt.rn.f16.f64 (= double_to_half, half.hpp:30-61),
@@ -90,6 +91,7 @@ int pack_dispatch(const fier_shape* s, const void* K, int32_t tokens, uint32_t* 
         case FIER_F32: return launch_pack<float>(s, K, tokens, bits, params, nonfinite, st);
         case FIER_F16: return launch_pack<__half>(s, K, tokens, bits, params, nonfinite, st);
         case FIER_BF16: return launch_pack<__nv_bfloat16>(s, K, tokens, bits, params, nonfinite, st);
+        case FIER_F64: return launch_pack<double>(s, K, tokens, bits, params, nonfinite, st);
     }
     return fail(FIER_EINVAL, "fier_pack_keys: unknown dtype");
 }
@@ -105,6 +107,8 @@ int append_dispatch(const fier_shape* s, void* K, void* V, const void* k_new, co
         case FIER_BF16:
             return launch_append<__nv_bfloat16>(s, K, V, k_new, v_new, pos, bits, params,
                                                 nonfinite, zero_words, zero_n, st);
+        case FIER_F64:
+            return launch_append<double>(s, K, V, k_new, v_new, pos, bits, params, nonfinite, zero_words, zero_n, st);
     }
     return fail(FIER_EINVAL, "fier_append: unknown dtype");
 }

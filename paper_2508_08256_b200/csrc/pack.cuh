@@ -8,20 +8,35 @@ namespace fier_cuda {
 
 constexpr int kPackThreads = 128;  // 4 warps; warp w packs channel slices w, w+4, ...
 
+// Arithmetic type of the packer: 16/32-bit keys are exact in fp32; fp64 keys (the
+// reference's own KeyCache type) stay fp64 end to end.
+template <typename T>
+struct PackVal {
+    using type = float;
+    __device__ static float get(T x) { return to_f32(x); }
+};
+template <>
+struct PackVal<double> {
+    using type = double;
+    __device__ static double get(double x) { return x; }
+};
+__device__ __forceinline__ bool pack_finite(float x) { return isfinite(x); }
+__device__ __forceinline__ bool pack_finite(double x) { return isfinite(x); }
+
 // Values of one 32-token chunk of this lane's channel, loaded together (one
 // memory latency per chunk instead of one per token).  bf16/fp16/fp32 are
 // exact in fp32; they are widened to fp64 for the arithmetic below.  Token
 // tnew (the row a decode-time append is storing right now) takes the value
 // xnew, read from the appended row itself, so the group's loads do not wait
 // behind the store (the loaded copy of that row is discarded).
-template <typename T>
+template <typename T, typename VT = typename PackVal<T>::type>
 __device__ __forceinline__ void load_chunk(const T* Kseq, int d, int c, bool valid,
-                                           int tc, int cnt, float (&v)[32], float xnew, int tnew) {
+                                           int tc, int cnt, VT (&v)[32], VT xnew, int tnew) {
 #pragma unroll
     for (int i = 0; i < 32; ++i) {
         // read-only path: the only row this launch writes (tnew) is stored after the
         // re-pack, and its loaded copy is discarded
-        const float x = (valid && i < cnt) ? to_f32(__ldg(Kseq + (int64_t)(tc + i) * d + c)) : 0.f;
+        const VT x = (valid && i < cnt) ? PackVal<T>::get(__ldg(Kseq + (int64_t)(tc + i) * d + c)) : VT(0);
         v[i] = tc + i == tnew ? xnew : x;
     }
 }
@@ -38,11 +53,13 @@ __device__ __forceinline__ void pack_group(const T* Kseq,  // no restrict: appen
     const bool valid = c < d;
     const int t0 = gi * g;
     const int t1 = min(t0 + g, t_end);  // short final group (quant1bit.hpp:84)
-    float v[32];
-    const float xnew = (nrow && valid) ? to_f32(nrow[c]) : 0.f;
-    // min/max on the exact fp32 values (== their fp64 widenings), sequential with
-    // std::min/std::max semantics: a tie keeps the first-seen value (+0 vs -0).
-    float mn = 0.f, mx = 0.f;
+    using VT = typename PackVal<T>::type;
+    VT v[32];
+    const VT xnew = (nrow && valid) ? PackVal<T>::get(nrow[c]) : VT(0);
+    // min/max on the exact values (fp32 holds every 16/32-bit key exactly, == its fp64
+    // widening), sequential with std::min/std::max semantics: a tie keeps the
+    // first-seen value (+0 vs -0).
+    VT mn = 0, mx = 0;
     bool bad = false;
     for (int tc = t0; tc < t1; tc += 32) {
         const int cnt = min(32, t1 - tc);
@@ -50,8 +67,8 @@ __device__ __forceinline__ void pack_group(const T* Kseq,  // no restrict: appen
 #pragma unroll
         for (int i = 0; i < 32; ++i) {
             if (i < cnt) {
-                const float x = v[i];
-                bad |= !isfinite(x);
+                const VT x = v[i];
+                bad |= !pack_finite(x);
                 if (tc == t0 && i == 0) {
                     mn = mx = x;
                 } else {
@@ -65,10 +82,15 @@ __device__ __forceinline__ void pack_group(const T* Kseq,  // no restrict: appen
     const double z = ((double)mx + (double)mn) / 2.0;
     const double s = ((double)mx - (double)mn) / 2.0;
     if (valid) sz_seq[(int64_t)gi * d + c] = __halves2half2(__double2half(s), __double2half(z));
-    if (bad && nonfinite) atomicExch(nonfinite, 1);
-    // x >= z (fp64) <=> x >= zc for fp32 x, zc = the smallest float >= z.
-    float zc = __double2float_rn(z);
-    if ((double)zc < z) zc = nextafterf(zc, INFINITY);
+    if (bad && nonfinite) atomicOr(nonfinite, 1);  // FIER_NONFINITE_KEY
+    // x >= z (fp64) <=> x >= zc for fp32 x, zc = the smallest float >= z (fp64 keys: z).
+    VT zc;
+    if constexpr (sizeof(VT) == 8) {
+        zc = z;
+    } else {
+        zc = __double2float_rn(z);
+        if ((double)zc < z) zc = nextafterf(zc, INFINITY);
+    }
     const bool all_one = (s == 0.0);
     // pass 2: one ballot per token -> the word of (token, 32 channels); for
     // g <= 32 the chunk is still in registers.

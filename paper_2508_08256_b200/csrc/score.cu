@@ -41,7 +41,21 @@ struct AppendArgs {  // K == nullptr: no fused append
     int pos;
     int* zero_words;
     int zero_n;
+    int32_t* nonfinite;  // FIER_NONFINITE_KEY / _QUERY (may be null)
 };
+
+// The appending CTA of a (sequence, kv head) flags a non-finite query of its heads
+// ("softmax: non-finite logit", core.hpp:122): warp 0's lanes hold every channel.
+template <int HPG>
+__device__ __forceinline__ void flag_query(const float (&qv)[HPG][4], int32_t* nonfinite) {
+    if (!nonfinite || (threadIdx.x >> 5) != 0) return;
+    bool bad = false;
+#pragma unroll
+    for (int hh = 0; hh < HPG; ++hh)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) bad |= !isfinite(qv[hh][i]);
+    if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(nonfinite, 2);
+}
 
 __device__ __forceinline__ uint4 ldg_cg(const void* p) {
     uint4 v;
@@ -158,7 +172,8 @@ __global__ void __launch_bounds__(kScoreWarps * 32) score128_kernel(
             kr = static_cast<const T*>(ap.k_new)[seq * D + threadIdx.x];
             vr = static_cast<const T*>(ap.v_new)[seq * D + threadIdx.x];
         }
-        pack_group<T>(Kseq, D, 4, g, ap.pos / g, ap.pos + 1, bseq, zseq, nullptr,
+        flag_query<HPG>(qv, ap.nonfinite);
+        pack_group<T>(Kseq, D, 4, g, ap.pos / g, ap.pos + 1, bseq, zseq, ap.nonfinite,
                       static_cast<const T*>(ap.k_new) + seq * D, ap.pos);
         if (own) {
             Kseq[(int64_t)ap.pos * D + threadIdx.x] = kr;
@@ -202,7 +217,7 @@ template <typename T>
 __global__ void score_generic_kernel(const T* __restrict__ q, const uint32_t* __restrict__ bits,
                                      const __half2* __restrict__ sz, int cap, int G, int hkv, int hq,
                                      int tokens, int d, int W, int g, float* __restrict__ scores,
-                                     int64_t ld) {
+                                     int64_t ld, int32_t* nonfinite) {
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
     const int h = blockIdx.y, b = blockIdx.z;
     if (t >= tokens) return;
@@ -216,6 +231,11 @@ __global__ void score_generic_kernel(const T* __restrict__ q, const uint32_t* __
         const float2 p = __half22float2(prow[j]);
         const bool bit = (brow[j >> 5] >> (j & 31)) & 1u;
         acc += to_f32(qp[j]) * ((bit ? p.x : -p.x) + p.y);
+    }
+    if (nonfinite && t == 0 && !isfinite(acc)) {  // one thread per q head checks its query
+        bool bad = false;
+        for (int j = 0; j < d; ++j) bad |= !isfinite(to_f32(qp[j]));
+        if (bad) atomicOr(nonfinite, 2);
     }
     scores[((int64_t)b * hq + h) * ld + t] = acc;
 }
@@ -244,25 +264,16 @@ static int launch_fast(const fier_shape* s, const void* q, const uint32_t* bits,
 bool score_mma_ok(const fier_shape* s);
 int score_mma_dispatch(const fier_shape* s, const void* q, const uint32_t* bits, const void* params, int tokens,
                        float* scores, int64_t ld, void* K, void* V, const void* k_new, const void* v_new, int pos,
-                       int* zero_words, int zero_n, cudaStream_t st);
-
-// FIER_SCORE_KERNEL=cuda_core selects the CUDA-core kernel (A/B measurements only)
-static bool use_cuda_core_scorer() {
-    static const bool v = [] {
-        const char* e = getenv("FIER_SCORE_KERNEL");
-        return e && std::string(e) == "cuda_core";
-    }();
-    return v;
-}
+                       int* zero_words, int zero_n, int32_t* nonfinite, cudaStream_t st);
 
 template <typename T>
 static int launch_score(const fier_shape* s, const void* q, const uint32_t* bits, const void* params,
                         int tokens, float* scores, int64_t ld, const AppendArgs& ap, cudaStream_t st) {
     const int hpg = s->q_heads / s->kv_heads;
     // MHA: the CUDA-core kernel is still ahead of the tensor-core one (ncu, profiles/)
-    if (score_mma_ok(s) && hpg > 1 && !use_cuda_core_scorer())
+    if (score_mma_ok(s) && hpg > 1)
         return score_mma_dispatch(s, q, bits, params, tokens, scores, ld, ap.K, ap.V, ap.k_new, ap.v_new, ap.pos,
-                                  ap.zero_words, ap.zero_n, st);
+                                  ap.zero_words, ap.zero_n, ap.nonfinite, st);
     if (s->dim == 128 && s->group % 32 == 0 && (hpg == 1 || hpg == 2 || hpg == 4 || hpg == 8)) {
         switch (hpg) {
             case 1: return launch_fast<T, 1>(s, q, bits, params, tokens, scores, ld, ap, st);
@@ -273,7 +284,7 @@ static int launch_score(const fier_shape* s, const void* q, const uint32_t* bits
     }
     if (ap.K) {  // generic shapes: separate append launch first
         const int rc = append_dispatch(s, ap.K, ap.V, ap.k_new, ap.v_new, ap.pos, const_cast<uint32_t*>(bits),
-                                       const_cast<void*>(params), nullptr, ap.zero_words, ap.zero_n, st);
+                                       const_cast<void*>(params), ap.nonfinite, ap.zero_words, ap.zero_n, st);
         if (rc) return rc;
     }
     const int W = (s->dim + 31) / 32;
@@ -282,7 +293,7 @@ static int launch_score(const fier_shape* s, const void* q, const uint32_t* bits
     score_generic_kernel<T><<<grid, 128, 0, st>>>(static_cast<const T*>(q), bits,
                                                  static_cast<const __half2*>(params), s->capacity, G,
                                                  s->kv_heads, s->q_heads, tokens, s->dim, W, s->group,
-                                                 scores, ld);
+                                                 scores, ld, ap.K ? ap.nonfinite : nullptr);
     return check_launch("fier_score");
 }
 
@@ -298,7 +309,7 @@ static int score_typed(const fier_shape* s, const void* q, const uint32_t* bits,
 
 int score_dispatch(const fier_shape* s, const void* q, const uint32_t* bits, const void* params, int tokens,
                    float* scores, int64_t ld, cudaStream_t st) {
-    const AppendArgs none = {nullptr, nullptr, nullptr, nullptr, 0, nullptr, 0};
+    const AppendArgs none = {nullptr, nullptr, nullptr, nullptr, 0, nullptr, 0, nullptr};
     return score_typed(s, q, bits, params, tokens, scores, ld, none, st);
 }
 
@@ -306,8 +317,8 @@ int score_dispatch(const fier_shape* s, const void* q, const uint32_t* bits, con
 // tokens [0, pos] -- zero_words (the attention counters) are cleared on the way.
 int append_score_dispatch(const fier_shape* s, const void* q, void* K, void* V, const void* k_new,
                           const void* v_new, int pos, uint32_t* bits, void* params, float* scores,
-                          int64_t ld, int* zero_words, int zero_n, cudaStream_t st) {
-    const AppendArgs ap = {K, V, k_new, v_new, pos, zero_words, zero_n};
+                          int64_t ld, int* zero_words, int zero_n, int32_t* nonfinite, cudaStream_t st) {
+    const AppendArgs ap = {K, V, k_new, v_new, pos, zero_words, zero_n, nonfinite};
     return score_typed(s, q, bits, params, pos + 1, scores, ld, ap, st);
 }
 

@@ -54,16 +54,12 @@ struct AppendArgs2 {  // K == nullptr: no fused append
     int* zero_words;
     int zero_n;
     int rebalance;  // sealed slabs fewer per warp of an appending CTA
+    int32_t* nonfinite;  // FIER_NONFINITE_KEY / _QUERY (may be null)
 };
 
-// FIER_MMA_REBALANCE overrides the default (measurement knob)
-static int mma_rebalance() {
-    static const int v = [] {
-        const char* e = getenv("FIER_MMA_REBALANCE");
-        return e ? atoi(e) : 6;
-    }();
-    return v;
-}
+// sealed slabs fewer per warp of an appending CTA (C3 sweep, K2: 0 -> 75.3 us,
+// 6 -> 71.6 us, 8-12 -> 73.2 us)
+constexpr int kMmaRebalance = 6;
 
 // k-slot (0..127, = 16 * k-step + k) -> channel and exponent of its A value
 __host__ __device__ constexpr int kslot_i(int ks) { return 2 * (ks >> 4) + ((ks & 15) >= 8 ? 1 : 0); }
@@ -309,7 +305,13 @@ __global__ void __launch_bounds__(kMmaWarps * 32) score_mma_kernel(const T* __re
                 kr = static_cast<const T*>(ap.k_new)[(int64_t)seq * 128 + threadIdx.x];
                 vr = static_cast<const T*>(ap.v_new)[(int64_t)seq * 128 + threadIdx.x];
             }
-            pack_group<T>(Kseq, 128, 4, g, ap.pos >> (5 + lg), ap.pos + 1, bseq, zseq, nullptr,
+            if (ap.nonfinite && threadIdx.x < 32) {  // the query heads of this kv head
+                bool bad = false;
+                for (int i = threadIdx.x; i < HPG * 128; i += 32)
+                    bad |= !isfinite(to_f32(q[((int64_t)b * hq + h * HPG) * 128 + i]));
+                if (__any_sync(0xffffffffu, bad) && threadIdx.x == 0) atomicOr(ap.nonfinite, 2);
+            }
+            pack_group<T>(Kseq, 128, 4, g, ap.pos >> (5 + lg), ap.pos + 1, bseq, zseq, ap.nonfinite,
                           static_cast<const T*>(ap.k_new) + (int64_t)seq * 128, ap.pos);
             if (own) {
                 Kseq[(int64_t)ap.pos * 128 + threadIdx.x] = kr;
@@ -445,8 +447,8 @@ static int mma_typed(const fier_shape* s, const void* q, const uint32_t* bits, c
 
 int score_mma_dispatch(const fier_shape* s, const void* q, const uint32_t* bits, const void* params, int tokens,
                        float* scores, int64_t ld, void* K, void* V, const void* k_new, const void* v_new, int pos,
-                       int* zero_words, int zero_n, cudaStream_t st) {
-    const AppendArgs2 ap = {K, V, k_new, v_new, pos, zero_words, zero_n, mma_rebalance()};
+                       int* zero_words, int zero_n, int32_t* nonfinite, cudaStream_t st) {
+    const AppendArgs2 ap = {K, V, k_new, v_new, pos, zero_words, zero_n, kMmaRebalance, nonfinite};
     switch (s->dtype) {
         case FIER_F32: return mma_typed<float>(s, q, bits, params, tokens, scores, ld, ap, st);
         case FIER_F16: return mma_typed<__half>(s, q, bits, params, tokens, scores, ld, ap, st);

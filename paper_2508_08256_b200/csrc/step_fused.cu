@@ -128,6 +128,7 @@ struct FsArgs {
     int pos, tokens, cap, G, hq, g, g_shift, k, kpt;  // g_shift = log2(g) or -1
     float scale_log2;
     RopeTable rope;  // rd = 0: no rotary embedding
+    int32_t* nonfinite;  // FIER_NONFINITE_KEY / _QUERY (may be null)
 };
 
 // The degenerate-row path, out of line: its code would otherwise sit between the hot
@@ -149,7 +150,10 @@ __device__ __noinline__ void fused_fallback_select(cg::cluster_group& cluster, c
 template <typename T>
 __global__ void __launch_bounds__(kFsThreads, 1) step_fused_kernel(const FsArgs a) {
     constexpr int D = kFsD;
-    constexpr int PF = 4;  // slabs in flight per warp
+#ifndef FIER_FS_PF
+#define FIER_FS_PF 4
+#endif
+    constexpr int PF = FIER_FS_PF;  // slabs in flight per warp
     cg::cluster_group cluster = cg::this_cluster();
     const int rank = (int)cluster.block_rank();
     const int nct = (int)cluster.num_blocks();
@@ -186,6 +190,9 @@ __global__ void __launch_bounds__(kFsThreads, 1) step_fused_kernel(const FsArgs 
         const T* qh = static_cast<const T*>(a.q) + (int64_t)row * kFsD;
         // rotated in fp32, rounded to the cache dtype like the rotated k row (rope.cuh)
         qrot[tid] = to_f32(T(rope_channel(a.rope, tid, [&](int j) { return to_f32(qh[j]); })));
+        // the query's logits cannot be finite ("softmax: non-finite logit", core.hpp:122)
+        if (a.nonfinite && rank == 0 && __any_sync(0xffffffffu, !isfinite(qrot[tid])) && (tid & 31) == 0)
+            atomicOr(a.nonfinite, 2);
     }
     __syncthreads();
     asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
@@ -205,6 +212,8 @@ __global__ void __launch_bounds__(kFsThreads, 1) step_fused_kernel(const FsArgs 
         const T* kn = static_cast<const T*>(a.k_new) + seq * D;
         const T kv = T(rope_channel(a.rope, tid, [&](int j) { return to_f32(kn[j]); }));
         const T vv = static_cast<const T*>(a.v_new)[seq * D + tid];
+        // "quantize: non-finite key entry" (quant1bit.hpp:68) for the appended row
+        if (a.nonfinite && __any_sync(0xffffffffu, !isfinite(to_f32(kv))) && (tid & 31) == 0) atomicOr(a.nonfinite, 1);
         pack_open_group<T>(Kseq, D, a.g, a.pos / a.g, a.pos + 1, bseq, zseq, to_f32(kv), a.pos);
         Kseq[(int64_t)a.pos * D + tid] = kv;  // after the re-pack: its loads do not queue behind this store
         Vseq[(int64_t)a.pos * D + tid] = vv;
@@ -248,7 +257,7 @@ __global__ void __launch_bounds__(kFsThreads, 1) step_fused_kernel(const FsArgs 
             __syncwarp();
             const float sc = nibble_score(tab, bw);
             if (t < a.tokens) {
-                key = isnan(sc) ? 0u : float_key(sc);
+                key = score_key(sc);
                 if (srow) srow[t] = sc;
             }
         }
@@ -276,6 +285,34 @@ __global__ void __launch_bounds__(kFsThreads, 1) step_fused_kernel(const FsArgs 
         }
     }
     uint4 pb[PF], bb[PF];  // register ring: (s, z) and bit rows of the next PF slabs
+    if (cnt == kFsMaxKpt && a.g_shift >= 0 && s0 + 32 * (start + cnt) <= a.tokens) {
+        // full slabs only: compile-time trip count, no per-slab bounds checks
+        const uint32_t* bw0 = bseq + (int64_t)(s0 + 32 * start + lane) * 4;
+        const __half2* zw0 = zseq + (int64_t)((s0 + 32 * start) >> a.g_shift) * D + 4 * lane;
+        auto ld = [&](int j, uint4& p, uint4& bw) {
+            p = ld_cg16(zw0 + (int64_t)((32 * j) >> a.g_shift) * D);
+            bw = ld_cg16(bw0 + (int64_t)j * 128);
+        };
+#pragma unroll
+        for (int u = 0; u < PF; ++u) ld(u, pb[u], bb[u]);
+        for (int j0 = 0; j0 < kFsMaxKpt; j0 += PF) {
+#pragma unroll
+            for (int u = 0; u < PF; ++u) {
+                const int j = j0 + u;
+                const uint4 p = pb[u], bw = bb[u];
+                if (j + PF < kFsMaxKpt) ld(j + PF, pb[u], bb[u]);
+                const uint32_t tab = tab0 + (u & 1) * kFsLutBytes;
+                build_nibble_table(tab, p, qv);
+                __syncwarp();
+                const float sc = nibble_score(tab, bw);
+                const uint32_t key = score_key(sc);
+                if (srow) srow[s0 + 32 * (start + j) + lane] = sc;
+                keys_s[32 * (start + j) + lane] = key;
+                rx_count(S, key);
+            }
+        }
+        cnt = 0;
+    }
 #pragma unroll
     for (int u = 0; u < PF; ++u)
         if (u < cnt) load(start + u, pb[u], bb[u]);
@@ -415,14 +452,6 @@ __global__ void __launch_bounds__(kFsThreads, 1) step_fused_kernel(const FsArgs 
 
 // ---- host side -------------------------------------------------------------------
 
-static bool fused_disabled() {  // FIER_STEP=unfused: the separate-kernel path (A/B measurements)
-    static const bool v = [] {
-        const char* e = getenv("FIER_STEP");
-        return e && std::string(e) == "unfused";
-    }();
-    return v;
-}
-
 template <typename T>
 static int launch_fused(int cluster, int rows, const FsArgs& args, cudaStream_t st) {
     auto kern = step_fused_kernel<T>;
@@ -471,15 +500,16 @@ static bool fused_shape_ok(const fier_shape* s) {
 
 bool fused_step_applies(const fier_shape* s, int tokens) {
     int cluster = 0, kpt = 0;
-    return !fused_disabled() && fused_shape_ok(s) && s->batch * s->q_heads <= 65535 &&
+    return fused_shape_ok(s) && s->batch * s->q_heads <= 65535 &&
            fused_plan(s->batch * s->q_heads, tokens, s->group, &cluster, &kpt);
 }
 
 // Returns -1 when the shape is not covered (the caller runs the separate kernels).
 int fused_step_dispatch(const fier_shape* s, const void* q, const void* k_new, const void* v_new, int pos, void* K,
                         void* V, uint32_t* bits, void* params, int n, float scale, const fier_rope* rope,
-                        float* out, int32_t* sel, float* scores_out, int64_t ld, cudaStream_t st) {
-    if (fused_disabled() || !fused_shape_ok(s)) return -1;
+                        float* out, int32_t* sel, float* scores_out, int64_t ld, int32_t* nonfinite,
+                        cudaStream_t st) {
+    if (!fused_shape_ok(s)) return -1;
     const int tokens = pos + 1, rows = s->batch * s->q_heads;
     if (rows > 65535) return -1;
     int cluster = 0, kpt = 0;
@@ -507,6 +537,7 @@ int fused_step_dispatch(const fier_shape* s, const void* q, const void* k_new, c
     args.kpt = kpt;
     args.scale_log2 = scale * kLog2e;
     args.rope = rope_table(rope, pos);
+    args.nonfinite = nonfinite;
     if (s->dtype == FIER_BF16) return launch_fused<__nv_bfloat16>(cluster, rows, args, st);
     return launch_fused<__half>(cluster, rows, args, st);
 }

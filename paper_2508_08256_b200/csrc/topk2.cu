@@ -35,7 +35,7 @@ __global__ void __launch_bounds__(kT2Threads, 2) topk2_kernel(const float* __res
     for (int j = 0; j < KPT; ++j) {
         const int p = wbase + 32 * j + lane;
         const float v = p < cnt ? srow[s0 + p] : __int_as_float(0x7fffffff);
-        key[j] = isnan(v) ? 0u : float_key(v);
+        key[j] = p < cnt ? score_key(v) : 0u;  // 0: empty slot past the row end
         if (isfinite(v)) {
             mn = fminf(mn, v);
             mx = fmaxf(mx, v);
@@ -73,7 +73,7 @@ __global__ void __launch_bounds__(kT2Threads, 2) topk2s_kernel(const float* __re
     for (int j = 0; j < kpt; ++j) {
         const int p = wbase + 32 * j + lane;
         const float v = p < cnt ? srow[s0 + p] : __int_as_float(0x7fffffff);
-        keys_s[p] = isnan(v) ? 0u : float_key(v);
+        keys_s[p] = p < cnt ? score_key(v) : 0u;  // 0: empty slot past the row end
         if (isfinite(v)) {
             mn = fminf(mn, v);
             mx = fmaxf(mx, v);
@@ -147,10 +147,7 @@ int topk2_dispatch(const float* scores, int rows, int tokens, int64_t ld, int k,
     int c = 1;
     // grow the cluster until the grid covers the chip (or slices reach 8 keys per thread),
     // then until the slice fits the 32 registers per thread
-    static const int max_c = [] {  // FIER_TOPK_CLUSTER caps the first growth step (tuning only)
-        const char* e = getenv("FIER_TOPK_CLUSTER");
-        return e ? atoi(e) : 4;
-    }();
+    constexpr int max_c = 4;  // cap of the first growth step (K3: cluster 4/8 sweeps)
     while (c < max_c && (int64_t)rows * c < 2 * num_sms() && ceil_div(tokens, c) > 8 * kT2Threads) c *= 2;
     while (c < kT2MaxCluster && ceil_div(tokens, c) > 32 * kT2Threads) c *= 2;
     const int64_t slice = ceil_div(tokens, c);
@@ -161,11 +158,6 @@ int topk2_dispatch(const float* scores, int rows, int tokens, int64_t ld, int k,
     if (kpt <= 4) return launch_t2<4>(c, rows, st, scores, tokens, ld, k, 4 * kT2Threads, sel);
     if (kpt <= 8) return launch_t2<8>(c, rows, st, scores, tokens, ld, k, 8 * kT2Threads, sel);
     if (kpt <= 16) return launch_t2<16>(c, rows, st, scores, tokens, ld, k, 16 * kT2Threads, sel);
-    static const bool regs32 = [] {  // FIER_TOPK2_REGS32=1: the register-key kernel (A/B only)
-        const char* e = getenv("FIER_TOPK2_REGS32");
-        return e && atoi(e) != 0;
-    }();
-    if (regs32) return launch_t2<32>(c, rows, st, scores, tokens, ld, k, 32 * kT2Threads, sel);
     return launch_t2s(c, rows, st, scores, tokens, ld, k, 32, sel);
 }
 

@@ -48,7 +48,8 @@ struct TlPublished {
     int32_t cidx[kTlCtaCand];
 };
 
-__device__ __forceinline__ uint32_t tl_key(float v) { return isnan(v) ? 0u : float_key(v); }
+// key of position i of a row ending at s1 (0: empty slot past the end)
+__device__ __forceinline__ uint32_t tl_key(float v, int i, int s1) { return i < s1 ? score_key(v) : 0u; }
 
 constexpr int kTlDepth = 8;  // tiles of loads in flight per thread (64 KB per SM)
 
@@ -71,10 +72,10 @@ __device__ __forceinline__ void tl_stream(const float* srow, int s0, int s1, F&&
 #pragma unroll
         for (int u = 0; u < kTlDepth; ++u) {
             const int i = t0 + u * kTlTile + 4 * threadIdx.x;
-            f(tl_key(v[u].x), i);
-            f(tl_key(v[u].y), i + 1);
-            f(tl_key(v[u].z), i + 2);
-            f(tl_key(v[u].w), i + 3);
+            f(tl_key(v[u].x, i, s1), i);
+            f(tl_key(v[u].y, i + 1, s1), i + 1);
+            f(tl_key(v[u].z, i + 2, s1), i + 2);
+            f(tl_key(v[u].w, i + 3, s1), i + 3);
         }
     }
 }
@@ -128,7 +129,8 @@ __device__ __forceinline__ void tl_emit(const float* srow, int s0, int s1, uint3
         float4 v = vv[0];
 #pragma unroll
         for (int w = 1; w < DEP; ++w) v = u == w ? vv[w] : v;
-        const uint32_t kk[4] = {tl_key(v.x), tl_key(v.y), tl_key(v.z), tl_key(v.w)};
+        const uint32_t kk[4] = {tl_key(v.x, i, s1), tl_key(v.y, i + 1, s1), tl_key(v.z, i + 2, s1),
+                                tl_key(v.w, i + 3, s1)};
         uint32_t tot = 0, eq_pre = 0;
         if constexpr (RANKED) {
             uint32_t neq = 0;

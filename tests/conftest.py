@@ -54,3 +54,21 @@ def cuda():
     from paper_2508_08256_b200 import _lib
     _lib.load()  # raises if the library is missing: no fallback
     return torch.device("cuda:0")
+
+
+SCORE_TOL = 1e-3  # |gpu - ref| <= 1e-3 * max(1, |ref|)  (BASELINE.json north star)
+
+
+def check_selection(gpu_sel, ref_scores, n, port, min_recall=0.999):
+    """The north-star selection bar against topk_oracle of the REFERENCE's scores: every
+    index the two selections disagree on lies within score tolerance of the reference's
+    threshold (a tie within 1e-3), and recall >= min_recall (evalharness.hpp:25-34)."""
+    ref_sel = port.topk(ref_scores, n)
+    T = ref_scores[ref_sel].min()
+    diff = np.setxor1d(np.asarray(gpu_sel, np.int64), ref_sel)
+    tol = 2 * SCORE_TOL * np.maximum(1.0, np.abs(ref_scores[diff]))
+    far = diff[np.abs(ref_scores[diff] - T) > tol]
+    assert far.size == 0, f"selection differs beyond score tolerance at {far[:8]} (T={T})"
+    rec = port.recall(np.asarray(gpu_sel, np.int64), ref_sel)
+    assert rec >= min_recall or diff.size <= 2, f"recall {rec} < {min_recall}"
+    return rec

@@ -208,3 +208,23 @@ def test_cpp_shim_matches_oracle(cuda, port, tmp_path):
     bufq = port.quantize_fier(KQ, g)
     est_q = port.approx_scores_fier(q, bufq)
     assert np.array_equal(qq, port.select_by_page_scores(port.page_mean(est_q, 16), 4096, 16, 300))
+
+
+@pytest.mark.parametrize("l,g", [(4096, 32), (4096, 128), (4096, 256), (4096, 1), (100, 32), (1, 1), (33, 32),
+                                 (131072, 32), (1048577, 32), (7, 1000)])
+def test_load_ratio_fier_matches_reference(l, g):
+    """fier_load_ratio_fier == the reference's load_ratio_fier (quant1bit.hpp:176-184) on exact
+    bit counts, the reduced Rational and the formula flag (acceptance_main.cpp:66-109: 0.125,
+    0.078125, 0.0703125 at g = 32, 128, 256; short groups force exact accounting)."""
+    import paper_2508_08256_b200 as F
+    from oracle.oracle import Ref, REF_SO
+    r = F.load_ratio_fier(l, g)
+    if os.path.exists(REF_SO):
+        bits, ratio, formula = Ref().load_ratio_fier(l, g)
+        assert (r.numerator_bits, r.denominator_bits) == bits
+        assert r.ratio() == ratio and r.formula == formula
+    expect = {(4096, 32): 0.125, (4096, 128): 0.078125, (4096, 256): 0.0703125}
+    if (l, g) in expect:
+        assert r.value() == expect[(l, g)] and r.formula
+    with pytest.raises(ValueError, match="load_ratio_fier: l and g must be >= 1"):
+        F.load_ratio_fier(0, g)

@@ -8,8 +8,6 @@ exactly topk_oracle of the GPU's own scores, the output within 1e-2 of
 gather_attention on that selection.
 """
 import os
-import subprocess
-import sys
 
 import numpy as np
 import pytest
@@ -27,7 +25,7 @@ def score_err(gpu, ref):
     return np.max(np.abs(gpu - ref) / np.maximum(1.0, np.abs(ref)))
 
 
-def run_step(cuda, B, H, cap, pos, n, g, dtype, seed=5, K=None):
+def run_step(cuda, B, H, cap, pos, n, g, dtype, seed=5, K=None, separate=False):
     import paper_2508_08256_b200 as F
     torch.manual_seed(seed)
     dt, d = TDT[dtype], 128
@@ -40,7 +38,7 @@ def run_step(cuda, B, H, cap, pos, n, g, dtype, seed=5, K=None):
     vn = torch.randn(B, H, d, device=cuda).to(dt)
     ld = pos + 1 + (-(pos + 1)) % 32
     scores = torch.empty(B, H, ld, device=cuda)
-    out, sel = layer.step(q, kn, vn, pos, n, scores_out=scores)
+    out, sel = layer.step(q, kn, vn, pos, n, scores_out=scores, separate=separate)
     torch.cuda.synchronize()
     return layer, q, kn, vn, out, sel, scores
 
@@ -130,22 +128,9 @@ def test_fused_step_repeated_decode(cuda, port):
         assert layer.pk.to_fier(0, h) == port.quantize_fier(Kc[0, h, :pos + 1], g)
 
 
-_UNFUSED = r"""
-import sys, numpy as np, torch
-sys.path.insert(0, {root!r}); sys.path.insert(0, {root!r} + "/tests")
-from test_step_fused_gpu import run_step, check
-from oracle.oracle import Port
-dev = torch.device("cuda:0")
-r = run_step(dev, 1, 4, 9000, 8500, 935, 32, "bf16")
-check(Port(), r[0], r[1], r[2], r[4], r[5], r[6], 8500, 935, 32)
-print("unfused ok")
-"""
-
-
-def test_unfused_step_path_still_matches(cuda):
-    """FIER_STEP=unfused forces the separate-kernel path (score -> top-k -> attention)
-    for the same MHA shape: it must stay correct since it serves A/B measurements."""
-    env = dict(os.environ, FIER_STEP="unfused")
-    r = subprocess.run([sys.executable, "-c", _UNFUSED.format(root=ROOT)], env=env, capture_output=True,
-                       text=True, timeout=600)
-    assert r.returncode == 0 and "unfused ok" in r.stdout, r.stdout + r.stderr
+def test_separate_step_path_still_matches(cuda, port):
+    """FIER_STEP_SEPARATE forces the separate-kernel path (score -> top-k -> attention) for
+    the same MHA shape: it must stay correct since it serves A/B measurements."""
+    r = run_step(cuda, 1, 4, 9000, 8500, 935, 32, "bf16", separate=True)
+    assert r[0].launches(8501, 935, separate=True) == 3 and r[0].launches(8501, 935) == 1
+    check(port, r[0], r[1], r[2], r[4], r[5], r[6], 8500, 935, 32)

@@ -15,6 +15,7 @@
 #include <cstdio>
 #include <vector>
 #include <algorithm>
+#include <cstdlib>
 
 #include "nibble.cuh"
 #include "common.cuh"
@@ -36,7 +37,7 @@ __global__ void __launch_bounds__(NT, 1) probe(const uint32_t* bits, const __hal
     const uint32_t tab0 = base + warp * 2 * kNibTableBytes;
     uint32_t* run = reinterpret_cast<uint32_t*>(sm + 16 * 2 * kNibTableBytes) + wbase;
     uint32_t* hist = reinterpret_cast<uint32_t*>(sm + 16 * 2 * kNibTableBytes + NT * KPT * 4);
-    if (MODE == 6) {
+    if (MODE >= 6) {
         for (int i = threadIdx.x; i < 4096; i += NT) hist[i] = 0;
         __syncthreads();
     }
@@ -98,13 +99,15 @@ __global__ void __launch_bounds__(NT, 1) probe(const uint32_t* bits, const __hal
                 }
                 run[32 * j + lane] = __float_as_uint(sc);
                 if (MODE == 6) atomicAdd(hist + (float_key(sc) >> 20), 1u);
+                if (MODE == 7 && (j & 7) == 0) atomicAdd(hist + (float_key(sc) >> 20), 1u);
+                if (MODE == 8) { const uint32_t kk = float_key(sc) >> 20; const uint32_t m = __match_any_sync(~0u, kk); if ((__ffs(m) - 1) == lane) atomicAdd(hist + kk, (uint32_t)__popc(m)); }
             }
         }
     }
     __syncthreads();
     if (MODE != 0)
         for (int j = 0; j < KPT; ++j) x ^= run[32 * j + lane];
-    if (MODE == 6) x ^= hist[threadIdx.x];
+    if (MODE >= 6) x ^= hist[threadIdx.x];
     if (x == 0x12345678u) out[0] = 1.f;
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -122,10 +125,13 @@ __global__ void flush(const uint4* p, size_t n, float* out) {
     if (acc == 0x12345) out[1] = acc;
 }
 
+static int g_cluster = 0, g_smem = 0;
+
 template <int MODE, int PF>
 float run(const uint32_t* bits, const __half2* sz, const float* q, float* out, const uint4* fl, size_t fn) {
     const int smem = 16 * 2 * kNibTableBytes + NT * KPT * 4 + 4096 * 4;
-    cudaFuncSetAttribute(probe<MODE, PF>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (g_smem < smem) g_smem = smem;
+    cudaFuncSetAttribute(probe<MODE, PF>, cudaFuncAttributeMaxDynamicSharedMemorySize, g_smem);
     cudaEvent_t a, b;
     cudaEventCreate(&a);
     cudaEventCreate(&b);
@@ -135,7 +141,22 @@ float run(const uint32_t* bits, const __half2* sz, const float* q, float* out, c
         unsigned long long init[2] = {~0ull, 0ull};
         cudaMemcpy(reinterpret_cast<unsigned long long*>(out) + 8, init, 16, cudaMemcpyHostToDevice);
         cudaEventRecord(a);
-        probe<MODE, PF><<<128, NT, smem>>>(bits, sz, q, out);
+        if (g_cluster) {
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3(128);
+            cfg.blockDim = dim3(NT);
+            cfg.dynamicSmemBytes = g_smem;
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeClusterDimension;
+            at[0].val.clusterDim.x = g_cluster;
+            at[0].val.clusterDim.y = 1;
+            at[0].val.clusterDim.z = 1;
+            cfg.attrs = at;
+            cfg.numAttrs = 1;
+            cudaLaunchKernelEx(&cfg, probe<MODE, PF>, bits, sz, q, out);
+        } else {
+            probe<MODE, PF><<<128, NT, g_smem>>>(bits, sz, q, out);
+        }
         cudaEventRecord(b);
         cudaEventSynchronize(b);
         float ms;
@@ -151,7 +172,9 @@ float run(const uint32_t* bits, const __half2* sz, const float* q, float* out, c
     return ds[3];
 }
 
-int main() {
+int main(int argc, char** argv) {
+    if (argc > 1) g_cluster = atoi(argv[1]);
+    if (argc > 2) g_smem = atoi(argv[2]);
     const size_t nb = (size_t)H * L * 4, nz = (size_t)H * G * D;
     uint32_t* bits;
     __half2* sz;
@@ -175,6 +198,8 @@ int main() {
     auto rep = [&](const char* name, float us) {
         printf("%-34s %8.2f us  %7.0f GB/s\n", name, us, bytes / us / 1e3);
     };
+    for (int pass = 0; pass < 2; ++pass) {
+    printf("pass %d\n", pass);
     rep("mode0 loads only PF=4", run<0, 4>(bits, sz, q, out, fl, fn));
     rep("mode0 loads only PF=8", run<0, 8>(bits, sz, q, out, fl, fn));
     rep("mode1 full PF=4", run<1, 4>(bits, sz, q, out, fl, fn));
@@ -185,6 +210,9 @@ int main() {
     rep("mode4 lookups only", run<4, 4>(bits, sz, q, out, fl, fn));
     rep("mode5 lookups as ALU", run<5, 4>(bits, sz, q, out, fl, fn));
     rep("mode6 full + digit histogram", run<6, 4>(bits, sz, q, out, fl, fn));
+    rep("mode7 full + 1/8 sampled histogram", run<7, 4>(bits, sz, q, out, fl, fn));
+    rep("mode8 full + match_any aggregated hist", run<8, 4>(bits, sz, q, out, fl, fn));
+    }
     cudaError_t e = cudaGetLastError();
     printf("status: %s\n", cudaGetErrorString(e));
     return 0;
