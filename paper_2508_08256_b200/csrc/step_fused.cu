@@ -20,7 +20,7 @@
 //            of 32 table reads, one per nibble of its 128-bit row: per nibble one
 //            PRMT (address), one LDS, one FADD -- ~3.5 lane-instructions per 4
 //            bits instead of ~2.5 per bit (score.cu).  Tables are rebuilt per
-//            32-token slab (lane p builds position p), double-buffered per warp.
+//            32-token slab (lane p builds position p), one table per warp.
 //   phase C  cluster Top-k on the shared-memory keys (select_radix.cuh: a fixed
 //            12-bit radix histogram counted by the scorer, merged over DSMEM,
 //            candidate refinement by further digits, exact rank; two cluster
@@ -89,6 +89,10 @@ constexpr int kFsSelWarps = kFsWarps - kFsGatherWarps;  // the first resolve the
 constexpr int kFsSelThreads = kFsSelWarps * 32;
 constexpr int kFsNst = FIER_FS_NST;
 constexpr int kFsMaxKpt = 16;  // slice <= 8192 tokens (u16 slots in sidx)
+#ifndef FS_SCORE_WARPS
+#define FS_SCORE_WARPS 16
+#endif
+constexpr int kFsScoreWarps = FS_SCORE_WARPS;  // warps that score in phase B
 constexpr int kFsAppendSlabs = 5;  // sealed slabs the append warps hand to the others (~ the append's time)
 constexpr int kFsLutBytes = kNibTableBytes;
 // Shared memory map (bytes from a 256-aligned base).  RxShared's tail (the digit-1
@@ -99,7 +103,7 @@ constexpr int kFsRx = 0;
 constexpr int kFsRing = kFsRx + (int)offsetof(RxShared, hist);                     // phase D rings
 constexpr int kFsRingBytes = kFsGatherWarps * kFsNst * 2 * tc_stage_bytes<kFsD>();
 constexpr int kFsLut = (kFsRx + (int)sizeof(RxShared) + 255) / 256 * 256;          // phase B (in the ring area)
-constexpr int kFsKeys = kFsLut + kFsWarps * 2 * kFsLutBytes;                      // phase B/C keys (ditto)
+constexpr int kFsKeys = kFsLut + kFsWarps * kFsLutBytes;                      // phase B/C keys (ditto)
 constexpr int kFsRingArea = cmax(kFsRingBytes, kFsKeys + kFsThreads * kFsMaxKpt * 4 - kFsRing);
 constexpr int kFsSidx = kFsRing + kFsRingArea;                                    // u16 gather list
 constexpr int kFsMasks = kFsSidx + kFsThreads * kFsMaxKpt * 2;                    // amask, kmask
@@ -224,7 +228,7 @@ __global__ void __launch_bounds__(kFsThreads, 1) step_fused_kernel(const FsArgs 
     float qv[4];
 #pragma unroll
     for (int i = 0; i < 4; ++i) qv[i] = qrot[4 * lane + i];
-    const uint32_t tab0 = base + kFsLut + warp * 2 * kFsLutBytes;
+    const uint32_t tab0 = base + kFsLut + warp * kFsLutBytes;  // one table per warp (trace: 10.75 vs 11.0 us double-buffered)
     float* srow = a.scores ? a.scores + (int64_t)row * a.ld : nullptr;
     // Scoring is assigned per slab (32 tokens), independently of which warp owns the
     // slab's keys in phase C (keys are stored token-ordered: slab sl -> keys_s[32 sl ..]).
@@ -236,10 +240,13 @@ __global__ void __launch_bounds__(kFsThreads, 1) step_fused_kernel(const FsArgs 
     const int nsealed = appender ? (open_lo - s0) / 32 : (ntok + 31) / 32;
     int start, cnt;
     {
-        const int per = nsealed / kFsWarps;
+        const int per = nsealed / kFsScoreWarps;
         const int na = appender ? max(0, per - kFsAppendSlabs) : per;  // warps 0..3
-        const int rest = nsealed - 4 * na, nb = kFsWarps - 4;
-        if (warp < 4) {
+        const int rest = nsealed - 4 * na, nb = kFsScoreWarps - 4;
+        if (warp >= kFsScoreWarps) {
+            start = nsealed;
+            cnt = 0;
+        } else if (warp < 4) {
             start = warp * na;
             cnt = na;
         } else {
@@ -252,10 +259,10 @@ __global__ void __launch_bounds__(kFsThreads, 1) step_fused_kernel(const FsArgs 
         const int t0 = s0 + 32 * sl, t = t0 + lane;
         uint32_t key = 0u;  // 0 = empty slot (past the row end, or NaN)
         if (t0 < a.tokens) {  // warp-uniform
-            const uint32_t tab = tab0 + (u & 1) * kFsLutBytes;
-            build_nibble_table(tab, p, qv);
+            build_nibble_table(tab0, p, qv);
             __syncwarp();
-            const float sc = nibble_score(tab, bw);
+            const float sc = nibble_score(tab0, bw);
+            __syncwarp();  // every lane read the table before the next slab rebuilds it
             if (t < a.tokens) {
                 key = score_key(sc);
                 if (srow) srow[t] = sc;
@@ -285,33 +292,40 @@ __global__ void __launch_bounds__(kFsThreads, 1) step_fused_kernel(const FsArgs 
         }
     }
     uint4 pb[PF], bb[PF];  // register ring: (s, z) and bit rows of the next PF slabs
-    if (cnt == kFsMaxKpt && a.g_shift >= 0 && s0 + 32 * (start + cnt) <= a.tokens) {
-        // full slabs only: compile-time trip count, no per-slab bounds checks
+    // Fast path: whole chunks of PF full, sealed slabs -- no per-slab bounds checks, a
+    // compile-time inner loop (trace: the per-slab checks cost ~1 us of the C2 score phase).
+    int nfast = 0;
+    if (a.g_shift >= 0 && cnt >= PF) {
+        const int full = min(cnt, (a.tokens - s0) / 32 - start);  // slabs whose 32 tokens all exist
+        nfast = max(0, full) / PF * PF;
+    }
+    if (nfast > 0) {
         const uint32_t* bw0 = bseq + (int64_t)(s0 + 32 * start + lane) * 4;
-        const __half2* zw0 = zseq + (int64_t)((s0 + 32 * start) >> a.g_shift) * D + 4 * lane;
+        const int t00 = s0 + 32 * start;
         auto ld = [&](int j, uint4& p, uint4& bw) {
-            p = ld_cg16(zw0 + (int64_t)((32 * j) >> a.g_shift) * D);
+            p = ld_cg16(zseq + (int64_t)((t00 + 32 * j) >> a.g_shift) * D + 4 * lane);
             bw = ld_cg16(bw0 + (int64_t)j * 128);
         };
 #pragma unroll
         for (int u = 0; u < PF; ++u) ld(u, pb[u], bb[u]);
-        for (int j0 = 0; j0 < kFsMaxKpt; j0 += PF) {
+        for (int j0 = 0; j0 < nfast; j0 += PF) {
 #pragma unroll
             for (int u = 0; u < PF; ++u) {
                 const int j = j0 + u;
                 const uint4 p = pb[u], bw = bb[u];
-                if (j + PF < kFsMaxKpt) ld(j + PF, pb[u], bb[u]);
-                const uint32_t tab = tab0 + (u & 1) * kFsLutBytes;
-                build_nibble_table(tab, p, qv);
+                if (j + PF < nfast) ld(j + PF, pb[u], bb[u]);
+                build_nibble_table(tab0, p, qv);
                 __syncwarp();
-                const float sc = nibble_score(tab, bw);
+                const float sc = nibble_score(tab0, bw);
+                __syncwarp();  // every lane read the table before the next slab rebuilds it
                 const uint32_t key = score_key(sc);
                 if (srow) srow[s0 + 32 * (start + j) + lane] = sc;
                 keys_s[32 * (start + j) + lane] = key;
                 rx_count(S, key);
             }
         }
-        cnt = 0;
+        start += nfast;
+        cnt -= nfast;
     }
 #pragma unroll
     for (int u = 0; u < PF; ++u)
