@@ -441,6 +441,7 @@ template <int NT>
 __device__ __forceinline__ RxFind rx_find(int nct, int k, RxShared& S, RxPublished& P, uint64_t* cbar) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     __syncthreads();  // this CTA's histogram is complete
+    T2_MARK(17);
     for (int c = warp; c < 64; c += NT / 32) {  // coarse bins: 64 fine bins each, two per lane
         const uint2 v = reinterpret_cast<const uint2*>(S.hist + 64 * c)[lane];
         uint32_t x = v.x + v.y;

@@ -35,7 +35,10 @@ __global__ void __launch_bounds__(kT2Threads, 2) topk2_kernel(const float* __res
     for (int j = 0; j < KPT; ++j) {
         const int p = wbase + 32 * j + lane;
         const float v = p < cnt ? srow[s0 + p] : __int_as_float(0x7fffffff);
-        key[j] = p < cnt ? score_key(v) : 0u;  // 0: empty slot past the row end
+        // 1: a NaN score (ranks lowest, score_key), 0: an empty slot past the row end.  Kept
+        // branch-free around the load: with the row-end test first the compiler serialised
+        // the KPT loads (C4 Top-k 151 -> 251 us).
+        key[j] = isnan(v) ? (p < cnt ? 1u : 0u) : float_key(v);
         if (isfinite(v)) {
             mn = fminf(mn, v);
             mx = fmaxf(mx, v);
@@ -73,7 +76,7 @@ __global__ void __launch_bounds__(kT2Threads, 2) topk2s_kernel(const float* __re
     for (int j = 0; j < kpt; ++j) {
         const int p = wbase + 32 * j + lane;
         const float v = p < cnt ? srow[s0 + p] : __int_as_float(0x7fffffff);
-        keys_s[p] = p < cnt ? score_key(v) : 0u;  // 0: empty slot past the row end
+        keys_s[p] = isnan(v) ? (p < cnt ? 1u : 0u) : float_key(v);  // 1: NaN score, 0: empty slot
         if (isfinite(v)) {
             mn = fminf(mn, v);
             mx = fmaxf(mx, v);
@@ -147,7 +150,7 @@ int topk2_dispatch(const float* scores, int rows, int tokens, int64_t ld, int k,
     int c = 1;
     // grow the cluster until the grid covers the chip (or slices reach 8 keys per thread),
     // then until the slice fits the 32 registers per thread
-    constexpr int max_c = 4;  // cap of the first growth step (K3: cluster 4/8 sweeps)
+    constexpr int max_c = 4;
     while (c < max_c && (int64_t)rows * c < 2 * num_sms() && ceil_div(tokens, c) > 8 * kT2Threads) c *= 2;
     while (c < kT2MaxCluster && ceil_div(tokens, c) > 32 * kT2Threads) c *= 2;
     const int64_t slice = ceil_div(tokens, c);
