@@ -489,15 +489,24 @@ def run_ours(args, cfg, world, rank, local):
 
 
 def run_sharded(args, cfg, world, rank, local):
-    """C5 over N > 1 GPUs: the context is sequence-sharded (whole groups per rank); every step
-    runs shard-local append/score/Top-k, one NCCL all-gather of the (score, index) candidates,
-    the global merge, ragged K4 and a second all-gather of the (o, lse) partials
-    (paper_2508_08256_b200.shard.sharded_step).  Eager launches; time = max over ranks."""
+    """C5 sequence-sharded over the N ranks (N = 1 with --sharded: the same protocol on one
+    GPU): every step runs shard-local append/score/Top-k, one NCCL all-gather of the (score,
+    index) candidates, the global merge, ragged K4 and a second all-gather of the (o, lse)
+    partials (paper_2508_08256_b200.shard.sharded_step).  The whole step -- kernels and both
+    collectives -- is captured in one CUDA graph per rank (eager if capture fails); device
+    time with CUDA events, max over ranks.  e2e: the same step with q / k_new / v_new copied
+    from pinned host memory and the output copied back, inside the timed region."""
     import torch
+    import torch.distributed as dist
 
     from paper_2508_08256_b200.shard import DistExchange, ShardedDecodeLayer, sharded_step
 
     dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    if not dist.is_initialized():  # --sharded at N = 1: a one-rank NCCL group
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29511")
+        dist.init_process_group("nccl", rank=0, world_size=1, device_id=dev)
     B, Hq, Hkv, L, d, n, g = (cfg[k] for k in ("B", "Hq", "Hkv", "L", "d", "n", "g"))
     dt = {"bf16": torch.bfloat16, "f16": torch.float16, "f32": torch.float32}[cfg["dtype"]]
     shard = ShardedDecodeLayer(B, Hq, Hkv, L, d, g, rank=rank, shards=world, dtype=dt, device=dev)
@@ -511,22 +520,90 @@ def run_sharded(args, cfg, world, rank, local):
     pos = L - 1
     shard.prefill(pos)
     ex = DistExchange()
-    for _ in range(args.warmup):
-        sharded_step(shard, ex, q, kn, vn, pos, n)
+    stream = torch.cuda.Stream(device=dev)
+    out_buf = torch.empty((B, Hq, d), dtype=torch.float32, device=dev)
+
+    def step():
+        out_buf.copy_(sharded_step(shard, ex, q, kn, vn, pos, n))
+
+    with torch.cuda.stream(stream):
+        for _ in range(2):  # eager: buffers allocated, NCCL communicator warmed up
+            step()
     torch.cuda.synchronize()
-    barrier(world)
-    torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    graph = None
+    try:
+        g0 = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g0, stream=stream):
+            step()
+        g0.replay()
+        torch.cuda.synchronize()
+        graph = g0
+    except Exception as e:  # noqa: BLE001 -- fall back to eager launches, say so in the line
+        print(f"[bench] graph capture of the sharded step failed ({e}); eager", file=sys.stderr)
+        torch.cuda.synchronize()
+    run = graph.replay if graph is not None else step
+
+    def timed(fn, steps):
+        barrier(world)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(stream):
+            e0.record(stream)
+            for _ in range(steps):
+                fn()
+            e1.record(stream)
+        torch.cuda.synchronize()
+        barrier(world)
+        return max_over_ranks(e0.elapsed_time(e1), world) * 1000.0 / steps
+
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            run()
     sampler = ClockSampler(local)
     with sampler:
-        e0.record()
-        for _ in range(args.steps):
-            sharded_step(shard, ex, q, kn, vn, pos, n)
-        e1.record()
-        torch.cuda.synchronize()
-    barrier(world)
-    us = max_over_ranks(e0.elapsed_time(e1), world) * 1000.0 / args.steps
-    return us, sampler.summary()
+        us = timed(run, args.steps)
+
+    # e2e: q / k_new / v_new from pinned host memory (one H2D), the output back (one D2H)
+    hin = torch.cat([q.reshape(-1), kn.reshape(-1), vn.reshape(-1)]).cpu().pin_memory()
+    hout = torch.empty(out_buf.shape, dtype=torch.float32).pin_memory()
+    din = torch.empty_like(hin, device=dev)
+    nq, nk = q.numel(), kn.numel()
+
+    def e2e_step():
+        din.copy_(hin, non_blocking=True)
+        q.copy_(din[:nq].view_as(q))
+        kn.copy_(din[nq:nq + nk].view_as(kn))
+        vn.copy_(din[nq + nk:].view_as(vn))
+        run()
+        hout.copy_(out_buf, non_blocking=True)
+
+    with torch.cuda.stream(stream):
+        for _ in range(3):
+            e2e_step()
+    e2e_us = timed(e2e_step, max(10, args.steps // 4))
+    # per-rank algorithmic bytes: this shard's packed index + its share of the selected rows + q/o
+    lt = shard.end - shard.start
+    es = elem_size(cfg["dtype"])
+    packed = B * Hkv * (lt * ((d + 7) // 8) + ((lt + g - 1) // g) * d * 4)
+    sel = shard.sel_global
+    rows = int(((sel >= shard.start) & (sel < shard.end)).sum().item()) if sel is not None else B * Hq * n // world
+    alg = packed + rows * d * 2 * es + B * Hq * d * (es + 4)
+    peak, src = peaks()
+    ach = alg / (us * 1e-6) / 1e9
+    info = {
+        "graph": graph is not None,
+        "roofline": {"bound": "hbm", "kernel": "sharded step of one rank (all kernels + 2 all-gathers)",
+                     "achieved": round(ach, 1), "peak": peak, "unit": "GB/s", "frac": round(ach / peak, 4),
+                     "traffic": None, "alg_bytes": alg, "peak_source": src,
+                     "note": "rank-local algorithmic bytes (its packed slice + its selected rows + q/o) over "
+                             "the max-over-ranks step time"},
+        "e2e": {"value": round(e2e_us, 3), "unit": UNIT, "h2d_bytes_per_step": hin.numel() * hin.element_size(),
+                "d2h_bytes_per_step": hout.numel() * 4,
+                "how": "q/k_new/v_new H2D from pinned memory + the captured sharded step + output D2H, per rank"},
+        "launches_per_step": 8,
+        "clocks": sampler.summary(),
+    }
+    return us, info
 
 
 def cpu_baseline(cfg, K, V, inp, budget_s=20.0):
@@ -644,15 +721,19 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=2000)
     ap.add_argument("--warmup", type=int, default=20)
-    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default=None, choices=sorted(CONFIGS),
+                    help="default: c2 at N = 1 (the headline), c5 sequence-sharded at N > 1")
+    ap.add_argument("--sharded", action="store_true", help="c5: run the sharded protocol even at N = 1")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--layers", type=int, default=0, help="override the layer-rotation count")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
-    cfg = CONFIGS[args.config]
     world, rank, local = dist_setup(args)
+    if args.config is None:  # N > 1 exercises the sequence-sharded exchange
+        args.config = "c5" if world > 1 and args.impl == "ours" else "c2"
+    cfg = CONFIGS[args.config]
 
     if args.impl == "reference":
         out = run_reference(args, cfg, world, rank)
@@ -660,8 +741,8 @@ def main():
             print(json.dumps(out))
         return
 
-    if world > 1 and args.config == "c5":
-        us, clocks = run_sharded(args, cfg, world, rank, local)
+    if args.config == "c5" and (world > 1 or args.sharded):
+        us, info = run_sharded(args, cfg, world, rank, local)
         if rank == 0:
             packed, kvb, qo = algorithmic_bytes(cfg)
             print(json.dumps({
@@ -669,9 +750,13 @@ def main():
                 "warmup": args.warmup, "ms_per_step": round(us / 1000.0, 6), "higher_is_better": False,
                 "scaling": "strong", "vs_baseline": None, "dtype": cfg["dtype"],
                 "data": "synthetic random-init Q/K/V (torch Philox), prefix index pre-packed",
-                "config": dict(config_block(args, cfg, world), parallelism=f"sequence-sharded x{world} (NCCL)"),
-                "roofline": None, "cpu_baseline": None, "e2e": None,
-                "gpu_launches": args.steps * (4 + 3 + 1) * 1, "clocks": clocks,
+                "config": dict(config_block(args, cfg, world),
+                               parallelism=f"sequence-sharded x{world} (NCCL all-gathers, CUDA graph: "
+                                           f"{info['graph']})",
+                               l2="inputs larger than L2: each rank streams its whole slice (>= 134 MB of "
+                                  "K/V + index per rank at N <= 8) every step"),
+                "roofline": info["roofline"], "cpu_baseline": None, "e2e": info["e2e"],
+                "gpu_launches": args.steps * info["launches_per_step"], "clocks": info["clocks"],
                 "alg_bytes_per_step": packed + kvb + qo}))
         import torch.distributed as dist
         dist.destroy_process_group()

@@ -69,6 +69,20 @@ class DistExchange:
         return torch.stack(parts)
 
 
+class HostStagedExchange(DistExchange):
+    """all_gather of device tensors over a CPU backend (gloo): device -> host copy,
+    gather, host -> device.  Lets several processes that share one GPU (or GPUs without
+    a peer path) run the sharded protocol with the CUDA kernels on every shard."""
+
+    def all_gather(self, t: torch.Tensor) -> torch.Tensor:
+        if not t.is_cuda:
+            return super().all_gather(t)
+        h = t.contiguous().cpu()
+        parts = [torch.empty_like(h) for _ in range(self.world)]
+        self.dist.all_gather(parts, h, group=self.group)
+        return torch.stack(parts).to(t.device)
+
+
 def _pack_candidates(cs: torch.Tensor, ci: torch.Tensor) -> torch.Tensor:
     return torch.stack([cs.view(torch.int32), ci])
 

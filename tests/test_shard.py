@@ -241,3 +241,71 @@ def test_virtual_sharded_1m_context(cuda, port):
         o = port.gather_attention(q[0, h].double().cpu().numpy(), Kd, Vd,
                                   s1[0, h].cpu().numpy().astype(np.int64))
         assert port.relative_l2_error(out[0, h].cpu().numpy(), o) < 1e-2
+
+
+def _cuda_shard_worker(rank, world, port_no, L, Hq, Hkv, n, dt_name, seed, result_path):
+    """One process per shard, all on cuda:0: the CUDA ShardedDecodeLayer of `rank`, the
+    exchange over gloo through host copies (HostStagedExchange)."""
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port_no)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2508_08256_b200.shard import HostStagedExchange, ShardedDecodeLayer, sharded_step
+    dev = torch.device("cuda", 0)
+    dt = getattr(torch, dt_name)
+    d, g = 128, 32
+    gen = torch.Generator(device="cpu").manual_seed(seed)  # identical full inputs on every rank
+    K = torch.randn((1, Hkv, L, d), generator=gen).to(dt)
+    V = torch.randn((1, Hkv, L, d), generator=gen).to(dt)
+    q = torch.randn((1, Hq, d), generator=gen).to(dt).to(dev)
+    kn = torch.randn((1, Hkv, d), generator=gen).to(dt).to(dev)
+    vn = torch.randn((1, Hkv, d), generator=gen).to(dt).to(dev)
+    pos = L - 1
+    s = ShardedDecodeLayer(1, Hq, Hkv, L, d, g, rank=rank, shards=world, dtype=dt, device=dev)
+    s.K[:, :, : s.end - s.start].copy_(K[:, :, s.start:s.end])
+    s.V[:, :, : s.end - s.start].copy_(V[:, :, s.start:s.end])
+    s.prefill(pos)
+    ex = HostStagedExchange()
+    outs = []
+    for _ in range(2):  # two steps: the second re-appends the same token (idempotent)
+        outs.append(sharded_step(s, ex, q, kn, vn, pos, n).cpu())
+    torch.cuda.synchronize()
+    np.savez(result_path + f".{rank}.npz", out=outs[-1].numpy(), out0=outs[0].numpy(),
+             sel=s.sel_global.cpu().numpy())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world,L,Hq,Hkv,n,dt", [(2, 4096, 8, 2, 400, "bfloat16"), (3, 3000, 4, 4, 350, "float16")])
+def test_two_process_cuda_sharded_step(cuda, tmp_path, world, L, Hq, Hkv, n, dt):
+    """SURVEY §8(e) on real processes: `world` ranks, each a CUDA ShardedDecodeLayer on cuda:0,
+    exchanging candidates and partials over gloo -- the same selection as the unsharded GPU
+    step and the same output within fp32 merge rounding, identical on every rank."""
+    import torch.multiprocessing as mp
+    import paper_2508_08256_b200 as F
+    seed = 21
+    res = str(tmp_path / "res")
+    mp.spawn(_cuda_shard_worker, args=(world, _free_port(), L, Hq, Hkv, n, dt, seed, res), nprocs=world,
+             join=True)
+    outs = [np.load(res + f".{r}.npz") for r in range(world)]
+    for r in range(world):
+        assert np.array_equal(outs[r]["sel"], outs[0]["sel"])
+        assert np.array_equal(outs[r]["out"], outs[0]["out"])
+        assert np.array_equal(outs[r]["out0"], outs[r]["out"])
+    # the unsharded step on the same inputs (same generator order as the workers)
+    d, g = 128, 32
+    tdt = getattr(torch, dt)
+    gen = torch.Generator(device="cpu").manual_seed(seed)
+    K = torch.randn((1, Hkv, L, d), generator=gen).to(tdt)
+    V = torch.randn((1, Hkv, L, d), generator=gen).to(tdt)
+    q = torch.randn((1, Hq, d), generator=gen).to(tdt).to(cuda)
+    kn = torch.randn((1, Hkv, d), generator=gen).to(tdt).to(cuda)
+    vn = torch.randn((1, Hkv, d), generator=gen).to(tdt).to(cuda)
+    pos = L - 1
+    layer = F.DecodeLayer(1, Hq, Hkv, L, d, g, dtype=tdt, device=cuda, K=K.to(cuda), V=V.to(cuda))
+    layer.prefill(pos)
+    o1, s1 = layer.step(q, kn, vn, pos, n)
+    torch.cuda.synchronize()
+    assert np.array_equal(outs[0]["sel"], s1.cpu().numpy()), "sharded selection differs from unsharded"
+    assert np.allclose(outs[0]["out"], o1.cpu().numpy(), rtol=1e-4, atol=1e-5)
