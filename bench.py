@@ -280,8 +280,12 @@ def run_ours(args, cfg, world, rank, local):
         _lib.check(lib.fier_score(C.byref(lay.shape), _p(q), _p(lay.pk.bits), _p(lay.pk.params), pos + 1,
                                   _p(scores[li]), ld, _stream()))
 
-    def k_topk(li):
-        _lib.check(lib.fier_topk(_p(scores[li]), B * Hq, pos + 1, ld, n, _p(sels[li]), None, 0, _stream()))
+    tws_b = lib.fier_topk_workspace(B * Hq, pos + 1, n)
+    tws = torch.empty(max(tws_b, 1), dtype=torch.uint8, device=dev)
+
+    def k_topk(li):  # with the workspace, as in the decode step
+        _lib.check(lib.fier_topk(_p(scores[li]), B * Hq, pos + 1, ld, n, _p(sels[li]), _p(tws), tws_b,
+                                 _stream()))
 
     def k_attn(li):
         lay, (q, _, _) = layers[li], inputs[li]

@@ -103,7 +103,11 @@ FIER_API int fier_score(const fier_shape* s, const void* q, const uint32_t* bits
 /* ---- K3: Top-k selector -------------------------------------------------------- */
 /* topk_oracle (core.hpp:134-148) on `rows` rows of `tokens` fp32 scores
  * (row stride ld): the k largest, ties to the lower index, ascending output
- * in sel[row][0..k).  Requires 1 <= k <= tokens ("topk_oracle: k out of range"). */
+ * in sel[row][0..k).  Requires 1 <= k <= tokens ("topk_oracle: k out of range").
+ * With a device workspace of fier_topk_workspace() bytes (0 = none needed), launches
+ * holding millions of keys take the wide-grid radix select (histogram pass, collect pass,
+ * per-row resolve + sort: 3 kernels and a memset); without one (NULL, 0), the per-row
+ * cluster select.  Both return identical selections. */
 FIER_API size_t fier_topk_workspace(int32_t rows, int32_t tokens, int32_t k);
 FIER_API int fier_topk(const float* scores, int32_t rows, int32_t tokens, int64_t ld, int32_t k,
               int32_t* sel, void* workspace, size_t workspace_bytes, void* stream);

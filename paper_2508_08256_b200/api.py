@@ -267,11 +267,13 @@ def approx_scores(q: torch.Tensor, pk: PackedKeys) -> torch.Tensor:
     return scores.view(-1) if single else scores
 
 
-def topk_oracle(scores: torch.Tensor, k: int) -> torch.Tensor:
+def topk_oracle(scores: torch.Tensor, k: int, wide: bool = True) -> torch.Tensor:
     """topk_oracle (core.hpp:134-148): int32 ascending indices [k] or [..., k].
 
-    float32 scores take the decode path's cluster select (fier_topk); float64 scores
-    (the reference's own ScoreVector type) the exact fp64 select (fier_topk_f64)."""
+    float32 scores take the decode path's select (fier_topk: with ``wide``, launches of
+    millions of keys use the wide-grid radix select and its workspace, else the per-row
+    cluster select); float64 scores (the reference's own ScoreVector type) the exact fp64
+    select (fier_topk_f64)."""
     s = _cuda(scores, "topk_oracle")
     _require(s.dtype in (torch.float32, torch.float64), "topk_oracle: scores must be float32 or float64")
     l = s.shape[-1]
@@ -281,7 +283,10 @@ def topk_oracle(scores: torch.Tensor, k: int) -> torch.Tensor:
     if s.dtype == torch.float64:
         check(_lib.load().fier_topk_f64(_p(s), rows, l, l, k, _p(sel), _stream()))
     else:
-        check(_lib.load().fier_topk(_p(s), rows, l, l, k, _p(sel), None, 0, _stream()))
+        lib = _lib.load()
+        wsb = lib.fier_topk_workspace(rows, l, k) if wide else 0
+        ws = torch.empty(wsb, dtype=torch.uint8, device=s.device) if wsb else None
+        check(lib.fier_topk(_p(s), rows, l, l, k, _p(sel), _p(ws) if ws is not None else None, wsb, _stream()))
     return sel
 
 

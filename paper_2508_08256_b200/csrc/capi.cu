@@ -31,6 +31,7 @@ int append_dispatch(const fier_shape*, void*, void*, const void*, const void*, i
 int score_dispatch(const fier_shape*, const void*, const uint32_t*, const void*, int, float*, int64_t,
                    cudaStream_t);
 int topk_dispatch(const float*, int, int, int64_t, int, int32_t*, cudaStream_t);
+int topk_dispatch_ws(const float*, int, int, int64_t, int, int32_t*, void*, size_t, cudaStream_t);
 size_t topk_workspace(int, int, int);
 size_t sparse_workspace(const fier_shape*, int);
 size_t full_workspace(const fier_shape*, int);
@@ -138,13 +139,12 @@ size_t fier_topk_workspace(int32_t rows, int32_t tokens, int32_t k) { return top
 
 int fier_topk(const float* scores, int32_t rows, int32_t tokens, int64_t ld, int32_t k, int32_t* sel,
               void* workspace, size_t workspace_bytes, void* stream) {
-    (void)workspace;
-    (void)workspace_bytes;
     FIER_REQUIRE(rows >= 1 && rows <= 65535, "topk_oracle: rows out of range");
     FIER_REQUIRE(k >= 1 && k <= tokens, "topk_oracle: k out of range");
     FIER_REQUIRE(ld >= tokens, "topk_oracle: score row stride shorter than tokens");
     FIER_REQUIRE(scores && sel, "topk_oracle: null buffer");
-    return topk_dispatch(scores, rows, tokens, ld, k, sel, static_cast<cudaStream_t>(stream));
+    return topk_dispatch_ws(scores, rows, tokens, ld, k, sel, workspace, workspace ? workspace_bytes : 0,
+                            static_cast<cudaStream_t>(stream));
 }
 
 size_t fier_sparse_attention_workspace(const fier_shape* s, int32_t n) {
@@ -301,7 +301,9 @@ int fier_decode_step_ex(const fier_shape* s, const void* q, const void* k_new, c
     int rc = append_score_dispatch(s, q, K, V, k_new, v_new, pos, bits, params, scores, ld, counters,
                                    s->batch * s->q_heads, nonfinite, st);
     if (rc) return rc;
-    rc = topk_dispatch(scores, s->batch * s->q_heads, tokens, ld, n, sel, st);
+    uint8_t* tws = attn_ws + align_up(sparse_workspace(s, n));
+    rc = topk_dispatch_ws(scores, s->batch * s->q_heads, tokens, ld, n, sel, tws,
+                          topk_workspace(s->batch * s->q_heads, tokens, n), st);
     if (rc) return rc;
     return sparse_dispatch(s, q, K, V, sel, n, tokens, scale, out, attn_ws, true, st, nullptr, nullptr);
 }

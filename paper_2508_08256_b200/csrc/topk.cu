@@ -3,7 +3,9 @@
 // Replaces topk_oracle (reference core.hpp:134-148): the k largest scores,
 // ties to the LOWER index, returned in ascending index order.
 //
-//   rows <= 16 * 512 * 32 keys   topk2.cu      one thread-block cluster per row (the fast path)
+//   many short rows              topk_global.cu  tr_row_kernel: one small CTA per row (C4)
+//   millions of keys (workspace) topk_global.cu  wide grid, per-row radix state in global memory
+//   rows <= 16 * 512 * 32 keys   topk2.cu      one thread-block cluster per row
 //   longer rows (C5, 1M tokens)  topk_long.cu  three streaming passes around a radix threshold
 //   anything else                topk_stream_kernel below (exact smem radix select)
 #include <cooperative_groups.h>
@@ -139,12 +141,12 @@ __global__ void __launch_bounds__(1024, 1)
     cluster.sync();
 }
 
-size_t topk_workspace(int rows, int tokens, int k) {
-    (void)rows;
-    (void)tokens;
-    (void)k;
-    return 0;
-}
+size_t topk_global_workspace(int rows, int tokens, int k);
+int topk_global_dispatch(const float* scores, int rows, int tokens, int64_t ld, int k, int32_t* sel,
+                         void* workspace, size_t workspace_bytes, cudaStream_t st);
+
+// Workspace of the wide-grid path (topk_global.cu); 0 where it does not apply.
+size_t topk_workspace(int rows, int tokens, int k) { return topk_global_workspace(rows, tokens, k); }
 
 template <typename Kern, typename... Args>
 static int launch_cluster(Kern kern, int cluster, int rows, int threads, size_t smem, cudaStream_t st,
@@ -173,9 +175,26 @@ static int launch_cluster(Kern kern, int cluster, int rows, int threads, size_t 
 int topk2_dispatch(const float*, int, int, int64_t, int, int32_t*, cudaStream_t);
 int topk_long_dispatch(const float* scores, int rows, int tokens, int64_t ld, int k, int32_t* sel, cudaStream_t st);
 
+int topk_dispatch(const float* scores, int rows, int tokens, int64_t ld, int k, int32_t* sel, cudaStream_t st);
+
+// With a workspace of topk_workspace() bytes, rows holding millions of keys take the
+// wide-grid radix select (topk_global.cu); otherwise the cluster paths below.
+int topk_dispatch_ws(const float* scores, int rows, int tokens, int64_t ld, int k, int32_t* sel, void* workspace,
+                     size_t workspace_bytes, cudaStream_t st) {
+    if ((ld & 3) == 0 && (reinterpret_cast<uintptr_t>(scores) & 15) == 0) {
+        const int rc = topk_global_dispatch(scores, rows, tokens, ld, k, sel, workspace, workspace_bytes, st);
+        if (rc >= 0) return rc;
+    }
+    return topk_dispatch(scores, rows, tokens, ld, k, sel, st);
+}
+
+int topk_rows_dispatch(const float* scores, int rows, int tokens, int64_t ld, int k, int32_t* sel, cudaStream_t st);
+
 int topk_dispatch(const float* scores, int rows, int tokens, int64_t ld, int k, int32_t* sel,
                   cudaStream_t st) {
-    int rc = topk2_dispatch(scores, rows, tokens, ld, k, sel, st);
+    int rc = topk_rows_dispatch(scores, rows, tokens, ld, k, sel, st);  // many short rows (C4): a CTA per row
+    if (rc >= 0) return rc;
+    rc = topk2_dispatch(scores, rows, tokens, ld, k, sel, st);
     if (rc >= 0) return rc;
     rc = topk_long_dispatch(scores, rows, tokens, ld, k, sel, st);  // rows too long for the on-chip path (C5)
     if (rc >= 0) return rc;

@@ -53,12 +53,16 @@ __device__ __forceinline__ uint32_t tl_key(float v, int i, int s1) { return i < 
 
 constexpr int kTlDepth = 8;  // tiles of loads in flight per thread (64 KB per SM)
 
+// (an explicit branch: a select let the compiler issue the guarded scalar loads next to
+// every vector load)
 __device__ __forceinline__ float4 tl_load4(const float* srow, int i, int s1) {
-    return i + 3 < s1 ? ldg_stream_f4(srow + i)
-                      : make_float4(i < s1 ? srow[i] : __int_as_float(0x7fffffff),
-                                    i + 1 < s1 ? srow[i + 1] : __int_as_float(0x7fffffff),
-                                    i + 2 < s1 ? srow[i + 2] : __int_as_float(0x7fffffff),
-                                    __int_as_float(0x7fffffff));
+    if (i + 3 < s1) return ldg_stream_f4(srow + i);
+    float4 x = make_float4(__int_as_float(0x7fffffff), __int_as_float(0x7fffffff), __int_as_float(0x7fffffff),
+                           __int_as_float(0x7fffffff));
+    if (i < s1) x.x = srow[i];
+    if (i + 1 < s1) x.y = srow[i + 1];
+    if (i + 2 < s1) x.z = srow[i + 2];
+    return x;
 }
 
 // f(key, index) for every key of [s0, s1) (s0 % 4 == 0), 4 consecutive keys per thread

@@ -188,7 +188,9 @@ class ShardedDecodeLayer:
         sel = self._buf(f"sel{k}", (self.rows, k), torch.int32)
         check(lib.fier_score(sh, _p(q), _p(self.layer.pk.bits), _p(self.layer.pk.params), lt, _p(scores), ld,
                              _stream()))
-        check(lib.fier_topk(_p(scores), self.rows, lt, ld, k, _p(sel), None, 0, _stream()))
+        twb = lib.fier_topk_workspace(self.rows, lt, k)
+        tws = self._buf("tws", (max(twb, 1),), torch.uint8)
+        check(lib.fier_topk(_p(scores), self.rows, lt, ld, k, _p(sel), _p(tws), twb, _stream()))
         check(lib.fier_shard_candidates(_p(scores), self.rows, ld, _p(sel), k, n, self.start, _p(cs), _p(ci),
                                         _stream()))
         return cs, ci

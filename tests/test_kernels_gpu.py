@@ -460,3 +460,40 @@ def test_topk_nan_scores_rank_lowest(cuda, l, k):
         nan = np.isnan(v)
         order = np.lexsort((np.arange(l), -np.where(nan, 0.0, v), nan))  # numbers desc, then NaN; index asc
         np.testing.assert_array_equal(got[r], np.sort(order[:k]))
+
+
+@pytest.mark.parametrize("rows,l,k", [(128, 131072, 4096), (1024, 32768, 3604), (17, 1048576, 4096),
+                                      (36, 500001, 8192), (256, 65537, 1), (160, 131072, 8192),
+                                      (700, 4096, 4096), (800, 5001, 1), (640, 65536, 60000), (600, 1030, 515)])
+def test_topk_wide_grid(cuda, port, rows, l, k):
+    """The wide-grid radix selects (topk_global.cu): the CTA-per-row kernel for launches of
+    many short rows (C4) and the global-state kernels for millions of keys in few rows (C5):
+    exact vs the oracle on random rows, tie plateaus at the threshold, range outliers,
+    -inf padding, NaN rows, a constant row (candidate overflow -> the in-kernel exact
+    path); identical to the cluster select on every row."""
+    F = fier()
+    g = torch.Generator(device="cpu").manual_seed(rows + l + k)
+    s = torch.randn(rows, l, generator=g) * 20
+    s[1] = torch.round(s[1])                              # ties everywhere
+    s[2, :] = 1.0
+    s[2, ::97] = 2.0                                      # plateau straddling the k-th value
+    s[3, 5], s[3, 6] = 3e38, -3e38                        # range outliers
+    s[4, l // 3:] = -float("inf")                         # padding
+    if rows > 5:
+        s[5, ::3] = float("nan")
+        s[5, 1::3] = 1e-3 * torch.randn(len(range(1, l, 3)), generator=g) + 5.0  # narrow band + NaN
+    if rows > 6:
+        s[6] = 0.5                                        # constant: one bin holds every key
+    sd = s.to(cuda)
+    wide = F.topk_oracle(sd, k).cpu().numpy()
+    clus = F.topk_oracle(sd, k, wide=False).cpu().numpy()
+    np.testing.assert_array_equal(wide, clus)
+    for r in list(range(min(rows, 7))) + list(range(7, rows, max(1, rows // 8))):
+        v = s[r].double().numpy()
+        nan = np.isnan(v)
+        if nan.any():
+            order = np.lexsort((np.arange(l), -np.where(nan, 0.0, v), nan))
+            want = np.sort(order[:k])
+        else:
+            want = port.topk(v, k)
+        np.testing.assert_array_equal(wide[r], want, err_msg=f"row {r}")

@@ -55,8 +55,11 @@ def main():
         _lib.check(lib.fier_score(C.byref(lay.shape), _p(q), _p(lay.pk.bits), _p(lay.pk.params), pos + 1,
                                   _p(sc[i]), ld, _stream()))
 
-    def k_topk(i):
-        _lib.check(lib.fier_topk(_p(sc[i]), B * Hq, pos + 1, ld, n, _p(sel[i]), None, 0, _stream()))
+    tws_b = lib.fier_topk_workspace(B * Hq, pos + 1, n)
+    tws = torch.empty(max(tws_b, 1), dtype=torch.uint8, device=dev)
+
+    def k_topk(i):  # with the workspace, as in the decode step
+        _lib.check(lib.fier_topk(_p(sc[i]), B * Hq, pos + 1, ld, n, _p(sel[i]), _p(tws), tws_b, _stream()))
 
     def k_attn(i):
         lay, (q, _, _) = layers[i], inp[i]
