@@ -1,38 +1,31 @@
-// score_mma.cu -- K2 on the tensor cores: packed-key scoring with the bits fed
-// straight into mma.sync as bf16 "exponent-bit" operands.
+// score_mma.cu -- K2 on the tensor cores for GQA layers: packed-key scoring with the
+// sign bits applied to the group scales inside mma.sync operands.
 //
 // Replaces approx_scores (reference quant1bit.hpp:121-140):
-//     s~_t = sum_j q_j ((bit_tj ? s_gj : -s_gj) + z_gj) = bias_g + 2 sum_j bit_tj w_gj,
-//     w_gj = q_j s_gj,  bias_g = sum_j q_j (z_gj - s_gj).
-// The sum over bits is a [tokens x 128] x [128 x heads] product per group.
-//
-// Operand A (tokens x channels) comes from the packed words with ONE LOP3 per
-// two elements: a bf16 half-word with a single bit set at position 7+i
-// (0 <= i < 8) is the normal number 2^(2^i - 127), so `x & mask` turns two bits
-// of a word into two bf16 values {0, 2^e}; a rotate by 8 brings the other 16
-// bits of the word into those positions (17 instructions per 32 bits).  The
-// per-k-slot factor 2^-e is folded into operand B = w * 2^(-e - sigma), split
-// into three bf16 pieces hi + mid + lo (exact for an fp32 w: two pieces leave a
-// 2^-17 relative error per term, too coarse when large terms cancel), so every
-// product is exactly bit * w * 2^-sigma and the fp32 accumulation sees only
-// w-sized terms.  The
-// channel permutation this implies (k-slot -> channel, see kslot_channel) is
-// applied to B; the sum does not care about channel order.
+//     s~_t = sum_j q_j (z_gj + sigma_tj s_gj),  sigma = +1 for a set bit, -1 otherwise
+//          = bias_g + sum_j q_j (sigma_tj s_gj),  bias_g = sum_j q_j z_gj.
+// The second sum is a [tokens x 128] x [128 x heads] product per group with
+//   A[t][j] = sigma_tj * s_gj   (fp16: s is the index's binary16 scale, exact)
+//   B[j][h] = q_hj * 2^-e_h     (fp16 hi + lo pieces of the query, two columns per head)
+// so B is built ONCE per (sequence, kv head) and never per group, and A costs two
+// instructions per register: LOP3 flips the signs of the scale pair (s_c, s_{c+16}) of the
+// token's channel word with the complemented bits c and c+16 of the packed word shifted to
+// positions 15 and 31 (channel pairs (c, c + 16) share a register; the k-slot ->
+// channel permutation is applied to B).  Products are exact in the fp32 accumulator; all q
+// heads of a GQA group share every packed word (columns of B).
 //
 // Layout per warp and 32-token slab (one group for g = 32):
-//   A: m16n8k16 rows = tokens, lane (r, c) owns word c of tokens r, r+8 -> 16 regs
-//      per 16-token m-tile per k-step pair ... 8 k-steps cover the 128 channels
-//   B: columns 2h, 2h+1 = (hi, mid) and column 2*HPG + h = lo of query head h of
-//      the GQA group; built once per group by the whole warp (lane = 4 k-slots)
-//      into a swizzled smem tile and read back with ldmatrix
-//   D: thread (r, c) sums (hi, mid) of head 4*tile + c for tokens r, r + 8 and
-//      fetches lo with two shuffles
-// Packed bits and (s, z) stream HBM -> smem through a per-CTA ring filled by the
-// bulk-copy engine (cp.async.bulk + mbarrier), one stage = one slab per warp.
+//   A: m16n8k16 rows = tokens, lane (r, c) owns channel word c of tokens r, r + 8; per k-step
+//      s the registers hold channels 32c + 2s (+16) and 32c + 2s + 1 (+16)
+//   B: column 2h + p = piece p (hi, lo) of head h, in registers for the whole sequence
+//   D: thread (r, c) holds head c's (hi, lo) sums for tokens r, r + 8 (n-tile 0; heads 4..7
+//      in n-tile 1 for 8 heads per group)
+// Packed bits and (s, z) stream HBM -> smem through a per-warp ring filled by the bulk-copy
+// engine (cp.async.bulk + mbarrier), one stage = one slab.
 //
-// The decode-step variant fuses the K1 append: before its main loop, CTA c
-// writes the new k/v row of sequence c and re-packs that sequence's open group
-// (pack_group), then scores the open slabs itself.
+// The decode-step variant fuses the K1 append: before its main loop, CTA c writes the new
+// k/v row of sequence c and re-packs that sequence's open group (pack_group), then scores
+// the open slabs itself.
 #include <algorithm>
 
 #include "pack.cuh"
@@ -41,9 +34,15 @@ namespace fier_cuda {
 
 constexpr int kMmaWarps = 8;      // consumer warps per CTA (one slab each per stage)
 constexpr int kMmaStages = 4;     // ring depth
-constexpr int kSigma = 60;        // B = w * 2^(-e - sigma) stays inside the fp32/bf16 range
 constexpr int kSlabBytes = 32 * 16;  // bits of one 32-token slab (d = 128)
 constexpr int kParBytes = 128 * 4;   // (s, z) half2 of one group (d = 128)
+// The group's (s, z) row lands contiguously (one bulk copy) and the warp re-lays it out as
+// 4 channel words of 128 B at a 144-B stride: the 4 lanes of a quad read words 0..3 at
+// the same offset, and the 16-B skew puts those reads in different banks (contiguous, they
+// were a 4-way conflict; four 128-B bulk copies cost 45 instructions per slab).
+constexpr int kParWordStride = 144;
+constexpr int kParStage = 4 * kParWordStride;
+constexpr int kStage = kSlabBytes + kParBytes + kParStage;  // bits, params as copied, params skewed
 
 struct AppendArgs2 {  // K == nullptr: no fused append
     void* K;
@@ -61,170 +60,152 @@ struct AppendArgs2 {  // K == nullptr: no fused append
 // 6 -> 71.6 us, 8-12 -> 73.2 us)
 constexpr int kMmaRebalance = 6;
 
-// k-slot (0..127, = 16 * k-step + k) -> channel and exponent of its A value
-__host__ __device__ constexpr int kslot_i(int ks) { return 2 * (ks >> 4) + ((ks & 15) >= 8 ? 1 : 0); }
-__host__ __device__ constexpr int kslot_channel(int ks) {
-    const int k = ks & 15, h = k & 1, c = (k & 7) >> 1, i = kslot_i(ks);
-    const int off = i < 8 ? (h == 0 ? 7 + i : 23 + i) : (h == 0 ? 15 + (i - 8) : (31 + (i - 8)) & 31);
-    return 32 * c + off;
-}
-__host__ __device__ constexpr int kslot_exp(int ks) { return (1 << (kslot_i(ks) & 7)) - 127; }
-
-__device__ __forceinline__ void mma_bf16(float* d, uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t b0,
-                                         uint32_t b1) {
+__device__ __forceinline__ void mma_f16(float* d, uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t b0,
+                                        uint32_t b1) {
     asm volatile(
-        "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
         "{%0,%1,%2,%3};"
         : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
         : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
 }
 
-__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
-    asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
-                 : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
-                 : "r"(addr));
-}
-
-// A register R_i (0..15) of word x: bits (7+i, 23+i) for i < 8, else of rotr(x, 8)
-template <int I>
-__device__ __forceinline__ uint32_t abits(uint32_t x, uint32_t y) {
-    constexpr uint32_t m = (0x80u << (I & 7)) | (0x800000u << (I & 7));
-    return (I < 8 ? x : y) & m;
-}
-
-// B tile of one warp: [NCOL][128 k-slots] bf16, rows of 256 B, 16-B chunks XOR-swizzled by row
-__device__ __forceinline__ uint32_t btile_off(int col, int kslot) {
-    return (uint32_t)(col * 256 + ((((kslot >> 3) ^ (col & 7)) & 15) << 4) + (kslot & 7) * 2);
-}
+__device__ __forceinline__ float pow2f(int k) { return __int_as_float((k + 127) << 23); }  // -126 <= k <= 127
 
 template <int HPG>
-struct MmaTraits {
-    static constexpr int NT = (3 * HPG + 7) / 8;  // n-tiles of 8 columns (hi, mid, lo per head)
-    static constexpr int NHM = (2 * HPG + 7) / 8;  // n-tiles holding (hi, mid)
-    static constexpr int NCOL = 8 * NT;
-    static constexpr int BTILE = NCOL * 256;    // bytes of a warp's B tile
+struct SgnTraits {
+    static constexpr int NT = (2 * HPG + 7) / 8;  // n-tiles of 8 columns (hi, lo per head)
 };
 
-// Per-lane constants: q' = q * 2^(-e - sigma) for this lane's 4 k-slots x HPG heads,
-// the slot channels and the 2^(e + sigma) factors (for the bias).
+// Per-(sequence, kv head) lane constants.
 template <int HPG>
 struct LaneConst {
-    float qp[HPG][4];
-    int ch[4];
-    float up[4];
+    uint32_t bq[SgnTraits<HPG>::NT][8][2];  // B fragments: column 8 nt + (lane >> 2), k-steps 0..7
+    float qz[HPG][4];                       // q of this lane's channels 4 lane .. 4 lane + 3
+    float up[HPG];                          // 2^e_h
 };
 
-// Score one 32-token slab.  bits_s: 512 B of token rows (smem), par_s: 512 B of the
-// group's (s, z) half2 (smem), btile: this warp's B tile (smem).  ntok valid tokens.
-template <int HPG>
-__device__ __forceinline__ void score_slab_mma(const LaneConst<HPG>& L, const uint8_t* bits_s, const uint8_t* par_s,
-                                               uint8_t* btile, int t0, int ntok, float* out, int64_t ld) {
-    using TR = MmaTraits<HPG>;
-    const int lane = threadIdx.x & 31, r = lane >> 2, c = lane & 3;
-    // ---- B = w * 2^(-e - sigma) as bf16 hi + lo, and the per-head bias ----
-    float bias[HPG];
+// k-slot kappa (0..15) of k-step s -> channel (the A layout above)
+__device__ __forceinline__ int sgn_channel(int s, int kappa) {
+    return 32 * ((kappa >> 1) & 3) + 2 * s + (kappa >= 8 ? 1 : 0) + 16 * (kappa & 1);
+}
+
+template <typename T, int HPG>
+__device__ __forceinline__ void lane_q(const T* qg, LaneConst<HPG>& L) {
+    const int lane = threadIdx.x & 31, g = lane >> 2, c = lane & 3;
+    float mx[HPG];
 #pragma unroll
-    for (int h = 0; h < HPG; ++h) bias[h] = 0.f;
-    {
-        float sv[4], dz[4];
+    for (int h = 0; h < HPG; ++h) {
+        float m = 0.f;
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            const __half2 p = *reinterpret_cast<const __half2*>(par_s + L.ch[u] * 4);
-            const float2 f = __half22float2(p);
-            sv[u] = f.x;
-            dz[u] = (f.y - f.x) * L.up[u];  // (z - s) * 2^(e + sigma): q' * dz = q (z - s)
+        for (int i = 0; i < 4; ++i) {
+            L.qz[h][i] = to_f32(qg[h * 128 + 4 * lane + i]);
+            m = fmaxf(m, fabsf(L.qz[h][i]));
         }
 #pragma unroll
-        for (int h = 0; h < HPG; ++h) {
-            float w[4];
-            uint32_t hi[2], mid[2], lo[2];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                w[u] = L.qp[h][u] * sv[u];
-                bias[h] = fmaf(L.qp[h][u], dz[u], bias[h]);
-            }
-#pragma unroll
-            for (int v = 0; v < 2; ++v) {
-                __nv_bfloat162 hb = __floats2bfloat162_rn(w[2 * v], w[2 * v + 1]);
-                hi[v] = *reinterpret_cast<uint32_t*>(&hb);
-                const float h0 = __uint_as_float(hi[v] << 16), h1 = __uint_as_float(hi[v] & 0xFFFF0000u);
-                const float r0 = w[2 * v] - h0, r1 = w[2 * v + 1] - h1;  // exact
-                __nv_bfloat162 mb = __floats2bfloat162_rn(r0, r1);
-                mid[v] = *reinterpret_cast<uint32_t*>(&mb);
-                const float m0 = __uint_as_float(mid[v] << 16), m1 = __uint_as_float(mid[v] & 0xFFFF0000u);
-                __nv_bfloat162 lb = __floats2bfloat162_rn(r0 - m0, r1 - m1);
-                lo[v] = *reinterpret_cast<uint32_t*>(&lb);
-            }
-            // (hi, mid) of head h in columns (2h, 2h+1), lo in column 2*HPG + h
-            *reinterpret_cast<uint2*>(btile + btile_off(2 * h, 4 * lane)) = make_uint2(hi[0], hi[1]);
-            *reinterpret_cast<uint2*>(btile + btile_off(2 * h + 1, 4 * lane)) = make_uint2(mid[0], mid[1]);
-            *reinterpret_cast<uint2*>(btile + btile_off(2 * HPG + h, 4 * lane)) = make_uint2(lo[0], lo[1]);
-        }
+        for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+        mx[h] = m;
     }
-    // full-warp reductions of the biases (every lane ends with every head's total)
+    float dn[HPG];
 #pragma unroll
-    for (int h = 0; h < HPG; ++h) bias[h] = warp_sum(bias[h]);
-    __syncwarp();
-    // ---- B fragments: ldmatrix.x4 per pair of k-steps per n-tile ----
-    uint32_t bf[TR::NT][8][2];
-    const uint32_t bt = smem_u32(btile);
-#pragma unroll
-    for (int nt = 0; nt < TR::NT; ++nt)
-#pragma unroll
-        for (int kp = 0; kp < 4; ++kp) {
-            // matrix m = lane / 8: k-step 2kp + m/2, k-half m%2; row = column nt*8 + lane%8
-            const int m = lane >> 3, col = nt * 8 + (lane & 7);
-            const int kslot = (2 * kp + (m >> 1)) * 16 + (m & 1) * 8;
-            ldsm_x4(bt + btile_off(col, kslot), bf[nt][2 * kp][0], bf[nt][2 * kp][1], bf[nt][2 * kp + 1][0],
-                    bf[nt][2 * kp + 1][1]);
+    for (int h = 0; h < HPG; ++h) {  // |q * 2^-e| < 2^14: the fp16 hi + lo pieces keep 22 bits
+        int e = 0;
+        if (mx[h] > 0.f && isfinite(mx[h])) {
+            frexpf(mx[h], &e);
+            e = min(max(e - 14, -126), 127);
         }
-    __syncwarp();  // the tile may be rewritten by the next slab
-    // ---- two m-tiles of 16 tokens ----
-#pragma unroll
-    for (int mt = 0; mt < 2; ++mt) {
-        const uint32_t x0 = *reinterpret_cast<const uint32_t*>(bits_s + (mt * 16 + r) * 16 + 4 * c);
-        const uint32_t x1 = *reinterpret_cast<const uint32_t*>(bits_s + (mt * 16 + r + 8) * 16 + 4 * c);
-        const uint32_t y0 = __funnelshift_r(x0, x0, 8), y1 = __funnelshift_r(x1, x1, 8);
-        float d[TR::NT][4];
-#pragma unroll
-        for (int nt = 0; nt < TR::NT; ++nt) d[nt][0] = d[nt][1] = d[nt][2] = d[nt][3] = 0.f;
-#define FIER_KSTEP(KS)                                                                                        \
-    {                                                                                                         \
-        const uint32_t a0 = abits<2 * KS>(x0, y0), a1 = abits<2 * KS>(x1, y1);                               \
-        const uint32_t a2 = abits<2 * KS + 1>(x0, y0), a3 = abits<2 * KS + 1>(x1, y1);                       \
-        _Pragma("unroll") for (int nt = 0; nt < TR::NT; ++nt)                                                 \
-            mma_bf16(d[nt], a0, a1, a2, a3, bf[nt][KS][0], bf[nt][KS][1]);                                    \
+        L.up[h] = pow2f(e);
+        dn[h] = pow2f(-e);
     }
-        FIER_KSTEP(0) FIER_KSTEP(1) FIER_KSTEP(2) FIER_KSTEP(3) FIER_KSTEP(4) FIER_KSTEP(5) FIER_KSTEP(6)
-        FIER_KSTEP(7)
-#undef FIER_KSTEP
-        // thread (r, c): head h = nt*4 + c, columns (hi, mid) in tile nt, lo in
-        // column 2*HPG + h = lane (r, lc/2) element lc%2 of tile lc/8
-        constexpr float kScale = 2.f * 1152921504606846976.f;  // 2 * 2^sigma
 #pragma unroll
-        for (int nt = 0; nt < TR::NHM; ++nt) {
-            const int h = nt * 4 + c;
-            const int lc = 2 * HPG + (h < HPG ? h : 0);
-            const int lt = lc >> 3, src = (lane & ~3) | ((lc & 7) >> 1), el = lc & 1;
-            float la0 = 0.f, la1 = 0.f, lb0 = 0.f, lb1 = 0.f;
+    for (int nt = 0; nt < SgnTraits<HPG>::NT; ++nt) {
+        const int col = 8 * nt + g, h = col >> 1, piece = col & 1;
 #pragma unroll
-            for (int t = (2 * HPG) / 8; t <= (3 * HPG - 1) / 8; ++t) {  // the lo tile(s)
-                const float x0 = __shfl_sync(0xffffffffu, d[t][0], src);
-                const float x1 = __shfl_sync(0xffffffffu, d[t][1], src);
-                const float y0 = __shfl_sync(0xffffffffu, d[t][2], src);
-                const float y1 = __shfl_sync(0xffffffffu, d[t][3], src);
-                if (t == lt) {
-                    la0 = x0; la1 = x1; lb0 = y0; lb1 = y1;
+        for (int s = 0; s < 8; ++s) {
+            uint32_t r[2] = {0u, 0u};
+            if (h < HPG) {
+#pragma unroll
+                for (int v = 0; v < 2; ++v) {  // b0: kappa 2c, 2c+1; b1: kappa 2c+8, 2c+9
+                    float x[2];
+#pragma unroll
+                    for (int e2 = 0; e2 < 2; ++e2) {
+                        float hdn = 0.f;
+#pragma unroll
+                        for (int hh = 0; hh < HPG; ++hh) hdn = hh == h ? dn[hh] : hdn;
+                        const float w = to_f32(qg[h * 128 + sgn_channel(s, 2 * c + 8 * v + e2)]) * hdn;
+                        const float hi = __half2float(__float2half_rn(w));
+                        x[e2] = piece ? w - hi : hi;
+                    }
+                    const __half2 hv = __floats2half2_rn(x[0], x[1]);
+                    r[v] = *reinterpret_cast<const uint32_t*>(&hv);
                 }
             }
-            if (h < HPG) {
-                float bh = bias[0];
+            L.bq[nt][s][0] = r[0];
+            L.bq[nt][s][1] = r[1];
+        }
+    }
+}
+
+// Score one 32-token slab.  bits_s: 512 B of token rows (smem), par_s: 512 B of the group's
+// (s, z) half2 (smem).  ntok valid tokens.
+template <int HPG>
+__device__ __forceinline__ void score_slab_mma(const LaneConst<HPG>& L, const uint8_t* bits_s, const uint8_t* par_s,
+                                               int t0, int ntok, float* out, int64_t ld) {
+    constexpr int NT = SgnTraits<HPG>::NT;
+    const int lane = threadIdx.x & 31, r = lane >> 2, c = lane & 3;
+    // ---- the scale pairs (s_{32c+k}, s_{32c+k+16}) and the offset pairs
+    // (z_{32c+k}, z_{32c+k+16}) of this lane's channel word ----
+    const uint4* pw = reinterpret_cast<const uint4*>(par_s + c * kParWordStride);  // channels 32c .. 32c + 31
+    uint32_t sp[16], zp[16];
 #pragma unroll
-                for (int hh = 1; hh < HPG; ++hh) bh = (h == hh) ? bias[hh] : bh;
-                const float loa = el ? la1 : la0, lob = el ? lb1 : lb0;
+    for (int j = 0; j < 4; ++j) {
+        const uint4 lo = pw[j], hi = pw[j + 4];  // channels 32c + 4j .. +3 and +16
+        const uint32_t l[4] = {lo.x, lo.y, lo.z, lo.w}, h[4] = {hi.x, hi.y, hi.z, hi.w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            sp[4 * j + i] = __byte_perm(l[i], h[i], 0x5410);
+            zp[4 * j + i] = __byte_perm(l[i], h[i], 0x7632);
+        }
+    }
+    // ---- bias = sum_j q_j z_j through the tensor cores: every A row = the group's z, so
+    // one m-tile pass gives it for all 32 tokens (rows g and g + 8 alike) ----
+    float dz[NT][4];
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) dz[nt][0] = dz[nt][1] = dz[nt][2] = dz[nt][3] = 0.f;
+#pragma unroll
+    for (int ks = 0; ks < 8; ++ks)
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt)
+            mma_f16(dz[nt], zp[2 * ks], zp[2 * ks], zp[2 * ks + 1], zp[2 * ks + 1], L.bq[nt][ks][0], L.bq[nt][ks][1]);
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt) {
+        // complemented words: a clear bit flips the (positive) scale to -s
+        const uint32_t x0 = ~*reinterpret_cast<const uint32_t*>(bits_s + (mt * 16 + r) * 16 + 4 * c);
+        const uint32_t x1 = ~*reinterpret_cast<const uint32_t*>(bits_s + (mt * 16 + r + 8) * 16 + 4 * c);
+        float d[NT][4];
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) d[nt][0] = d[nt][1] = d[nt][2] = d[nt][3] = 0.f;
+#pragma unroll
+        for (int ks = 0; ks < 8; ++ks) {
+            // channels (2ks, 2ks + 16) and (2ks + 1, 2ks + 17) of the word: bits to 15 / 31
+            const uint32_t a0 = sp[2 * ks] ^ ((x0 << (15 - 2 * ks)) & 0x80008000u);
+            const uint32_t a1 = sp[2 * ks] ^ ((x1 << (15 - 2 * ks)) & 0x80008000u);
+            const uint32_t a2 = sp[2 * ks + 1] ^ ((x0 << (14 - 2 * ks)) & 0x80008000u);
+            const uint32_t a3 = sp[2 * ks + 1] ^ ((x1 << (14 - 2 * ks)) & 0x80008000u);
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt) mma_f16(d[nt], a0, a1, a2, a3, L.bq[nt][ks][0], L.bq[nt][ks][1]);
+        }
+        // thread (r, c): head h = 4 nt + c, its (hi, lo) in columns 2c, 2c + 1 of n-tile nt
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+            const int h = 4 * nt + c;
+            if (h < HPG) {
+                float uh = L.up[0];
+#pragma unroll
+                for (int hh = 1; hh < HPG; ++hh) uh = h == hh ? L.up[hh] : uh;
+                const float bz = dz[nt][0] + dz[nt][1];  // sum_j q'_hj z_j (hi + lo)
                 const int ta = mt * 16 + r, tb = ta + 8;
-                if (ta < ntok) out[h * ld + t0 + ta] = fmaf((d[nt][0] + d[nt][1]) + loa, kScale, bh);
-                if (tb < ntok) out[h * ld + t0 + tb] = fmaf((d[nt][2] + d[nt][3]) + lob, kScale, bh);
+                if (ta < ntok) out[h * ld + t0 + ta] = ((d[nt][0] + d[nt][1]) + bz) * uh;
+                if (tb < ntok) out[h * ld + t0 + tb] = ((d[nt][2] + d[nt][3]) + bz) * uh;
             }
         }
     }
@@ -238,18 +219,7 @@ __device__ __forceinline__ void score_slab_mma(const LaneConst<HPG>& L, const ui
 // per ring slot.  No CTA-wide barrier in the main loop.
 template <int HPG>
 constexpr size_t mma_smem() {
-    return (size_t)kMmaWarps * kMmaStages * (kSlabBytes + kParBytes) + (size_t)kMmaWarps * MmaTraits<HPG>::BTILE +
-           (size_t)kMmaWarps * kMmaStages * 8;
-}
-
-__device__ __forceinline__ float pow2f(int k) { return __int_as_float((k + 127) << 23); }  // -126 <= k <= 127
-
-template <typename T, int HPG>
-__device__ __forceinline__ void lane_q(const T* qg, const int (&ch)[4], const float (&dn)[4], LaneConst<HPG>& L) {
-#pragma unroll
-    for (int u = 0; u < 4; ++u)
-#pragma unroll
-        for (int h = 0; h < HPG; ++h) L.qp[h][u] = to_f32(qg[h * 128 + ch[u]]) * dn[u];
+    return (size_t)kMmaWarps * kMmaStages * kStage + (size_t)kMmaWarps * kMmaStages * 8;
 }
 
 template <typename T, int HPG>
@@ -260,26 +230,10 @@ __global__ void __launch_bounds__(kMmaWarps * 32) score_mma_kernel(const T* __re
     extern __shared__ __align__(128) uint8_t smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int g = 32 << lg;  // group size, a power of two >= 32 (lg = log2(g / 32))
-    uint8_t* ring = smem + (size_t)warp * kMmaStages * (kSlabBytes + kParBytes);  // [slot] {bits, params}
-    uint8_t* btiles = smem + (size_t)kMmaWarps * kMmaStages * (kSlabBytes + kParBytes);
-    uint8_t* btile = btiles + (size_t)warp * MmaTraits<HPG>::BTILE;
-    uint64_t* full = reinterpret_cast<uint64_t*>(btiles + (size_t)kMmaWarps * MmaTraits<HPG>::BTILE) +
+    uint8_t* ring = smem + (size_t)warp * kMmaStages * kStage;  // [slot] {bits, params}
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)kMmaWarps * kMmaStages * kStage) +
                      warp * kMmaStages;
-    // zero this warp's B tile once: columns >= 3*HPG stay zero
-    for (int i = lane; i < MmaTraits<HPG>::BTILE / 16; i += 32)
-        reinterpret_cast<uint4*>(btile)[i] = make_uint4(0, 0, 0, 0);
-
-    // per-lane slot constants (independent of the sequence)
-    LaneConst<HPG> L;
-    float dn[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-        const int ks = 4 * lane + u;
-        L.ch[u] = kslot_channel(ks);
-        const int e = kslot_exp(ks);
-        L.up[u] = pow2f(e + kSigma);
-        dn[u] = pow2f(-e - kSigma);
-    }
+    LaneConst<HPG> L;  // per (sequence, kv head): lane_q
 
     const int nslabs = (tokens + 31) >> 5;
     // slabs [open0, nslabs) overlap the group re-packed by the fused append
@@ -318,7 +272,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32) score_mma_kernel(const T* __re
                 Vseq[(int64_t)ap.pos * 128 + threadIdx.x] = vr;
             }
             __syncthreads();
-            lane_q<T, HPG>(q + ((int64_t)b * hq + h * HPG) * 128, L.ch, dn, L);
+            lane_q<T, HPG>(q + ((int64_t)b * hq + h * HPG) * 128, L);
             for (int slab = open0 + warp; slab < nslabs; slab += kMmaWarps) {
                 uint8_t* bs = ring;
                 uint8_t* ps = bs + kSlabBytes;
@@ -326,10 +280,10 @@ __global__ void __launch_bounds__(kMmaWarps * 32) score_mma_kernel(const T* __re
                 // coherent (L1-bypassing) reads of what this CTA just wrote
                 reinterpret_cast<uint4*>(bs)[lane] =
                     lane < ntok ? __ldcg(reinterpret_cast<const uint4*>(bseq) + t0 + lane) : make_uint4(0, 0, 0, 0);
-                reinterpret_cast<uint4*>(ps)[lane] =
+                reinterpret_cast<uint4*>(ps + (lane >> 3) * kParWordStride)[lane & 7] =
                     __ldcg(reinterpret_cast<const uint4*>(zseq + (int64_t)(slab >> lg) * 128) + lane);
                 __syncwarp();
-                score_slab_mma<HPG>(L, bs, ps, btile, t0, ntok, scores + ((int64_t)b * hq + h * HPG) * ld, ld);
+                score_slab_mma<HPG>(L, bs, ps, t0, ntok, scores + ((int64_t)b * hq + h * HPG) * ld, ld);
                 __syncwarp();
             }
             __syncthreads();
@@ -363,7 +317,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32) score_mma_kernel(const T* __re
     int iseq = (int)(w0 / open0), islab = (int)(w0 - (int64_t)iseq * open0);
     auto issue = [&](int slot) {  // lane 0
         const int t0 = islab * 32, ntok = min(32, tokens - t0);
-        uint8_t* dst = ring + (size_t)slot * (kSlabBytes + kParBytes);
+        uint8_t* dst = ring + (size_t)slot * kStage;
         mbar_arrive_expect_tx(&full[slot], (uint32_t)ntok * 16 + kParBytes);
         bulk_g2s_evict_first(dst, bits + ((int64_t)iseq * cap + t0) * 4, (uint32_t)ntok * 16, &full[slot], pol);
         bulk_g2s_evict_first(dst + kSlabBytes, sz + ((int64_t)iseq * G + (islab >> lg)) * 128, kParBytes,
@@ -378,22 +332,27 @@ __global__ void __launch_bounds__(kMmaWarps * 32) score_mma_kernel(const T* __re
         for (int s = 0; s < kMmaStages - 1 && s < n; ++s) issue(s);
     int seq = (int)(w0 / open0), slab = (int)(w0 - (int64_t)seq * open0);
     int b = seq / hkv, h = seq - b * hkv;
-    lane_q<T, HPG>(q + ((int64_t)b * hq + h * HPG) * 128, L.ch, dn, L);
+    lane_q<T, HPG>(q + ((int64_t)b * hq + h * HPG) * 128, L);
     float* out = scores + ((int64_t)b * hq + h * HPG) * ld;
     for (int i = 0; i < n; ++i) {
         const int slot = i % kMmaStages;
         if (lane == 0 && i + kMmaStages - 1 < n) issue((i + kMmaStages - 1) % kMmaStages);
         mbar_wait(&full[slot], (uint32_t)((i / kMmaStages) & 1));
-        const uint8_t* stg = ring + (size_t)slot * (kSlabBytes + kParBytes);
+        uint8_t* stg = ring + (size_t)slot * kStage;
         const int t0 = slab * 32;
-        score_slab_mma<HPG>(L, stg, stg + kSlabBytes, btile, t0, min(32, tokens - t0), out, ld);
+        {  // skewed copy of the group's (s, z) row (see kParWordStride)
+            const uint4 v = reinterpret_cast<const uint4*>(stg + kSlabBytes)[lane];
+            reinterpret_cast<uint4*>(stg + kSlabBytes + kParBytes + (lane >> 3) * kParWordStride)[lane & 7] = v;
+            __syncwarp();
+        }
+        score_slab_mma<HPG>(L, stg, stg + kSlabBytes + kParBytes, t0, min(32, tokens - t0), out, ld);
         __syncwarp();  // every lane is done with `slot` before lane 0 refills it
         if (++slab == open0 && i + 1 < n) {
             slab = 0;
             ++seq;
             b = seq / hkv;
             h = seq - b * hkv;
-            lane_q<T, HPG>(q + ((int64_t)b * hq + h * HPG) * 128, L.ch, dn, L);
+            lane_q<T, HPG>(q + ((int64_t)b * hq + h * HPG) * 128, L);
             out = scores + ((int64_t)b * hq + h * HPG) * ld;
         }
     }
