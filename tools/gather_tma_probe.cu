@@ -5,6 +5,8 @@
 //   B  one cp.async.bulk per row (256 B, mbarrier completion), lanes 0..15 issue
 //   C  TMA tile::gather4: one cp.async.bulk.tensor ... tile::gather4 per 4 rows (a 2D tensor
 //     map over the [H*L][128] bf16 cache, box 128 x 1), lanes 0..3 issue
+//   D  the same with the layout ldmatrix needs: box 64 x 1 with the 128-byte swizzle, two
+//     gather4 per 4 rows (the 256-B rows cannot be swizzled in one box)
 // CTAs of 4 warps, 112 rows per warp (the K4 split), ring of NST stages.  In-kernel
 // globaltimer first start .. last end (no launch overhead), L2 flushed with clean lines.
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -o tools/gather_tma_probe tools/gather_tma_probe.cu
@@ -96,6 +98,24 @@ __global__ void __launch_bounds__(128) gather(const uint16_t* K, const uint16_t*
                             su32(dst + 4096 + lane * 256)),
                         "l"(V + off), "r"(bar)
                         : "memory");
+                }
+                if (MODE == 3 && lane < ROWS / 4) {
+                    int rw[4];
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) rw[j] = head * L + s[rb + min(4 * lane + j, nr - 1)];
+#pragma unroll
+                    for (int hh = 0; hh < 2; ++hh) {
+                        asm volatile(
+                            "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+                            " [%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(su32(dst + hh * 2048 + lane * 512)),
+                            "l"(&tk), "r"(bar), "r"(64 * hh), "r"(rw[0]), "r"(rw[1]), "r"(rw[2]), "r"(rw[3])
+                            : "memory");
+                        asm volatile(
+                            "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+                            " [%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(su32(dst + 4096 + hh * 2048 + lane * 512)),
+                            "l"(&tv), "r"(bar), "r"(64 * hh), "r"(rw[0]), "r"(rw[1]), "r"(rw[2]), "r"(rw[3])
+                            : "memory");
+                    }
                 }
                 if (MODE == 2 && lane < ROWS / 4) {
                     int rw[4];
@@ -206,7 +226,7 @@ int main() {
     EncodeTiled enc = nullptr;
     cudaDriverEntryPointQueryResult q;
     cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", reinterpret_cast<void**>(&enc), cudaEnableDefault, &q);
-    CUtensorMap tk{}, tv{};
+    CUtensorMap tk{}, tv{}, tk2{}, tv2{};
     const cuuint64_t dims[2] = {(cuuint64_t)D, (cuuint64_t)H * L};
     const cuuint64_t strides[1] = {(cuuint64_t)D * 2};
     const cuuint32_t box[2] = {(cuuint32_t)D, 1};
@@ -219,7 +239,14 @@ int main() {
              enc(&tv, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, V, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
                  CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
                  CUDA_SUCCESS;
-    printf("tensor maps: %s\n", ok ? "ok" : "FAILED");
+    const cuuint32_t box2[2] = {64, 1};
+    int ok2 = ok && enc(&tk2, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, K, dims, strides, box2, es,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS &&
+              enc(&tv2, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, V, dims, strides, box2, es,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+    printf("tensor maps: %s, swizzled: %s\n", ok ? "ok" : "FAILED", ok2 ? "ok" : "FAILED");
     for (int pass = 0; pass < 2; ++pass) {
         printf("pass %d (C2 selection: %d heads x %d rows of K and V, %.1f MB)\n", pass, H, N, H * N * 512 / 1e6);
         run<0, 2>("A cp.async 16 B", K, V, sel, tk, tv, tt, out, fl, fn);
@@ -229,6 +256,10 @@ int main() {
         if (ok) {
             run<2, 2>("C TMA tile::gather4", K, V, sel, tk, tv, tt, out, fl, fn);
             run<2, 3>("C TMA tile::gather4", K, V, sel, tk, tv, tt, out, fl, fn);
+        }
+        if (ok2) {
+            run<3, 2>("D TMA gather4, 64-col swizzled boxes", K, V, sel, tk2, tv2, tt, out, fl, fn);
+            run<3, 3>("D TMA gather4, 64-col swizzled boxes", K, V, sel, tk2, tv2, tt, out, fl, fn);
         }
     }
     printf("status: %s\n", cudaGetErrorString(cudaGetLastError()));
