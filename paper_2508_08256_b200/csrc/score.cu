@@ -173,8 +173,13 @@ __global__ void __launch_bounds__(kScoreWarps * 32) score128_kernel(
             vr = static_cast<const T*>(ap.v_new)[seq * D + threadIdx.x];
         }
         flag_query<HPG>(qv, ap.nonfinite);
-        pack_group<T>(Kseq, D, 4, g, ap.pos / g, ap.pos + 1, bseq, zseq, ap.nonfinite,
-                      static_cast<const T*>(ap.k_new) + seq * D, ap.pos);
+        // the compact open-group re-pack of the fused step (pack.cuh): the general pack_group
+        // inlined here grew the appending CTA's cold code path (C1 score+append 7.4 -> 9.7 us)
+        const float xn = own ? to_f32(kr) : 0.f;
+        if (ap.nonfinite && threadIdx.x < 32 * ((D + 31) / 32) &&
+            __any_sync(0xffffffffu, own && !isfinite(xn)) && (threadIdx.x & 31) == 0)
+            atomicOr(ap.nonfinite, 1);  // "quantize: non-finite key entry" (quant1bit.hpp:68), the new row
+        pack_open_group<T>(Kseq, D, g, ap.pos / g, ap.pos + 1, bseq, zseq, xn, ap.pos);
         if (own) {
             Kseq[(int64_t)ap.pos * D + threadIdx.x] = kr;
             Vseq[(int64_t)ap.pos * D + threadIdx.x] = vr;

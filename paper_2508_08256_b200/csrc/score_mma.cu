@@ -265,8 +265,12 @@ __global__ void __launch_bounds__(kMmaWarps * 32) score_mma_kernel(const T* __re
                     bad |= !isfinite(to_f32(q[((int64_t)b * hq + h * HPG) * 128 + i]));
                 if (__any_sync(0xffffffffu, bad) && threadIdx.x == 0) atomicOr(ap.nonfinite, 2);
             }
-            pack_group<T>(Kseq, 128, 4, g, ap.pos >> (5 + lg), ap.pos + 1, bseq, zseq, ap.nonfinite,
-                          static_cast<const T*>(ap.k_new) + (int64_t)seq * 128, ap.pos);
+            // the compact open-group re-pack (pack.cuh), the new row's non-finite check first
+            const float xn = own ? to_f32(kr) : 0.f;
+            if (ap.nonfinite && threadIdx.x < 128 && __any_sync(0xffffffffu, !isfinite(xn)) &&
+                (threadIdx.x & 31) == 0)
+                atomicOr(ap.nonfinite, 1);  // "quantize: non-finite key entry" (quant1bit.hpp:68)
+            pack_open_group<T>(Kseq, 128, g, ap.pos >> (5 + lg), ap.pos + 1, bseq, zseq, xn, ap.pos);
             if (own) {
                 Kseq[(int64_t)ap.pos * 128 + threadIdx.x] = kr;
                 Vseq[(int64_t)ap.pos * 128 + threadIdx.x] = vr;
