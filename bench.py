@@ -432,7 +432,9 @@ def run_ours(args, cfg, world, rank, local):
         # rows through L2); U = B*Hq*n for MHA
         "sparse_attn": unique_rows * d * 2 * es + qo,
         "append": B * Hkv * (g * d * es + 2 * d * es + g * d // 8 + d * 4),
-        "topk": None,
+        # the scratch scores are read at least once (not SURVEY §8(d) algorithmic bytes of the
+        # step, but what bounds a Top-k kernel from below)
+        "topk": B * Hq * (pos + 1) * 4,
     }
     pk_u, kv_u, qo_u = algorithmic_bytes(cfg, unique_rows)
     dom = max(per, key=per.get)
@@ -451,7 +453,8 @@ def run_ours(args, cfg, world, rank, local):
     t_dom = fused_us if dom == "fused_step" else per.get(dom)
     if alg.get(dom):
         ach = alg[dom] / (t_dom * 1e-6) / 1e9
-        roof = {"bound": "hbm", "kernel": "step_fused_kernel" if dom == "fused_step" else dom,
+        roof = {"bound": "hbm" if dom != "topk" else "latency (hbm bytes: one read of the scratch scores)",
+                "kernel": "step_fused_kernel" if dom == "fused_step" else dom,
                 "achieved": round(ach, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(ach / peak, 4), "traffic": traffic, "alg_bytes": alg[dom],
                 "launch_us": round(t_dom, 3), "peak_source": peak_src}
