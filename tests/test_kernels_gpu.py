@@ -284,7 +284,7 @@ def test_c2_shape_step_properties(cuda, port):
 @pytest.mark.parametrize("g,L,dtype", [(32, 1000, "bf16"), (64, 777, "f16"), (128, 2085, "f32"),
                                        (32, 31, "bf16"), (32, 8193, "bf16")])
 def test_score_tensor_core_shapes(cuda, port, hpg, g, L, dtype):
-    """K2 (tensor-core exponent-bit scorer, d = 128): every GQA ratio, g in {32, 64, 128},
+    """K2 (tensor-core sign-select scorer, d = 128): every GQA ratio, g in {32, 64, 128},
     ragged token counts, against approx_scores over the FIER round trip."""
     F = fier()
     torch.manual_seed(hpg * 1000 + L)
@@ -497,3 +497,34 @@ def test_topk_wide_grid(cuda, port, rows, l, k):
         else:
             want = port.topk(v, k)
         np.testing.assert_array_equal(wide[r], want, err_msg=f"row {r}")
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "f16", "f32"])
+def test_score_tensor_core_extremes(cuda, port, dtype):
+    """The sign-select scorer's operand ranges: per-head query scales 2^-20 .. 2^20 (2^-10 .. 2^10
+    for fp16 queries; the fp16 q pieces are scaled by 2^-e per head), channels spanning 2^-10 ..
+    2^10 inside one head, zero
+    heads, constant key groups (s = 0), groups with a large spread (s near the fp16 range), and
+    negative / positive offsets z -- all within the 1e-3 score tolerance of approx_scores."""
+    F = fier()
+    g_ = torch.Generator().manual_seed(7)
+    dt, B, Hkv, hpg, L, d, g = TDT[dtype], 1, 2, 4, 160, 128, 32
+    K = torch.randn(B, Hkv, L, d, generator=g_) * 2
+    K[0, 0, 0:32] = 3.25                                   # constant group: s = 0
+    K[0, 0, 32:64] *= 1500.0                               # large spread: s ~ 1e3..1e4
+    K[0, 1, 64:96] += 200.0                                # positive offsets
+    K[0, 1, 96:128] -= 300.0                               # negative offsets
+    q = torch.randn(B, Hkv * hpg, d, generator=g_)
+    big = 10 if dtype == "f16" else 20                     # (fp16 queries overflow past 2^16)
+    q[0, 0] *= 2.0 ** big
+    q[0, 1] *= 2.0 ** -big
+    q[0, 2] = 0.0
+    q[0, 3] *= torch.logspace(-big // 2, big // 2, d, base=2.0)  # dynamic range inside one head
+    q[0, 5] *= 2.0 ** (big // 2)
+    pk = F.quantize(K.to(dt).to(cuda), g)
+    qd = q.to(dt).to(cuda)
+    s = F.approx_scores(qd, pk).cpu().numpy().astype(np.float64)
+    for h in range(Hkv * hpg):
+        kv = h // hpg
+        ref = port.approx_scores_fier(qd[0, h].double().cpu().numpy(), pk.to_fier(0, kv))
+        assert score_err(s[0, h], ref) <= SCORE_TOL, h
