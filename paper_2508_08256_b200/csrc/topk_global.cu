@@ -31,7 +31,8 @@
 namespace fier_cuda {
 
 constexpr int kTgSlice = 8192;     // keys per chunk of the streaming passes (8 float4 per thread)
-constexpr int kTgChunks = 4;       // chunks per CTA of K3g-1 / K3g-2 (fewer global atomics)
+constexpr int kTgChunks = 4;       // chunks per CTA of K3g-1 (fewer global histogram atomics)
+constexpr int kTgChunksC = 1;      // chunks per CTA of K3g-2 (more CTAs in flight: C5 collect 96 -> 82 us)
 constexpr int kTgThreads = 256;    // streaming passes: 32 keys per thread, all loads in flight
 constexpr int kTgRowThreads = 512; // K3g-3
 constexpr int kTgBins = kRxBins;   // digit 1 (4096 bins)
@@ -162,8 +163,8 @@ __global__ void __launch_bounds__(kTgThreads, 4) tg_collect_kernel(const float* 
     constexpr int TILE = 4 * kTgThreads, U = kTgSlice / TILE, NW = kTgThreads / 32;
     __shared__ uint32_t wa[NW], wc[NW], base[2];
     const int row = blockIdx.y, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    for (int cc = kTgChunks - 1; cc >= 0; --cc) {  // reverse order: the last pass's tail is in L2
-        const int slice = (gridDim.x - 1 - blockIdx.x) * kTgChunks + cc;
+    for (int cc = kTgChunksC - 1; cc >= 0; --cc) {  // reverse order: the last pass's tail is in L2
+        const int slice = (gridDim.x - 1 - blockIdx.x) * kTgChunksC + cc;
         const int s0 = slice * kTgSlice, s1 = min(s0 + kTgSlice, tokens);
         if (s0 >= s1) continue;  // block-uniform
         TgRow& st = state[row];
@@ -668,7 +669,8 @@ int topk_global_dispatch(const float* scores, int rows, int tokens, int64_t ld, 
     const dim3 grid((unsigned)ceil_div(tokens, (int64_t)kTgSlice * kTgChunks), (unsigned)rows);
     tg_hist_kernel<<<grid, kTgThreads, 0, st>>>(scores, tokens, ld, k, hist, state);
     if (int rc = check_launch("fier_topk")) return rc;
-    tg_collect_kernel<<<grid, kTgThreads, 0, st>>>(scores, tokens, ld, k, L.cap, state, above, ckey, cidx);
+    const dim3 gridc((unsigned)ceil_div(tokens, (int64_t)kTgSlice * kTgChunksC), (unsigned)rows);
+    tg_collect_kernel<<<gridc, kTgThreads, 0, st>>>(scores, tokens, ld, k, L.cap, state, above, ckey, cidx);
     if (int rc = check_launch("fier_topk")) return rc;
     static const bool attr = [] {
         cudaFuncSetAttribute(tg_row_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(TgRowShared));
