@@ -364,7 +364,7 @@ __global__ void __launch_bounds__(kTgRowThreads) tg_row_kernel(const float* __re
     extern __shared__ __align__(16) uint8_t smem_raw[];
     TgRowShared& S = *reinterpret_cast<TgRowShared*>(smem_raw);
     constexpr int NT = kTgRowThreads;
-    const int row = blockIdx.x, tid = threadIdx.x;
+    const int row = blockIdx.y, tid = threadIdx.x;  // blockIdx.x: this CTA's index window
     const TgRow st = state[row];
     int32_t* out = sel + (int64_t)row * k;
     const uint32_t nab = st.nabove, nc = st.ncand;
@@ -418,40 +418,44 @@ __global__ void __launch_bounds__(kTgRowThreads) tg_row_kernel(const float* __re
     }
     const uint32_t T = S.res[4];
     const int32_t idxT = (int32_t)S.res[5];
-    // ---- ascending output: the kept indices (the above list and the kept candidates) set
-    // bits of a bitmap over a window of kTgWin indices; popcount prefix sums place them.
-    // Rows longer than the window take several windows. ----
+    // ---- ascending output: the kept indices (the above list and the kept candidates) in
+    // this CTA's window of kTgWin indices set bits of a bitmap; the kept indices below the
+    // window give its first output slot; popcount prefix sums place the rest.  One CTA per
+    // window (every CTA of a row redoes the small threshold search above). ----
     const int32_t* ab = above + (size_t)row * k;
-    uint32_t run = 0;
     constexpr int WPT = kTgWin / 32 / NT;  // bitmap words per thread of a full window
     const int wpt = min(WPT, ((tokens + 31) / 32 + NT - 1) / NT);  // short rows: a smaller window
     const int win = 32 * NT * wpt;
-    for (int w0 = 0; w0 < tokens; w0 += win) {
-        for (int i = tid; i < win / 32; i += NT) S.bm[i] = 0u;
-        __syncthreads();
-        for (uint32_t i = tid; i < nab; i += NT) {
-            const int32_t x = ab[i] - w0;
-            if (x >= 0 && x < win) atomicOr(&S.bm[x >> 5], 1u << (x & 31));
-        }
-        for (uint32_t i = tid; i < nc; i += NT) {
-            const uint32_t kk = gk[i];
-            const int32_t ix = gi[i], x = ix - w0;
-            if ((kk > T || (kk == T && ix <= idxT)) && x >= 0 && x < win) atomicOr(&S.bm[x >> 5], 1u << (x & 31));
-        }
-        __syncthreads();
-        uint32_t wv[WPT], c = 0;
-#pragma unroll
-        for (int j = 0; j < WPT; ++j) {
-            wv[j] = j < wpt ? S.bm[tid * wpt + j] : 0u;
-            c += __popc(wv[j]);
-        }
-        uint32_t tot = 0;
-        uint32_t o = run + tg_scan<NT>(c, S, &tot);
-#pragma unroll
-        for (int j = 0; j < WPT; ++j)
-            for (uint32_t m = wv[j]; m; m &= m - 1) out[o++] = w0 + 32 * (tid * wpt + j) + __ffs(m) - 1;
-        run += tot;
+    const int w0 = blockIdx.x * win;
+    if (w0 >= tokens) return;  // block-uniform
+    for (int i = tid; i < win / 32; i += NT) S.bm[i] = 0u;
+    __syncthreads();
+    uint32_t below = 0;
+    for (uint32_t i = tid; i < nab; i += NT) {
+        const int32_t x = ab[i] - w0;
+        below += x < 0;
+        if (x >= 0 && x < win) atomicOr(&S.bm[x >> 5], 1u << (x & 31));
     }
+    for (uint32_t i = tid; i < nc; i += NT) {
+        const uint32_t kk = gk[i];
+        const int32_t ix = gi[i], x = ix - w0;
+        const bool kept = kk > T || (kk == T && ix <= idxT);
+        below += kept && x < 0;
+        if (kept && x >= 0 && x < win) atomicOr(&S.bm[x >> 5], 1u << (x & 31));
+    }
+    uint32_t run = 0;
+    tg_scan<NT>(below, S, &run);  // (the scan's total = the kept indices below the window)
+    uint32_t wv[WPT], c = 0;
+#pragma unroll
+    for (int j = 0; j < WPT; ++j) {
+        wv[j] = j < wpt ? S.bm[tid * wpt + j] : 0u;
+        c += __popc(wv[j]);
+    }
+    uint32_t tot = 0;
+    uint32_t o = run + tg_scan<NT>(c, S, &tot);
+#pragma unroll
+    for (int j = 0; j < WPT; ++j)
+        for (uint32_t m = wv[j]; m; m &= m - 1) out[o++] = w0 + 32 * (tid * wpt + j) + __ffs(m) - 1;
 }
 
 // ---- K3r: one CTA per row, for launches of many short rows (C4: 1024 rows x 32768) ----
@@ -677,7 +681,8 @@ int topk_global_dispatch(const float* scores, int rows, int tokens, int64_t ld, 
         return true;
     }();
     (void)attr;
-    tg_row_kernel<<<rows, kTgRowThreads, sizeof(TgRowShared), st>>>(scores, tokens, ld, k, L.cap, state, above,
+    const int wins = (int)ceil_div(tokens, (int64_t)kTgWin);  // CTAs per row: one per index window
+    tg_row_kernel<<<dim3((unsigned)wins, (unsigned)rows), kTgRowThreads, sizeof(TgRowShared), st>>>(scores, tokens, ld, k, L.cap, state, above,
                                                                     ckey, cidx, sel);
     return check_launch("fier_topk");
 }
