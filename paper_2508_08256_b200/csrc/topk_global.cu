@@ -187,14 +187,21 @@ __global__ void __launch_bounds__(kTgThreads, 4) tg_collect_kernel(const float* 
                 fc |= (uint32_t)(ok && d == b1) << (4 * u + j);
             }
         }
-        // per-warp counts, one CTA reservation per list, then coalesced writes: step b of every
-        // lane of the warp writes at the warp's running offset (ballot ranks)
-        const uint32_t lt = t2_lanemask_lt();
-        const uint32_t na = __reduce_add_sync(0xffffffffu, (uint32_t)__popc(fa));
-        const uint32_t nc = __reduce_add_sync(0xffffffffu, (uint32_t)__popc(fc));
-        if (lane == 0) {
-            wa[warp] = na;
-            wc[warp] = nc;
+        // per-warp counts, one CTA reservation per list, then each lane writes its own flagged
+        // keys (few: a loop over set bits; the candidates' keys are re-read from L2) at its
+        // warp-exclusive offset -- a 32-step ballot loop per chunk cost ~10 instructions per key
+        uint32_t pa = __popc(fa), pc = __popc(fc);  // -> inclusive prefix over lanes
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t ya = __shfl_up_sync(0xffffffffu, pa, o), yc = __shfl_up_sync(0xffffffffu, pc, o);
+            if (lane >= o) {
+                pa += ya;
+                pc += yc;
+            }
+        }
+        if (lane == 31) {
+            wa[warp] = pa;
+            wc[warp] = pc;
         }
         __syncthreads();
         if (tid == 0) {
@@ -210,29 +217,17 @@ __global__ void __launch_bounds__(kTgThreads, 4) tg_collect_kernel(const float* 
             base[1] = tc ? atomicAdd(&st.ncand, tc) : 0u;
         }
         __syncthreads();
-        uint32_t oa = base[0] + wa[warp], oc = base[1] + wc[warp];
+        uint32_t oa = base[0] + wa[warp] + pa - __popc(fa), oc = base[1] + wc[warp] + pc - __popc(fc);
         int32_t* ab = above + (size_t)row * k;
         uint32_t* ck = ckey + (size_t)row * cap;
         int32_t* ci = cidx + (size_t)row * cap;
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const int i = s0 + u * TILE + 4 * tid;
-            const float e[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                const int b = 4 * u + j;
-                const bool a = (fa >> b) & 1u, c = (fc >> b) & 1u;
-                const uint32_t ma = __ballot_sync(0xffffffffu, a), mc = __ballot_sync(0xffffffffu, c);
-                if (a) ab[oa + __popc(ma & lt)] = i + j;  // < k by the choice of b1
-                if (c) {
-                    const uint32_t slot = oc + __popc(mc & lt);
-                    if (slot < (uint32_t)cap) {
-                        ck[slot] = score_key(e[j]);
-                        ci[slot] = i + j;
-                    }
-                }
-                oa += __popc(ma);
-                oc += __popc(mc);
+        auto index_of = [&](int b) { return s0 + (b >> 2) * TILE + 4 * tid + (b & 3); };
+        for (uint32_t m = fa; m; m &= m - 1) ab[oa++] = index_of(__ffs(m) - 1);  // < k by the choice of b1
+        for (uint32_t m = fc; m; m &= m - 1, ++oc) {
+            if (oc < (uint32_t)cap) {
+                const int ix = index_of(__ffs(m) - 1);
+                ck[oc] = score_key(__ldg(srow + ix));
+                ci[oc] = ix;
             }
         }
         __syncthreads();  // wa / wc / base are reused by the next chunk
