@@ -519,31 +519,47 @@ __global__ void __launch_bounds__(kTrThreads) tr_row_kernel(const float* __restr
         tg_row_exact<NT>(srow, tokens, k, out, S);
         return;
     }
-    const uint32_t lt = t2_lanemask_lt();
     for (int c0 = 0; c0 < tokens; c0 += CH) {
-        float4 v[CH / (4 * NT)];
+        constexpr int U = CH / (4 * NT);
+        float4 v[U];
         tg_load(srow, c0, min(c0 + CH, tokens), v);
+        uint32_t fa = 0, fc = 0;  // bit 4u + j: key j of float4 u is above b1 / a candidate
 #pragma unroll
-        for (int u = 0; u < CH / (4 * NT); ++u) {
+        for (int u = 0; u < U; ++u) {
             const int i = c0 + u * 4 * NT + 4 * tid;
             const float e[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
-                const uint32_t kj = score_key(e[j]), d = kj >> 20;
+                const uint32_t d = score_key(e[j]) >> 20;
                 const bool ok = i + j < tokens;
-                if (ok && d > b1) atomicOr(&S.bm[(i + j) >> 5], 1u << ((i + j) & 31));
-                const bool c = ok && d == b1;
-                const uint32_t m = __ballot_sync(0xffffffffu, c);
-                if (m) {
-                    uint32_t base = 0;
-                    if (lane == __ffs(m) - 1) base = atomicAdd(&S.ncand, (uint32_t)__popc(m));
-                    base = __shfl_sync(0xffffffffu, base, __ffs(m) - 1);
-                    const uint32_t slot = base + __popc(m & lt);
-                    if (c && slot < (uint32_t)kTrCand) {
-                        S.ck[slot] = kj;
-                        S.ci[slot] = i + j;
-                    }
-                }
+                fa |= (uint32_t)(ok && d > b1) << (4 * u + j);
+                fc |= (uint32_t)(ok && d == b1) << (4 * u + j);
+            }
+        }
+        // above b1: a float4's 4 tokens share one bitmap word -- one atomic per nibble
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint32_t nib = (fa >> (4 * u)) & 0xFu;
+            const int i = c0 + u * 4 * NT + 4 * tid;
+            if (nib) atomicOr(&S.bm[i >> 5], nib << (i & 31));
+        }
+        // candidates: each lane writes its own (few) at a warp-exclusive offset; keys re-read (L2)
+        uint32_t pc = __popc(fc);
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, pc, o);
+            if (lane >= o) pc += y;
+        }
+        uint32_t base = 0;
+        if (lane == 31 && pc) base = atomicAdd(&S.ncand, pc);
+        base = __shfl_sync(0xffffffffu, base, 31);
+        uint32_t slot = base + pc - __popc(fc);
+        for (uint32_t m = fc; m; m &= m - 1, ++slot) {
+            const int b = __ffs(m) - 1;
+            const int ix = c0 + (b >> 2) * 4 * NT + 4 * tid + (b & 3);
+            if (slot < (uint32_t)kTrCand) {
+                S.ck[slot] = score_key(__ldg(srow + ix));
+                S.ci[slot] = ix;
             }
         }
     }
