@@ -498,14 +498,24 @@ __device__ __forceinline__ void rx_partition(const Keys& keys, int s0, int wbase
                                              RxPublished& P, uint32_t* amask, uint32_t* kmask, uint16_t* alist) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int kpt = keys.count();
-    uint32_t mine = 0, above = 0, myw = 0;  // lane j keeps the above-mask of slot j
+    uint32_t mine = 0, fa = 0, myw = 0;  // lane j keeps the above-mask of slot j
     t2_for_keys(keys, [&](int j, uint32_t kj) {
         const uint32_t d = kj ? kj >> 20 : 0u;  // empty slots: never above, never candidates
         mine |= (uint32_t)(kj != 0u && d == b1) << j;
-        const uint32_t m = __ballot_sync(0xffffffffu, kj != 0u && d > b1);
+        const bool a = kj != 0u && d > b1;
+        fa |= (uint32_t)a << j;
+        const uint32_t m = __ballot_sync(0xffffffffu, a);
         myw = lane == j ? m : myw;
-        above += __popc(m);
     });
+    const uint32_t na = __popc(fa);
+    uint32_t pa = na;  // inclusive prefix over lanes of the keys above b1
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, pa, o);
+        if (lane >= o) pa += y;
+    }
+    const uint32_t above = __shfl_sync(0xffffffffu, pa, 31);
+    T2_MARK(18);
     if (lane < kpt) {
         amask[warp * kpt + lane] = myw;
         kmask[warp * kpt + lane] = 0u;
@@ -533,18 +543,19 @@ __device__ __forceinline__ void rx_partition(const Keys& keys, int s0, int wbase
             }
         }
     }
+    T2_MARK(19);
     __syncthreads();
+    T2_MARK(20);
+    // the gather list: each lane writes its own keys above b1 (a set-bit loop) at its
+    // warp's offset + its exclusive prefix -- lane-major inside a warp (the attention does
+    // not need index order; the selection itself is written from the per-slot masks)
     uint32_t run = 0;
     for (int w = 0; w < warp; ++w) run += S.wab[w];
-    const uint32_t lt = t2_lanemask_lt();
-    for (int j = 0; j < kpt; ++j) {
-        const uint32_t m = __shfl_sync(0xffffffffu, myw, j);
-        if ((m >> lane) & 1u) alist[run + __popc(m & lt)] = (uint16_t)(wbase + 32 * j + lane);
-        run += __popc(m);
-    }
-    if (tid == NT - 1) {  // the last warp's running count is the CTA's total
-        P.pub[1] = run;
-        S.nabove = run;
+    uint32_t o = run + pa - na;
+    for (uint32_t m = fa; m; m &= m - 1) alist[o++] = (uint16_t)(wbase + 32 * (__ffs(m) - 1) + lane);
+    if (tid == NT - 1) {  // the last warp's end is the CTA's total
+        P.pub[1] = run + above;
+        S.nabove = run + above;
     }
 }
 

@@ -24,7 +24,7 @@ from paper_2508_08256_b200 import _lib  # noqa: E402
 
 NAMES = ["start", "append", "score", "resolve", "emit", "gather", "merge_sync", "out",
          "t:hist_sync", "t:find_bin", "t:partition", "t:cand_sync", "t:cand_gather", "t:rank", "t:merged", "g:above_done",
-         "-", "cta_scored", "-", "-", "-", "-", "-", "-"]
+         "-", "cta_scored", "p:keys", "p:cands", "p:sync", "-", "-", "-"]
 
 
 def main():
