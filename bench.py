@@ -506,7 +506,7 @@ def run_sharded(args, cfg, world, rank, local):
     import torch
     import torch.distributed as dist
 
-    from paper_2508_08256_b200.shard import DistExchange, ShardedDecodeLayer, sharded_step
+    from paper_2508_08256_b200.shard import DistExchange, NcclDeviceExchange, ShardedDecodeLayer, sharded_step
 
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
@@ -526,7 +526,10 @@ def run_sharded(args, cfg, world, rank, local):
     vn = torch.randn((B, Hkv, d), generator=gq, device=dev).to(dt)
     pos = L - 1
     shard.prefill(pos)
-    ex = DistExchange()
+    if args.exchange == "device":  # the NCCL device API: LSA stores into symmetric windows + LSA barrier
+        ex = NcclDeviceExchange(slot_bytes=max(2 * B * Hq * n * 4, B * Hq * (d + 1) * 4))
+    else:  # host-launched ncclAllGather (torch.distributed)
+        ex = DistExchange()
     stream = torch.cuda.Stream(device=dev)
     out_buf = torch.empty((B, Hq, d), dtype=torch.float32, device=dev)
 
@@ -599,6 +602,7 @@ def run_sharded(args, cfg, world, rank, local):
     ach = alg / (us * 1e-6) / 1e9
     info = {
         "graph": graph is not None,
+        "exchange": args.exchange,
         "roofline": {"bound": "hbm", "kernel": "sharded step of one rank (all kernels + 2 all-gathers)",
                      "achieved": round(ach, 1), "peak": peak, "unit": "GB/s", "frac": round(ach / peak, 4),
                      "traffic": None, "alg_bytes": alg, "peak_source": src,
@@ -731,6 +735,8 @@ def main():
     ap.add_argument("--config", default=None, choices=sorted(CONFIGS),
                     help="default: c2 at N = 1 (the headline), c5 sequence-sharded at N > 1")
     ap.add_argument("--sharded", action="store_true", help="c5: run the sharded protocol even at N = 1")
+    ap.add_argument("--exchange", default="nccl", choices=["nccl", "device"],
+                    help="sharded step: host-launched NCCL all-gathers, or the NCCL device-API kernel")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--layers", type=int, default=0, help="override the layer-rotation count")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -758,7 +764,7 @@ def main():
                 "scaling": "strong", "vs_baseline": None, "dtype": cfg["dtype"],
                 "data": "synthetic random-init Q/K/V (torch Philox), prefix index pre-packed",
                 "config": dict(config_block(args, cfg, world),
-                               parallelism=f"sequence-sharded x{world} (NCCL all-gathers, CUDA graph: "
+                               parallelism=f"sequence-sharded x{world} ({'NCCL device-API exchange' if info['exchange'] == 'device' else 'NCCL all-gathers'}, CUDA graph: "
                                            f"{info['graph']})",
                                l2="inputs larger than L2: each rank streams its whole slice (>= 134 MB of "
                                   "K/V + index per rank at N <= 8) every step"),

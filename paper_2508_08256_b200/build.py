@@ -84,6 +84,42 @@ def build(force: bool = False, verbose: bool = False, trace: bool = False) -> st
     return out_so
 
 
+NCCL_SRC = os.path.join(PKG, "csrc_nccl", "devx.cu")
+NCCL_OUT = os.path.join(PKG, "libfier_nccl.so")
+
+
+def nccl_root():
+    """The NCCL that torch ships (headers incl. the 2.28 device API, libnccl.so.2)."""
+    try:
+        import nvidia.nccl
+        for d in list(getattr(nvidia.nccl, "__path__", [])):
+            if os.path.exists(os.path.join(d, "include", "nccl_device.h")):
+                return d
+    except ImportError:
+        pass
+    return None
+
+
+def build_nccl(force: bool = False) -> str:
+    """libfier_nccl.so: the device-API exchange of the sharded step (include/fier_nccl.h).
+    Returns "" when no NCCL with the device API is installed."""
+    root = nccl_root()
+    if root is None:
+        return ""
+    deps = [NCCL_SRC, os.path.join(ROOT, "include", "fier_nccl.h"), __file__]
+    if not force and os.path.exists(NCCL_OUT) and os.path.getmtime(NCCL_OUT) > max(os.path.getmtime(f) for f in deps):
+        return NCCL_OUT
+    os.makedirs(BUILD, exist_ok=True)
+    obj = os.path.join(BUILD, "devx.cu.o")
+    subprocess.run([nvcc(), *ARCH, *FLAGS, "-I" + os.path.join(root, "include"), "-c", NCCL_SRC, "-o", obj], check=True)
+    lib = os.path.join(root, "lib")
+    tmp = NCCL_OUT + ".tmp"
+    subprocess.run([nvcc(), *ARCH, "-shared", "-o", tmp, obj, "-L" + lib, "-l:libnccl.so.2",
+                    "-Xlinker", "-rpath=" + lib], check=True)
+    os.replace(tmp, NCCL_OUT)
+    return NCCL_OUT
+
+
 SHIM_SRC = os.path.join(ROOT, "tests", "cpp", "shim_test.cpp")
 SHIM_BIN = os.path.join(ROOT, "tests", "cpp", "shim_test")
 

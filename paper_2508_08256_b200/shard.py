@@ -83,6 +83,87 @@ class HostStagedExchange(DistExchange):
         return torch.stack(parts).to(t.device)
 
 
+_NCCL_LIB = None
+
+
+def _nccl_lib():
+    """libfier_nccl.so (include/fier_nccl.h): the NCCL device-API exchange."""
+    global _NCCL_LIB
+    if _NCCL_LIB is None:
+        import os
+        path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libfier_nccl.so")
+        if not os.path.exists(path):
+            raise RuntimeError("libfier_nccl.so is not built (paper_2508_08256_b200.build.build_nccl)")
+        lib = C.CDLL(path)
+        lib.fier_devx_unique_id.argtypes = [C.c_void_p]
+        lib.fier_devx_create.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.c_size_t, C.c_int32,
+                                         C.POINTER(C.c_void_p)]
+        lib.fier_devx_allgather.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p, C.POINTER(C.c_void_p)]
+        lib.fier_devx_destroy.argtypes = [C.c_void_p]
+        lib.fier_devx_last_error.restype = C.c_char_p
+        _NCCL_LIB = lib
+    return _NCCL_LIB
+
+
+class _CudaBytes:
+    """A uint8 view of a device allocation owned elsewhere (__cuda_array_interface__)."""
+
+    def __init__(self, ptr: int, nbytes: int):
+        self.__cuda_array_interface__ = {"shape": (nbytes,), "typestr": "|u1", "data": (ptr, False), "version": 3}
+
+
+class NcclDeviceExchange:
+    """all_gather done on the device through the NCCL 2.28 device API: a kernel
+    stores this rank's slot into every peer's symmetric window over NVLink (LSA pointers) and
+    closes with an LSA barrier -- no host-side collective in the step, graph-capturable like
+    any launch.  `slot_bytes` bounds one rank's payload (the larger of the two exchanges)."""
+
+    def __init__(self, slot_bytes: int, group=None, max_ctas: int = 64):
+        import torch.distributed as dist
+        lib = _nccl_lib()
+        self.lib, self.group = lib, group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        uid = torch.zeros(128, dtype=torch.uint8)
+        if self.rank == 0:
+            check_devx(lib, lib.fier_devx_unique_id(uid.data_ptr()))
+        if self.world > 1:
+            on_gpu = dist.get_backend(group) == "nccl"
+            t = uid.cuda() if on_gpu else uid
+            dist.broadcast(t, src=0, group=group)
+            uid = t.cpu()
+        self.slot = (int(slot_bytes) + 4095) // 4096 * 4096
+        h = C.c_void_p()
+        check_devx(lib, lib.fier_devx_create(uid.data_ptr(), self.world, self.rank, self.slot, max_ctas,
+                                             C.byref(h)))
+        self.handle = h
+        self._win = None
+
+    def all_gather(self, t: torch.Tensor) -> torch.Tensor:
+        t = t.contiguous()
+        nbytes = t.numel() * t.element_size()
+        pad = (-nbytes) % 16
+        src = t if pad == 0 else torch.cat([t.view(torch.uint8).reshape(-1),
+                                            torch.zeros(pad, dtype=torch.uint8, device=t.device)])
+        out = C.c_void_p()
+        check_devx(self.lib, self.lib.fier_devx_allgather(self.handle, src.data_ptr(), nbytes + pad, _stream(),
+                                                          C.byref(out)))
+        if self._win is None:
+            self._win = torch.as_tensor(_CudaBytes(out.value, self.world * self.slot), device=t.device)
+        g = self._win.view(self.world, self.slot)[:, :nbytes]
+        return g.contiguous().view(t.dtype).reshape((self.world,) + tuple(t.shape))
+
+    def close(self):
+        if self.handle:
+            self.lib.fier_devx_destroy(self.handle)
+            self.handle = None
+
+
+def check_devx(lib, rc: int) -> None:
+    if rc:
+        raise RuntimeError(lib.fier_devx_last_error().decode())
+
+
 def _pack_candidates(cs: torch.Tensor, ci: torch.Tensor) -> torch.Tensor:
     return torch.stack([cs.view(torch.int32), ci])
 

@@ -228,3 +228,22 @@ def test_load_ratio_fier_matches_reference(l, g):
         assert r.value() == expect[(l, g)] and r.formula
     with pytest.raises(ValueError, match="load_ratio_fier: l and g must be >= 1"):
         F.load_ratio_fier(0, g)
+
+
+def test_nccl_exchange_library_exports_its_header():
+    """libfier_nccl.so (the NCCL device-API exchange, include/fier_nccl.h) loads without a GPU
+    and exports every declared function; built by __graft_entry__.build() where torch's NCCL
+    ships the device-API headers."""
+    import ctypes
+    import re
+    from paper_2508_08256_b200 import build as b
+    path = b.build_nccl()
+    if not path:
+        pytest.skip("no NCCL with the device API in this environment")
+    lib = ctypes.CDLL(path)
+    text = open(os.path.join(ROOT, "include", "fier_nccl.h")).read()
+    names = re.findall(r"FIER_API\s+[\w\s\*]+?\b(fier_devx_\w+)\s*\(", text)
+    assert len(names) == 5
+    for name in names:
+        assert hasattr(lib, name), name
+    assert b"sm_100a" in open(path, "rb").read()

@@ -309,3 +309,56 @@ def test_two_process_cuda_sharded_step(cuda, tmp_path, world, L, Hq, Hkv, n, dt)
     torch.cuda.synchronize()
     assert np.array_equal(outs[0]["sel"], s1.cpu().numpy()), "sharded selection differs from unsharded"
     assert np.allclose(outs[0]["out"], o1.cpu().numpy(), rtol=1e-4, atol=1e-5)
+
+
+def _devx_worker(rank, world, port_no, result_path):
+    """One rank: the NCCL device-API exchange (libfier_nccl.so) inside the sharded step."""
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port_no)
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import paper_2508_08256_b200 as F
+    from paper_2508_08256_b200.shard import NcclDeviceExchange, ShardedDecodeLayer, sharded_step
+    dev = torch.device("cuda", 0)
+    L, Hq, Hkv, d, g, n = 3000, 8, 2, 128, 32, 300
+    gen = torch.Generator(device="cpu").manual_seed(5)
+    K = torch.randn((1, Hkv, L, d), generator=gen).to(torch.bfloat16)
+    V = torch.randn((1, Hkv, L, d), generator=gen).to(torch.bfloat16)
+    q = torch.randn((1, Hq, d), generator=gen).to(torch.bfloat16).to(dev)
+    kn = torch.randn((1, Hkv, d), generator=gen).to(torch.bfloat16).to(dev)
+    vn = torch.randn((1, Hkv, d), generator=gen).to(torch.bfloat16).to(dev)
+    pos = L - 1
+    ex = NcclDeviceExchange(slot_bytes=2 * Hq * n * 8, group=None)
+    # the raw all-gather: slot r holds rank r's bytes
+    x = (torch.arange(1000, device=dev, dtype=torch.int32) + 7 * rank)
+    gx = ex.all_gather(x)
+    assert gx.shape == (world, 1000) and torch.equal(gx[rank], x)
+    s = ShardedDecodeLayer(1, Hq, Hkv, L, d, g, rank=rank, shards=world, dtype=torch.bfloat16, device=dev)
+    s.K[:, :, : s.end - s.start].copy_(K[:, :, s.start:s.end])
+    s.V[:, :, : s.end - s.start].copy_(V[:, :, s.start:s.end])
+    s.prefill(pos)
+    out = sharded_step(s, ex, q, kn, vn, pos, n)
+    torch.cuda.synchronize()
+    layer = F.DecodeLayer(1, Hq, Hkv, L, d, g, dtype=torch.bfloat16, device=dev, K=K.to(dev), V=V.to(dev))
+    layer.prefill(pos)
+    o1, s1 = layer.step(q, kn, vn, pos, n)
+    torch.cuda.synchronize()
+    ok = torch.equal(s.sel_global, s1) and torch.allclose(out, o1, rtol=1e-4, atol=1e-5)
+    np.savez(result_path + f".{rank}.npz", ok=ok)
+    ex.close()
+    dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_nccl_device_exchange_single_rank(cuda, tmp_path):
+    """The NCCL device-API exchange (symmetric window, LSA stores, LSA barrier) on the one GPU
+    this build has (world 1: the path a multi-GPU run takes, with the rank's own slot): the
+    sharded step through it equals the unsharded GPU step."""
+    import torch.multiprocessing as mp
+    from paper_2508_08256_b200 import build as b
+    if not b.build_nccl():
+        pytest.skip("no NCCL with the device API")
+    res = str(tmp_path / "res")
+    mp.spawn(_devx_worker, args=(1, _free_port(), res), nprocs=1, join=True)
+    assert bool(np.load(res + ".0.npz")["ok"])
