@@ -31,6 +31,14 @@ FIER_API int fier_devx_create(const uint8_t* id, int32_t world, int32_t rank, si
  * rank's window, then an LSA barrier; *out = this rank's window (slot r at r * slot_bytes).
  * Graph-capturable (one kernel launch on `stream`). */
 FIER_API int fier_devx_allgather(void* handle, const void* src, size_t bytes, void* stream, void** out);
+/* fier_shard_candidates (include/fier_cuda.h) fused with the candidate all-gather: this
+ * shard's Top-k (sel [rows][k] local indices into scores [rows][ld]) becomes (score, start +
+ * index) pairs padded to nc with (-inf, -1), stored straight into slot `rank` of every peer's
+ * window as [2][rows][nc] 32-bit words (score bits, then indices), then the LSA barrier.
+ * rows * nc * 8 <= slot_bytes.  *out = this rank's window. */
+FIER_API int fier_devx_shard_candidates(void* handle, const float* scores, int64_t ld, const int32_t* sel,
+                                        int32_t rows, int32_t k, int32_t nc, int64_t start, void* stream,
+                                        void** out);
 FIER_API int fier_devx_destroy(void* handle);
 FIER_API const char* fier_devx_last_error(void);
 

@@ -9,6 +9,7 @@
 #include <nccl.h>
 #include <nccl_device.h>
 
+#include <climits>
 #include <cstring>
 #include <string>
 
@@ -50,9 +51,59 @@ __global__ void __launch_bounds__(kThreads) devx_allgather_kernel(ncclDevComm de
     bar.sync(ncclCoopCta(), cuda::memory_order_acq_rel);
 }
 
+// The candidate exchange fused with the candidate construction (fier_shard_candidates):
+// element i of row r of this shard's Top-min(n, l) becomes (score, global index) -- or the
+// (-inf, -1) padding past k -- and is stored straight into slot `rank` of every peer's window
+// ([2][rows][nc] words: score bits, then indices), then LSA barrier c as above.
+__global__ void __launch_bounds__(kThreads) devx_candidates_kernel(ncclDevComm dev, ncclWindow_t win, size_t slot,
+                                                                   int rank, int world,
+                                                                   const float* __restrict__ scores, int64_t ld,
+                                                                   const int32_t* __restrict__ sel, int rows, int k,
+                                                                   int nc, int start) {
+    const int64_t total = (int64_t)rows * nc;
+    const int64_t per = (total + gridDim.x - 1) / gridDim.x;
+    const int64_t e0 = blockIdx.x * per, e1 = e0 + per < total ? e0 + per : total;
+    for (int64_t e = e0 + threadIdx.x; e < e1; e += kThreads) {
+        const int row = (int)(e / nc), i = (int)(e - (int64_t)row * nc);
+        float v = -INFINITY;
+        int32_t gi = -1;
+        if (i < k) {
+            const int32_t t = sel[(int64_t)row * k + i];
+            v = scores[(int64_t)row * ld + t];
+            gi = start + t;
+        }
+        for (int p = 0; p < world; ++p) {
+            uint32_t* dst = reinterpret_cast<uint32_t*>(ncclGetLsaPointer(win, (size_t)rank * slot, p));
+            dst[e] = __float_as_uint(v);
+            dst[total + e] = (uint32_t)gi;
+        }
+    }
+    ncclLsaBarrierSession<ncclCoopCta> bar(ncclCoopCta(), dev, ncclTeamTagLsa(), blockIdx.x);
+    bar.sync(ncclCoopCta(), cuda::memory_order_acq_rel);
+}
+
 }  // namespace
 
 extern "C" {
+
+FIER_API int fier_devx_shard_candidates(void* handle, const float* scores, int64_t ld, const int32_t* sel,
+                                        int32_t rows, int32_t k, int32_t nc, int64_t start, void* stream,
+                                        void** out) {
+    Devx* d = static_cast<Devx*>(handle);
+    if (!d || !out || rows < 1 || nc < 1 || k < 0 || k > nc || (k > 0 && (!scores || !sel)) ||
+        (size_t)rows * nc * 8 > d->slot || start < 0 || start > INT32_MAX)
+        return fail(1, "fier_devx_shard_candidates: invalid arguments (rows * nc * 8 bytes must fit the slot)");
+    const int64_t total = (int64_t)rows * nc;
+    int ctas = (int)((total + kThreads * 4 - 1) / (kThreads * 4));
+    if (ctas > d->ctas) ctas = d->ctas;
+    if (ctas < 1) ctas = 1;
+    devx_candidates_kernel<<<ctas, kThreads, 0, static_cast<cudaStream_t>(stream)>>>(
+        d->dev, d->win, d->slot, d->rank, d->world, scores, ld, sel, rows, k, nc, (int)start);
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(3, std::string("fier_devx_shard_candidates: ") + cudaGetErrorString(e));
+    *out = d->buf;
+    return 0;
+}
 
 FIER_API const char* fier_devx_last_error(void) { return g_err.c_str(); }
 

@@ -99,6 +99,9 @@ def _nccl_lib():
         lib.fier_devx_create.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.c_size_t, C.c_int32,
                                          C.POINTER(C.c_void_p)]
         lib.fier_devx_allgather.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p, C.POINTER(C.c_void_p)]
+        lib.fier_devx_shard_candidates.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_int32,
+                                                   C.c_int32, C.c_int32, C.c_int64, C.c_void_p,
+                                                   C.POINTER(C.c_void_p)]
         lib.fier_devx_destroy.argtypes = [C.c_void_p]
         lib.fier_devx_last_error.restype = C.c_char_p
         _NCCL_LIB = lib
@@ -153,6 +156,19 @@ class NcclDeviceExchange:
         g = self._win.view(self.world, self.slot)[:, :nbytes]
         return g.contiguous().view(t.dtype).reshape((self.world,) + tuple(t.shape))
 
+    def gather_candidates(self, scores, ld: int, sel, rows: int, k: int, n: int, start: int):
+        """fier_shard_candidates fused with the candidate all-gather (fier_devx_shard_candidates):
+        returns (CS [P, rows, n] fp32, CI [P, rows, n] int32)."""
+        out = C.c_void_p()
+        check_devx(self.lib, self.lib.fier_devx_shard_candidates(
+            self.handle, _p(scores) if scores is not None else None, ld, _p(sel) if sel is not None else None,
+            rows, k, n, start, _stream(), C.byref(out)))
+        dev = scores.device if scores is not None else torch.device("cuda", torch.cuda.current_device())
+        if self._win is None:
+            self._win = torch.as_tensor(_CudaBytes(out.value, self.world * self.slot), device=dev)
+        w = self._win.view(self.world, self.slot)[:, : 2 * rows * n * 4].view(torch.int32).view(self.world, 2, rows, n)
+        return w[:, 0].contiguous().view(torch.float32), w[:, 1].contiguous()
+
     def close(self):
         if self.handle:
             self.lib.fier_devx_destroy(self.handle)
@@ -185,8 +201,11 @@ def _unpack_partial(g: torch.Tensor, d: int) -> Tuple[torch.Tensor, torch.Tensor
 def sharded_step(shard, exchange, q, k_new, v_new, pos: int, n: int) -> torch.Tensor:
     """One decode step of a sequence-sharded layer; returns out [B, Hq, d] (fp32),
     identical on every rank.  The two all-gathers are the only communication."""
-    cs, ci = shard.select_local(q, k_new, v_new, pos, n)
-    CS, CI = _unpack_candidates(exchange.all_gather(_pack_candidates(cs, ci)))
+    if hasattr(exchange, "gather_candidates"):  # candidates stored straight into the peers' windows
+        CS, CI = shard.select_local(q, k_new, v_new, pos, n, exchange=exchange)
+    else:
+        cs, ci = shard.select_local(q, k_new, v_new, pos, n)
+        CS, CI = _unpack_candidates(exchange.all_gather(_pack_candidates(cs, ci)))
     o, lse = shard.attend_local(q, CS, CI, n)
     O, LSE = _unpack_partial(exchange.all_gather(_pack_partial(o, lse)), o.shape[-1])
     return shard.combine(O, LSE)
@@ -247,7 +266,10 @@ class ShardedDecodeLayer:
         self.local_tokens = lt
 
     # -- protocol steps -----------------------------------------------------------
-    def select_local(self, q, k_new, v_new, pos: int, n: int):
+    def select_local(self, q, k_new, v_new, pos: int, n: int, exchange=None):
+        """Append (the shard holding pos), score, local Top-min(n, l); returns the (score, global
+        index) candidate lists -- or, with an exchange that fuses the candidate construction
+        into its all-gather (NcclDeviceExchange), the gathered [P, rows, n] lists."""
         lib = _lib.load()
         sh = C.byref(self.layer.shape)
         if self.start <= pos < self.end:
@@ -260,7 +282,10 @@ class ShardedDecodeLayer:
         cs = self._buf("cs", (self.rows, n), torch.float32)
         ci = self._buf("ci", (self.rows, n), torch.int32)
         k = min(n, lt)
+        fused = exchange is not None and hasattr(exchange, "gather_candidates")
         if k == 0:
+            if fused:
+                return exchange.gather_candidates(None, 1, None, self.rows, 0, n, self.start)
             check(lib.fier_shard_candidates(None, self.rows, 1, None, 0, n, self.start, _p(cs), _p(ci),
                                             _stream()))
             return cs, ci
@@ -272,6 +297,8 @@ class ShardedDecodeLayer:
         twb = lib.fier_topk_workspace(self.rows, lt, k)
         tws = self._buf("tws", (max(twb, 1),), torch.uint8)
         check(lib.fier_topk(_p(scores), self.rows, lt, ld, k, _p(sel), _p(tws), twb, _stream()))
+        if fused:
+            return exchange.gather_candidates(scores, ld, sel, self.rows, k, n, self.start)
         check(lib.fier_shard_candidates(_p(scores), self.rows, ld, _p(sel), k, n, self.start, _p(cs), _p(ci),
                                         _stream()))
         return cs, ci

@@ -243,7 +243,7 @@ def test_nccl_exchange_library_exports_its_header():
     lib = ctypes.CDLL(path)
     text = open(os.path.join(ROOT, "include", "fier_nccl.h")).read()
     names = re.findall(r"FIER_API\s+[\w\s\*]+?\b(fier_devx_\w+)\s*\(", text)
-    assert len(names) == 5
+    assert len(names) == 6
     for name in names:
         assert hasattr(lib, name), name
     assert b"sm_100a" in open(path, "rb").read()
