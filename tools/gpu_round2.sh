@@ -8,6 +8,7 @@ timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smok
 timeout 900 python bench.py > gpurun_out/bench_c2.json 2> gpurun_out/bench_c2.err; tail -c 400 gpurun_out/bench_c2.json
 for c in c1 c3 c4 c5; do timeout 600 python bench.py --config $c --steps 200 --warmup 5 > gpurun_out/bench_$c.json 2> gpurun_out/bench_$c.err; tail -c 300 gpurun_out/bench_$c.json; done
 timeout 600 python bench.py --config c5 --sharded --steps 50 --warmup 3 > gpurun_out/bench_c5_sharded.json 2> gpurun_out/bench_c5_sharded.err
+timeout 600 python bench.py --config c5 --sharded --exchange device --steps 50 --warmup 3 > gpurun_out/bench_c5_sharded_devx.json 2> gpurun_out/bench_c5_sharded_devx.err
 timeout 900 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_reference.json 2>&1; tail -c 300 gpurun_out/bench_reference.json
 FIER_LIB=paper_2508_08256_b200/libfier_cuda_trace.so timeout 300 python tools/step_trace.py --config c2 --reps 12 > gpurun_out/step_trace_c2.txt 2>&1
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches_c2.csv python bench.py --steps 20 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
