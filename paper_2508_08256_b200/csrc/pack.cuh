@@ -110,6 +110,33 @@ __device__ __forceinline__ void pack_group(const T* Kseq,  // no restrict: appen
     }  // channel slices
 }
 
+// The open-group re-pack's two halves, shared by pack_open_group and pack_open_group32:
+// z / s in fp64 from the first-seen min / max, stored as the group's half2 (s, z); returns
+// zc, the smallest float >= z (x >= z in fp64 <=> x >= zc for fp32 x).
+__device__ __forceinline__ float open_group_params(float mn, float mx, bool valid, __half2* dst, bool& all_one) {
+    const double z = ((double)mx + (double)mn) / 2.0;
+    const double s = ((double)mx - (double)mn) / 2.0;
+    if (valid) *dst = __halves2half2(__double2half(s), __double2half(z));
+    float zc = __double2float_rn(z);
+    if ((double)zc < z) zc = nextafterf(zc, INFINITY);
+    all_one = (s == 0.0);
+    return zc;
+}
+
+// One ballot per token of a 32-token chunk -> lane i holds token i's word (its warp's 32
+// channels); lanes < cnt store it.
+__device__ __forceinline__ void open_group_bits(const float (&v)[32], int cnt, bool valid, float zc, bool all_one,
+                                                uint32_t* words, int W) {
+    const int lane = threadIdx.x & 31;
+    uint32_t mine = 0;
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+        const uint32_t word = __ballot_sync(0xffffffffu, valid && (all_one || v[i] >= zc));
+        mine = lane == i ? word : mine;
+    }
+    if (lane < cnt) words[(int64_t)lane * W] = mine;
+}
+
 // Decode-time re-pack of the open group [gi*g, t_end) (one group per launch, so
 // the code stays small: no divergent unrolled paths).  Threads [0, 32*W) take
 // part, thread c owns channel c; the same rules as pack_group (first-seen
@@ -122,19 +149,22 @@ __device__ __forceinline__ void pack_open_group(const T* Kseq,  // no restrict: 
                                                 __half2* __restrict__ sz_seq, float xnew = 0.f,
                                                 int tnew = -1) {
     const int W = (d + 31) / 32;
-    const int c = threadIdx.x, lane = c & 31, w = c >> 5;
+    const int c = threadIdx.x, w = c >> 5;
     if (w >= W) return;
     const bool valid = c < d;
     const int t0 = gi * g;
     const int t1 = min(t0 + g, t_end);  // short final group (quant1bit.hpp:84)
     float mn = 0.f, mx = 0.f;
     float v[32];  // the current chunk (g <= 32: the whole group, reused by the ballot pass)
-    for (int tc = t0; tc < t1; tc += 32) {  // chunks of 32 tokens: 32 loads in flight
+    auto load = [&](int tc) {  // chunks of 32 tokens: 32 loads in flight
 #pragma unroll
         for (int i = 0; i < 32; ++i) {
             const int t = min(tc + i, t1 - 1);  // past the end: repeat the last token (no effect)
             v[i] = !valid ? 0.f : t == tnew ? xnew : to_f32(Kseq[(int64_t)t * d + c]);
         }
+    };
+    for (int tc = t0; tc < t1; tc += 32) {
+        load(tc);
         if (tc == t0) mn = mx = v[0];
 #pragma unroll
         for (int i = 0; i < 32; ++i) {  // std::min/max: a tie keeps the first-seen value
@@ -142,28 +172,49 @@ __device__ __forceinline__ void pack_open_group(const T* Kseq,  // no restrict: 
             mx = (mx < v[i]) ? v[i] : mx;
         }
     }
-    const double z = ((double)mx + (double)mn) / 2.0;
-    const double s = ((double)mx - (double)mn) / 2.0;
-    if (valid) sz_seq[(int64_t)gi * d + c] = __halves2half2(__double2half(s), __double2half(z));
-    float zc = __double2float_rn(z);
-    if ((double)zc < z) zc = nextafterf(zc, INFINITY);
-    const bool all_one = (s == 0.0);
+    bool all_one;
+    const float zc = open_group_params(mn, mx, valid, sz_seq + (int64_t)gi * d + c, all_one);
     for (int tc = t0; tc < t1; tc += 32) {
-        if (t1 - t0 > 32) {  // g > 32: reload this chunk
-#pragma unroll
-            for (int i = 0; i < 32; ++i) {
-                const int t = min(tc + i, t1 - 1);
-                v[i] = !valid ? 0.f : t == tnew ? xnew : to_f32(Kseq[(int64_t)t * d + c]);
-            }
-        }
-        uint32_t mine = 0;
-#pragma unroll
-        for (int i = 0; i < 32; ++i) {
-            const uint32_t word = __ballot_sync(0xffffffffu, valid && (all_one || v[i] >= zc));
-            mine = lane == i ? word : mine;
-        }
-        if (tc + lane < t1) bits_seq[(int64_t)(tc + lane) * W + w] = mine;
+        if (t1 - t0 > 32) load(tc);  // g > 32: reload this chunk
+        open_group_bits(v, t1 - tc, valid, zc, all_one, bits_seq + (int64_t)tc * W + w, W);
     }
+}
+
+// The open group's first 32 rows, channel threadIdx.x (token t0 + i clamped to t1 - 1), raw:
+// issued by a caller that wants them in flight before other traffic (step_fused.cu) and
+// converted only where pack_open_group32 uses them, so the loads do not stall the caller.
+template <typename T>
+__device__ __forceinline__ void open_group_preload(const T* Kseq, int d, int t0, int t1, T (&raw)[32]) {
+    const int c = threadIdx.x;
+    if (c < d) {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) raw[i] = Kseq[(int64_t)min(t0 + i, t1 - 1) * d + c];
+    }
+}
+
+// pack_open_group for g <= 32 from open_group_preload's rows (token tnew -> xnew).
+template <typename T>
+__device__ __forceinline__ void pack_open_group32(int d, int g, int gi, int t_end, uint32_t* __restrict__ bits_seq,
+                                                  __half2* __restrict__ sz_seq, float xnew, int tnew,
+                                                  const T (&raw)[32]) {
+    const int W = (d + 31) / 32;
+    const int c = threadIdx.x, w = c >> 5;
+    if (w >= W) return;
+    const bool valid = c < d;
+    const int t0 = gi * g;
+    const int t1 = min(t0 + g, t_end);
+    float v[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] = !valid ? 0.f : min(t0 + i, t1 - 1) == tnew ? xnew : to_f32(raw[i]);
+    float mn = v[0], mx = v[0];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+        mn = (v[i] < mn) ? v[i] : mn;
+        mx = (mx < v[i]) ? v[i] : mx;
+    }
+    bool all_one;
+    const float zc = open_group_params(mn, mx, valid, sz_seq + (int64_t)gi * d + c, all_one);
+    open_group_bits(v, t1 - t0, valid, zc, all_one, bits_seq + (int64_t)t0 * W + w, W);
 }
 
 }  // namespace fier_cuda

@@ -41,6 +41,14 @@ inline RopeTable rope_table(const fier_rope* r, int pos) {
 }
 
 // Rotated channel c of x (x(j) = channel j of the unrotated vector, as float).
+// The other channel rope_channel(t, c, x) reads (c itself when c is not rotated).
+__device__ __forceinline__ int rope_partner(const RopeTable& t, int c) {
+    if (c >= t.rd) return c;
+    if (t.interleaved) return c ^ 1;
+    const int h = t.rd >> 1;
+    return c < h ? c + h : c - h;
+}
+
 template <typename Ld>
 __device__ __forceinline__ float rope_channel(const RopeTable& t, int c, Ld&& x) {
     if (c >= t.rd) return x(c);

@@ -166,8 +166,10 @@ __device__ __forceinline__ void score_slab_mma(const LaneConst<HPG>& L, const ui
             zp[4 * j + i] = __byte_perm(l[i], h[i], 0x7632);
         }
     }
-    // ---- bias = sum_j q_j z_j through the tensor cores: every A row = the group's z, so
-    // one m-tile pass gives it for all 32 tokens (rows g and g + 8 alike) ----
+    // ---- bias = sum_j q_j z_j through the tensor cores: A rows g = the group's z, so one
+    // m-tile pass gives it for all 32 tokens.  Rows g + 8 (d[2], d[3]) are never read: they
+    // take the scale pairs, which puts (z, s, z', s') in one register quad without the
+    // copies a duplicated z would need (16 moves per slab) ----
     float dz[NT][4];
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt) dz[nt][0] = dz[nt][1] = dz[nt][2] = dz[nt][3] = 0.f;
@@ -175,15 +177,17 @@ __device__ __forceinline__ void score_slab_mma(const LaneConst<HPG>& L, const ui
     for (int ks = 0; ks < 8; ++ks)
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt)
-            mma_f16(dz[nt], zp[2 * ks], zp[2 * ks], zp[2 * ks + 1], zp[2 * ks + 1], L.bq[nt][ks][0], L.bq[nt][ks][1]);
+            mma_f16(dz[nt], zp[2 * ks], sp[2 * ks], zp[2 * ks + 1], sp[2 * ks + 1], L.bq[nt][ks][0], L.bq[nt][ks][1]);
 #pragma unroll
     for (int mt = 0; mt < 2; ++mt) {
         // complemented words: a clear bit flips the (positive) scale to -s
         const uint32_t x0 = ~*reinterpret_cast<const uint32_t*>(bits_s + (mt * 16 + r) * 16 + 4 * c);
         const uint32_t x1 = ~*reinterpret_cast<const uint32_t*>(bits_s + (mt * 16 + r + 8) * 16 + 4 * c);
-        float d[NT][4];
+        float d[NT][4], e[NT][4];  // two accumulator chains (even / odd k-steps): MMA latency
 #pragma unroll
-        for (int nt = 0; nt < NT; ++nt) d[nt][0] = d[nt][1] = d[nt][2] = d[nt][3] = 0.f;
+        for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+            for (int i = 0; i < 4; ++i) d[nt][i] = e[nt][i] = 0.f;
 #pragma unroll
         for (int ks = 0; ks < 8; ++ks) {
             // channels (2ks, 2ks + 16) and (2ks + 1, 2ks + 17) of the word: bits to 15 / 31
@@ -192,8 +196,14 @@ __device__ __forceinline__ void score_slab_mma(const LaneConst<HPG>& L, const ui
             const uint32_t a2 = sp[2 * ks + 1] ^ ((x0 << (14 - 2 * ks)) & 0x80008000u);
             const uint32_t a3 = sp[2 * ks + 1] ^ ((x1 << (14 - 2 * ks)) & 0x80008000u);
 #pragma unroll
-            for (int nt = 0; nt < NT; ++nt) mma_f16(d[nt], a0, a1, a2, a3, L.bq[nt][ks][0], L.bq[nt][ks][1]);
+            for (int nt = 0; nt < NT; ++nt) {
+                mma_f16((ks & 1) ? e[nt] : d[nt], a0, a1, a2, a3, L.bq[nt][ks][0], L.bq[nt][ks][1]);
+            }
         }
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+            for (int i = 0; i < 4; ++i) d[nt][i] += e[nt][i];
         // thread (r, c): head h = 4 nt + c, its (hi, lo) in columns 2c, 2c + 1 of n-tile nt
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) {
@@ -223,7 +233,7 @@ constexpr size_t mma_smem() {
 }
 
 template <typename T, int HPG>
-__global__ void __launch_bounds__(kMmaWarps * 32) score_mma_kernel(const T* __restrict__ q, uint32_t* bits,
+__global__ void __launch_bounds__(kMmaWarps * 32, HPG <= 4 ? 2 : 1) score_mma_kernel(const T* __restrict__ q, uint32_t* bits,
                                                                    __half2* sz, int cap, int G, int hkv, int hq,
                                                                    int nseq, int tokens, int lg, float* __restrict__ scores,
                                                                    int64_t ld, AppendArgs2 ap) {

@@ -437,6 +437,8 @@ __device__ __forceinline__ uint2 rx_cluster_sum2_max(uint32_t a, int nct, uint2*
 // krem = its rank inside b1, and the overflow decision.
 // Cluster barrier 1 is the mbarrier `cbar` of every CTA (nct arrivals, phase 0): warp 0
 // arrives on all of them and waits on its own; the other warps follow at CTA scope.
+// Warp 0 also arrives on every CTA's cbar[3] once its DSMEM reads of the peers'
+// histograms are done.
 template <int NT>
 __device__ __forceinline__ RxFind rx_find(int nct, int k, RxShared& S, RxPublished& P, uint64_t* cbar) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -479,6 +481,9 @@ __device__ __forceinline__ RxFind rx_find(int nct, int k, RxShared& S, RxPublish
                 over = n > (uint32_t)kRxCand || m > (uint32_t)kRxCtaCand;  // = rx_threshold's test
             }
         }
+        // this CTA is done reading its peers' histograms: barrier cbar[3] (nct arrivals)
+        // lets a peer overwrite them (the fused step's rings) before cluster barrier 2
+        if (lane < nct) mbar_arrive_remote(smem_u32(cbar + 3), lane);
         if (lane == 0) {
             S.res[0] = (uint32_t)b;
             S.res[1] = kr;

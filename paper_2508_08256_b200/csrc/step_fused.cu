@@ -93,7 +93,10 @@ constexpr int kFsMaxKpt = 16;  // slice <= 8192 tokens (u16 slots in sidx)
 #define FS_SCORE_WARPS 16
 #endif
 constexpr int kFsScoreWarps = FS_SCORE_WARPS;  // warps that score in phase B
-constexpr int kFsAppendSlabs = 5;  // sealed slabs the append warps hand to the others (~ the append's time)
+#ifndef FIER_FS_APPEND_SLABS
+#define FIER_FS_APPEND_SLABS 2
+#endif
+constexpr int kFsAppendSlabs = FIER_FS_APPEND_SLABS;  // sealed slabs the append warps hand to the others (~ the append's time)
 constexpr int kFsLutBytes = kNibTableBytes;
 // Shared memory map (bytes from a 256-aligned base).  RxShared's tail (the digit-1
 // histogram, dead after cluster barrier 2) opens the ring area; the scorer's LUTs and
@@ -111,8 +114,8 @@ constexpr int kFsPub = kFsMasks + 2 * kFsWarps * kFsMaxKpt * 4;                 
 constexpr int kFsWres = kFsPub + ((int)sizeof(RxPublished) + 15) / 16 * 16;        // warp partials
 constexpr int kFsCres = kFsWres + kFsGatherWarps * (kFsD + 2) * 4;                // CTA partials (rank 0)
 constexpr int kFsQrot = kFsCres + kT2MaxCluster * (kFsD + 2) * 4;                 // fp32 (rotated) query
-constexpr int kFsCbar = kFsQrot + kFsD * 4;                                       // 3 cluster mbarriers
-constexpr int kFsSmem = kFsCbar + 3 * 8 + 256;                                    // + base alignment
+constexpr int kFsCbar = kFsQrot + kFsD * 4;                                       // 4 cluster mbarriers
+constexpr int kFsSmem = kFsCbar + 4 * 8 + 256;                                    // + base alignment
 static_assert(kFsRing % 256 == 0, "");
 static_assert(sizeof(T2Shared) <= sizeof(RxShared), "");
 static_assert(kFsSmem <= 227 * 1024, "fused step exceeds shared memory");
@@ -185,8 +188,24 @@ __global__ void __launch_bounds__(kFsThreads, 1) step_fused_kernel(const FsArgs 
     // first remote arrive; only warp 0 waits on it (the others never use barrier.cluster
     // again, except on the degenerate-row path).
     uint64_t* cbar = reinterpret_cast<uint64_t*>(smem + kFsCbar);
+    // The appending CTA (its slice holds pos): warps 0..3 load the open group's rows first,
+    // before the scoring streams queue up in the memory system.
+    const bool appender = a.pos / slice == rank;  // CTA-uniform
+    const int open_lo = appender ? (a.pos / a.g) * a.g : INT_MAX;  // first token of the open group
+    // Raw registers: nothing waits on these loads before phase A uses them.
+    T vpre[32];             // g <= 32: the open group's rows, channel tid
+    T knr{}, knp{}, vnr{};  // the new k row's channels tid and rope_partner(tid), the new v
+    if (appender && tid < kFsD) {
+        const T* kn = static_cast<const T*>(a.k_new) + seq * kFsD;
+        knr = kn[tid];
+        knp = kn[rope_partner(a.rope, tid)];
+        vnr = static_cast<const T*>(a.v_new)[seq * kFsD + tid];
+        if (a.g <= 32)
+            open_group_preload<T>(static_cast<const T*>(a.K) + seq * a.cap * kFsD, kFsD, open_lo,
+                                  min(open_lo + a.g, a.pos + 1), vpre);
+    }
     if (tid == 0) {
-        for (int i = 0; i < 3; ++i) mbar_init(cbar + i, (uint32_t)nct);
+        for (int i = 0; i < 4; ++i) mbar_init(cbar + i, (uint32_t)nct);
     }
     rx_clear<kFsThreads>(S);  // the scorer counts every key into the digit-1 histogram
     float* qrot = reinterpret_cast<float*>(smem + kFsQrot);  // this head's query, rotated (RoPE)
@@ -210,15 +229,17 @@ __global__ void __launch_bounds__(kFsThreads, 1) step_fused_kernel(const FsArgs 
 
     // ---- phase A: append (the CTA whose slice holds pos; warps 0..3 re-pack the open
     // group while the other warps start scoring; the open group's slabs are scored last) ----
-    const bool appender = a.pos / slice == rank;  // CTA-uniform
-    const int open_lo = appender ? (a.pos / a.g) * a.g : INT_MAX;  // first token of the open group
     if (appender && tid < D) {
-        const T* kn = static_cast<const T*>(a.k_new) + seq * D;
-        const T kv = T(rope_channel(a.rope, tid, [&](int j) { return to_f32(kn[j]); }));
-        const T vv = static_cast<const T*>(a.v_new)[seq * D + tid];
+        const T kv = T(rope_channel(a.rope, tid, [&](int j) { return to_f32(j == tid ? knr : knp); }));
+        const T vv = vnr;
         // "quantize: non-finite key entry" (quant1bit.hpp:68) for the appended row
         if (a.nonfinite && __any_sync(0xffffffffu, !isfinite(to_f32(kv))) && (tid & 31) == 0) atomicOr(a.nonfinite, 1);
-        pack_open_group<T>(Kseq, D, a.g, a.pos / a.g, a.pos + 1, bseq, zseq, to_f32(kv), a.pos);
+        FS_MARK(16);
+        if (a.g <= 32)
+            pack_open_group32<T>(D, a.g, a.pos / a.g, a.pos + 1, bseq, zseq, to_f32(kv), a.pos, vpre);
+        else  // (an out-of-line call here measured +1 us on the whole step: register ABI)
+            pack_open_group<T>(Kseq, D, a.g, a.pos / a.g, a.pos + 1, bseq, zseq, to_f32(kv), a.pos);
+        FS_MARK(21);
         Kseq[(int64_t)a.pos * D + tid] = kv;  // after the re-pack: its loads do not queue behind this store
         Vseq[(int64_t)a.pos * D + tid] = vv;
     }
@@ -285,11 +306,13 @@ __global__ void __launch_bounds__(kFsThreads, 1) step_fused_kernel(const FsArgs 
         // the append warps re-packed the open group: a named barrier over those four
         // warps publishes it, and they score the open (and empty) slabs first
         asm volatile("bar.sync 1, 128;" ::: "memory");
+        FS_MARK(22);
         for (int sl = nsealed + warp; sl < nsl; sl += 4) {
             uint4 p, bw;
             load(sl, p, bw);
             score_slab(sl, sl, p, bw);
         }
+        FS_MARK(23);
     }
     uint4 pb[PF], bb[PF];  // register ring: (s, z) and bit rows of the next PF slabs
     // Fast path: whole chunks of PF full, sealed slabs -- no per-slab bounds checks, a
@@ -353,12 +376,14 @@ __global__ void __launch_bounds__(kFsThreads, 1) step_fused_kernel(const FsArgs 
     if (!f.over) {
         rx_partition<kFsThreads>(keys, s0, wbase, f.b1, S, P, amask, kmask, sidx);
         T2_MARK(10);
-        __syncthreads();  // P complete: cluster barrier 2 (as in rx_find)
+        __syncthreads();  // P and the gather list complete: cluster barrier 2 (as in rx_find)
         if (warp == 0) {
             if (lane < nct) mbar_arrive_remote(smem_u32(cbar + 1), lane);
             mbar_wait(cbar + 1, 0);
         }
-        __syncthreads();
+        // only the select warps read the peers' candidates; the gather warps start on the
+        // rows above b1 as soon as no peer reads this CTA's histogram any more (cbar[3])
+        if (warp < kFsSelWarps) NamedBar<2, kFsSelThreads>::sync();
         T2_MARK(11);
         nlist = (int)S.nabove;
     } else {  // candidate overflow (very narrow score range): exact MSD radix select, all warps
@@ -406,6 +431,7 @@ __global__ void __launch_bounds__(kFsThreads, 1) step_fused_kernel(const FsArgs 
             r0 = c0 + (sg - nga) * kTcRows;
             return min(kTcRows, c1 - r0);
         };
+        if (!f.over) mbar_wait(cbar + 3, 0);  // the rings overlay the histogram the peers read
         tc_stream_granules<T, D, true, kFsNst>(qb, Kseq, Vseq, ring, a.scale_log2, gran, tok, st);
         tc_store_state<D, 1>(st, wres + gw * (D + 2));
         FS_MARK_T(5, kFsSelThreads);

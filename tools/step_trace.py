@@ -24,7 +24,7 @@ from paper_2508_08256_b200 import _lib  # noqa: E402
 
 NAMES = ["start", "append", "score", "resolve", "emit", "gather", "merge_sync", "out",
          "t:hist_sync", "t:find_bin", "t:partition", "t:cand_sync", "t:cand_gather", "t:rank", "t:merged", "g:above_done",
-         "-", "cta_scored", "p:keys", "p:cands", "p:sync", "-", "-", "-"]
+         "a:pack_start", "cta_scored", "p:keys", "p:cands", "p:sync", "a:packed", "a:published", "a:open_scored"]
 
 
 def main():
@@ -73,11 +73,14 @@ def main():
         raws.append(t.copy())
     nct = rows[0].shape[0] // (B * Hq)  # CTAs per cluster (grid = cluster x rows)
     if nct > 1:
-        for mk, nm in ((2, "score end (warp 0)"), (17, "CTA scored (all warps)")):
+        for mk, nm in ((2, "score end (warp 0)"), (17, "CTA scored (all warps)"), (5, "gather done")):
             by_rank = np.stack([r[:B * Hq * nct, mk].reshape(B * Hq, nct) for r in rows])
             print(f"{nm} by cluster rank (median / max, us):",
                   [(round(float(np.median(by_rank[..., c])) / 1e3, 2), round(float(by_rank[..., c].max()) / 1e3, 2))
                    for c in range(nct)])
+            spread = by_rank.max(-1) - by_rank.min(-1)  # inside each cluster
+            print(f"  {nm}: spread inside a cluster (us) percentiles 10/50/90",
+                  np.round(np.percentile(spread, [10, 50, 90]) / 1e3, 2))
     t = np.concatenate(rows)
     print(f"{a.config}: {len(rows)} steps, {t.shape[0] // len(rows)} CTAs per step (us since first CTA start)")
     for i, nm in enumerate(NAMES):
