@@ -145,6 +145,24 @@ __device__ __forceinline__ void lane_q(const T* qg, LaneConst<HPG>& L) {
     }
 }
 
+// The warp re-lays the group's (s, z) row (128 half2, read as uint2 u = channels 2u, 2u + 1
+// through ld(u)) into par_s: channel word c (channels 32c .. 32c + 31) at c * kParWordStride,
+// slot ks = (z-pair, s-pair) of channel 32c + 2ks and of 32c + 2ks + 1, each paired with the
+// channel 16 above -- exactly the register quad of the bias pass's A operand (k-step ks),
+// so score_slab_mma loads it with one LDS.128 and no byte permutes (4 PRMT per lane here
+// instead of 32 in every lane there).
+template <typename Ld>
+__device__ __forceinline__ void skew_params(uint8_t* par_s, Ld ld) {
+    const int lane = threadIdx.x & 31, c = lane >> 3, ks = lane & 7;
+    const uint2 lo = ld(16 * c + ks), hi = ld(16 * c + ks + 8);  // channels 32c + 2ks (+1) and + 16
+    uint4 o;
+    o.x = __byte_perm(lo.x, hi.x, 0x7632);
+    o.y = __byte_perm(lo.x, hi.x, 0x5410);
+    o.z = __byte_perm(lo.y, hi.y, 0x7632);
+    o.w = __byte_perm(lo.y, hi.y, 0x5410);
+    reinterpret_cast<uint4*>(par_s + c * kParWordStride)[ks] = o;
+}
+
 // Score one 32-token slab.  bits_s: 512 B of token rows (smem), par_s: 512 B of the group's
 // (s, z) half2 (smem).  ntok valid tokens.
 template <int HPG>
@@ -157,14 +175,9 @@ __device__ __forceinline__ void score_slab_mma(const LaneConst<HPG>& L, const ui
     const uint4* pw = reinterpret_cast<const uint4*>(par_s + c * kParWordStride);  // channels 32c .. 32c + 31
     uint32_t sp[16], zp[16];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-        const uint4 lo = pw[j], hi = pw[j + 4];  // channels 32c + 4j .. +3 and +16
-        const uint32_t l[4] = {lo.x, lo.y, lo.z, lo.w}, h[4] = {hi.x, hi.y, hi.z, hi.w};
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            sp[4 * j + i] = __byte_perm(l[i], h[i], 0x5410);
-            zp[4 * j + i] = __byte_perm(l[i], h[i], 0x7632);
-        }
+    for (int ks = 0; ks < 8; ++ks) {  // paired by skew_params
+        const uint4 a = pw[ks];
+        zp[2 * ks] = a.x, sp[2 * ks] = a.y, zp[2 * ks + 1] = a.z, sp[2 * ks + 1] = a.w;
     }
     // ---- bias = sum_j q_j z_j through the tensor cores: A rows g = the group's z, so one
     // m-tile pass gives it for all 32 tokens.  Rows g + 8 (d[2], d[3]) are never read: they
@@ -294,8 +307,8 @@ __global__ void __launch_bounds__(kMmaWarps * 32, HPG <= 4 ? 2 : 1) score_mma_ke
                 // coherent (L1-bypassing) reads of what this CTA just wrote
                 reinterpret_cast<uint4*>(bs)[lane] =
                     lane < ntok ? __ldcg(reinterpret_cast<const uint4*>(bseq) + t0 + lane) : make_uint4(0, 0, 0, 0);
-                reinterpret_cast<uint4*>(ps + (lane >> 3) * kParWordStride)[lane & 7] =
-                    __ldcg(reinterpret_cast<const uint4*>(zseq + (int64_t)(slab >> lg) * 128) + lane);
+                const uint4* zrow = reinterpret_cast<const uint4*>(zseq + (int64_t)(slab >> lg) * 128);
+                skew_params(ps, [&](int u) { return __ldcg(reinterpret_cast<const uint2*>(zrow) + u); });
                 __syncwarp();
                 score_slab_mma<HPG>(L, bs, ps, t0, ntok, scores + ((int64_t)b * hq + h * HPG) * ld, ld);
                 __syncwarp();
@@ -354,9 +367,9 @@ __global__ void __launch_bounds__(kMmaWarps * 32, HPG <= 4 ? 2 : 1) score_mma_ke
         mbar_wait(&full[slot], (uint32_t)((i / kMmaStages) & 1));
         uint8_t* stg = ring + (size_t)slot * kStage;
         const int t0 = slab * 32;
-        {  // skewed copy of the group's (s, z) row (see kParWordStride)
-            const uint4 v = reinterpret_cast<const uint4*>(stg + kSlabBytes)[lane];
-            reinterpret_cast<uint4*>(stg + kSlabBytes + kParBytes + (lane >> 3) * kParWordStride)[lane & 7] = v;
+        {  // skewed, paired copy of the group's (s, z) row (skew_params)
+            const uint4* row = reinterpret_cast<const uint4*>(stg + kSlabBytes);
+            skew_params(stg + kSlabBytes + kParBytes, [&](int u) { return reinterpret_cast<const uint2*>(row)[u]; });
             __syncwarp();
         }
         score_slab_mma<HPG>(L, stg, stg + kSlabBytes + kParBytes, t0, min(32, tokens - t0), out, ld);
