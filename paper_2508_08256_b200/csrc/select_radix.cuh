@@ -57,6 +57,7 @@ struct RxShared {
     uint32_t cgt[kT2MaxCluster], ceq[kT2MaxCluster];
     uint32_t res[8];
     uint32_t over, nabove, nkept;  // split variant: overflow flag, gather-list lengths
+    uint32_t gclaim;               // the fused step's gather queue (granules claimed)
     alignas(256) uint32_t hist[kRxBins + 4];  // digit-1 histogram (scoring; read remotely); [kRxBins] = trash
     alignas(16) uint32_t coarse[64];          // sums of 64 consecutive digit-1 bins (read remotely)
 };

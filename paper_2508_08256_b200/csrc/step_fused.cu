@@ -114,8 +114,8 @@ constexpr int kFsPub = kFsMasks + 2 * kFsWarps * kFsMaxKpt * 4;                 
 constexpr int kFsWres = kFsPub + ((int)sizeof(RxPublished) + 15) / 16 * 16;        // warp partials
 constexpr int kFsCres = kFsWres + kFsGatherWarps * (kFsD + 2) * 4;                // CTA partials (rank 0)
 constexpr int kFsQrot = kFsCres + kT2MaxCluster * (kFsD + 2) * 4;                 // fp32 (rotated) query
-constexpr int kFsCbar = kFsQrot + kFsD * 4;                                       // 4 cluster mbarriers
-constexpr int kFsSmem = kFsCbar + 4 * 8 + 256;                                    // + base alignment
+constexpr int kFsCbar = kFsQrot + kFsD * 4;                                       // 4 cluster mbarriers + kready
+constexpr int kFsSmem = kFsCbar + 5 * 8 + 256;                                    // + base alignment
 static_assert(kFsRing % 256 == 0, "");
 static_assert(sizeof(T2Shared) <= sizeof(RxShared), "");
 static_assert(kFsSmem <= 227 * 1024, "fused step exceeds shared memory");
@@ -204,8 +204,11 @@ __global__ void __launch_bounds__(kFsThreads, 1) step_fused_kernel(const FsArgs 
             open_group_preload<T>(static_cast<const T*>(a.K) + seq * a.cap * kFsD, kFsD, open_lo,
                                   min(open_lo + a.g, a.pos + 1), vpre);
     }
+    uint64_t* kready = cbar + 4;  // the select warps' kept candidates are listed (kFsSelThreads arrivals)
     if (tid == 0) {
         for (int i = 0; i < 4; ++i) mbar_init(cbar + i, (uint32_t)nct);
+        mbar_init(kready, (uint32_t)kFsSelThreads);
+        S.gclaim = 0u;
     }
     rx_clear<kFsThreads>(S);  // the scorer counts every key into the digit-1 histogram
     float* qrot = reinterpret_cast<float*>(smem + kFsQrot);  // this head's query, rotated (RoPE)
@@ -390,6 +393,8 @@ __global__ void __launch_bounds__(kFsThreads, 1) step_fused_kernel(const FsArgs 
         if (warp != 0) asm volatile("barrier.cluster.wait.aligned;" ::: "memory");  // (its cluster.sync)
         uint32_t cbase = 0, ccount = 0;
         fused_fallback_select(cluster, keys, a.k, S, selrow, sidx, s0, wbase, &cbase, &ccount);
+        __syncthreads();  // (the fallback select's shared state overlays RxShared)
+        if (tid == 0) S.gclaim = 0u;
         __syncthreads();
         nlist = (int)ccount;
     }
@@ -404,32 +409,44 @@ __global__ void __launch_bounds__(kFsThreads, 1) step_fused_kernel(const FsArgs 
         st.init();
         const uint32_t ring = base + kFsRing + (uint32_t)gw * kFsNst * 2 * tc_stage_bytes<D>();
         auto tok = [&](int r) { return s0 + (int)sidx[r]; };
-        auto share = [&](int r0, int r1, int& w0, int& w1) {  // 16-row granules per warp
-            const int rpw = ((r1 - r0 + kFsGatherWarps - 1) / kFsGatherWarps + kTcRows - 1) / kTcRows * kTcRows;
-            w0 = min(r0 + gw * rpw, r1);
-            w1 = min(w0 + rpw, r1);
-        };
-        int w0, w1, c0 = 0, c1 = 0;
-        share(0, nlist, w0, w1);
-        const int nga = (w1 - w0 + kTcRows - 1) / kTcRows;  // granules above b1, then the kept candidates
-        bool listed = false;
+        // The granules (16 rows) form one CTA-wide queue: the rows above b1, then the kept
+        // candidates once the select warps have listed them (mbarrier kready).  Each warp
+        // claims its next granule from a shared counter one ring stage ahead, so the warps
+        // whose rows come back early take more, and no warp waits for the others.
+        const int nga = (nlist + kTcRows - 1) / kTcRows;  // granules above b1
+        int nk = -1;                                       // kept candidates, once listed
+        int m0 = -1, m0r = 0, m0n = 0, m1 = -1, m1r = 0, m1n = 0;  // claims of granules sg (even, odd)
         auto gran = [&](int sg, int& r0) {
-            if (sg < nga) {
-                r0 = w0 + sg * kTcRows;
-                return min(kTcRows, w1 - r0);
+            if (sg & 1) {
+                if (m1 == sg) return r0 = m1r, m1n;
+            } else if (m0 == sg) {
+                return r0 = m0r, m0n;
             }
-            if (!listed) {  // first call past the above rows: wait for the select warps' list
-                int nk = 0;
-                if (!f.over) {
-                    asm volatile("bar.sync 3, %0;" ::"n"(kFsThreads) : "memory");
-                    nk = (int)S.nkept;
+            uint32_t c = 0;
+            if (lane == 0) c = atomicAdd(&S.gclaim, 1u);
+            c = __shfl_sync(0xffffffffu, c, 0);
+            int nr;
+            if ((int)c < nga) {
+                r0 = (int)c * kTcRows;
+                nr = min(kTcRows, nlist - r0);
+            } else {
+                if (nk < 0) {  // first claim past the rows above b1: wait for the list
+                    nk = 0;
+                    if (!f.over) {
+                        mbar_wait(kready, 0);
+                        nk = (int)S.nkept;
+                    }
+                    FS_MARK_T(15, kFsSelThreads);
                 }
-                share(nlist, nlist + nk, c0, c1);
-                listed = true;
-                FS_MARK_T(15, kFsSelThreads);
+                r0 = nlist + ((int)c - nga) * kTcRows;
+                nr = min(kTcRows, nlist + nk - r0);
             }
-            r0 = c0 + (sg - nga) * kTcRows;
-            return min(kTcRows, c1 - r0);
+            if (sg & 1) {
+                m1 = sg, m1r = r0, m1n = nr;
+            } else {
+                m0 = sg, m0r = r0, m0n = nr;
+            }
+            return nr;
         };
         if (!f.over) mbar_wait(cbar + 3, 0);  // the rings overlay the histogram the peers read
         tc_stream_granules<T, D, true, kFsNst>(qb, Kseq, Vseq, ring, a.scale_log2, gran, tok, st);
@@ -439,8 +456,7 @@ __global__ void __launch_bounds__(kFsThreads, 1) step_fused_kernel(const FsArgs 
         using SelBar = NamedBar<2, kFsSelThreads>;
         const RxResult rx = rx_resolve<kFsSelThreads, SelBar>(cluster, s0, slice, f.krem, S, P, kmask, sidx + nlist);
         FS_MARK(3);
-        __threadfence_block();
-        asm volatile("bar.arrive 3, %0;" ::"n"(kFsThreads) : "memory");
+        mbar_arrive_local(kready);  // release: this thread's kept-list entries and S.nkept
         rx_emit_masks<kFsSelThreads, kFsWarps, SelBar>(rx, kpt, amask, kmask, S, [&](uint32_t slot, int kw, int j) {
             selrow[slot] = s0 + kw * 32 * kpt + 32 * j + lane;
         });
