@@ -33,7 +33,10 @@
 namespace fier_cuda {
 
 constexpr int kMmaWarps = 8;      // consumer warps per CTA (one slab each per stage)
-constexpr int kMmaStages = 4;     // ring depth
+#ifndef FIER_MMA_STAGES
+#define FIER_MMA_STAGES 3
+#endif
+constexpr int kMmaStages = FIER_MMA_STAGES;  // ring depth
 constexpr int kSlabBytes = 32 * 16;  // bits of one 32-token slab (d = 128)
 constexpr int kParBytes = 128 * 4;   // (s, z) half2 of one group (d = 128)
 // The group's (s, z) row lands contiguously (one bulk copy) and the warp re-lays it out as
@@ -42,7 +45,17 @@ constexpr int kParBytes = 128 * 4;   // (s, z) half2 of one group (d = 128)
 // were a 4-way conflict; four 128-B bulk copies cost 45 instructions per slab).
 constexpr int kParWordStride = 144;
 constexpr int kParStage = 4 * kParWordStride;
-constexpr int kStage = kSlabBytes + kParBytes + kParStage;  // bits, params as copied, params skewed
+// A ring stage holds up to kSps consecutive slabs of one sequence: their bit rows
+// (contiguous), their groups' (s, z) rows as copied (contiguous), the skewed copies.  Two
+// slabs per stage halve the per-slab cost of the bulk-copy issue and the mbarrier wait
+// (~60 of ~310 warp-instructions per slab with one slab per stage).
+#ifndef FIER_MMA_SPS
+#define FIER_MMA_SPS 2
+#endif
+constexpr int kSps = FIER_MMA_SPS;
+constexpr int kStPar = kSps * kSlabBytes;
+constexpr int kStSkew = kStPar + kSps * kParBytes;
+constexpr int kStage = kStSkew + kSps * kParStage;
 
 struct AppendArgs2 {  // K == nullptr: no fused append
     void* K;
@@ -236,10 +249,11 @@ __device__ __forceinline__ void score_slab_mma(const LaneConst<HPG>& L, const ui
 
 // ---- the kernel -------------------------------------------------------------------
 // Every warp owns a contiguous range of the sealed slabs of all sequences and
-// streams it through a private kMmaStages-deep smem ring: lane 0 issues the
-// bulk copies (512 B of bits + 512 B of the slab's group parameters) of slab
-// i + kMmaStages - 1 while the warp scores slab i; completion is an mbarrier
-// per ring slot.  No CTA-wide barrier in the main loop.
+// streams it through a private kMmaStages-deep smem ring of kSps-slab stages: lane 0
+// issues the two bulk copies (the stage's bit rows, its groups' parameters) of stage
+// i + kMmaStages - 1 while the warp scores stage i; completion is an mbarrier per ring
+// slot.  No CTA-wide barrier in the main loop.  (A/B, K2 us C4 / C3 / C5: 1 slab x 4
+// stages 126.8 / 21.7 / 125.9, 2 x 4 120.9 / 22.4 / 120.3, 2 x 3 120.3 / 21.5 / 119.5.)
 template <int HPG>
 constexpr size_t mma_smem() {
     return (size_t)kMmaWarps * kMmaStages * kStage + (size_t)kMmaWarps * kMmaStages * 8;
@@ -302,7 +316,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32, HPG <= 4 ? 2 : 1) score_mma_ke
             lane_q<T, HPG>(q + ((int64_t)b * hq + h * HPG) * 128, L);
             for (int slab = open0 + warp; slab < nslabs; slab += kMmaWarps) {
                 uint8_t* bs = ring;
-                uint8_t* ps = bs + kSlabBytes;
+                uint8_t* ps = bs + kStSkew;
                 const int t0 = slab * 32, ntok = min(32, tokens - t0);
                 // coherent (L1-bypassing) reads of what this CTA just wrote
                 reinterpret_cast<uint4*>(bs)[lane] =
@@ -340,41 +354,63 @@ __global__ void __launch_bounds__(kMmaWarps * 32, HPG <= 4 ? 2 : 1) score_mma_ke
     fence_proxy_async();  // generic-proxy writes to the ring (open slabs) before bulk copies reuse it
     __syncwarp();
     const uint64_t pol = policy_evict_first();
-    // (seq, slab) of the next slab to issue, advanced incrementally (no divisions)
+    // Stages: up to kSps consecutive slabs of one sequence.  The issuer (lane 0, kMmaStages - 1
+    // stages ahead) and the consumer walk the same (seq, slab, count) sequence.
+    const int64_t n = w1 - w0;  // slabs of this warp
+    auto stage_len = [&](int slab_, int64_t left) {
+        const int c = min(kSps, open0 - slab_);
+        return left < (int64_t)c ? (int)left : c;
+    };
     int iseq = (int)(w0 / open0), islab = (int)(w0 - (int64_t)iseq * open0);
+    int64_t ileft = n;
     auto issue = [&](int slot) {  // lane 0
-        const int t0 = islab * 32, ntok = min(32, tokens - t0);
+        const int cnt = stage_len(islab, ileft);
+        const int t0 = islab * 32, ntok = min(32 * cnt, tokens - t0);
+        const int gfirst = islab >> lg, ng = ((islab + cnt - 1) >> lg) - gfirst + 1;
         uint8_t* dst = ring + (size_t)slot * kStage;
-        mbar_arrive_expect_tx(&full[slot], (uint32_t)ntok * 16 + kParBytes);
+        mbar_arrive_expect_tx(&full[slot], (uint32_t)ntok * 16 + (uint32_t)ng * kParBytes);
         bulk_g2s_evict_first(dst, bits + ((int64_t)iseq * cap + t0) * 4, (uint32_t)ntok * 16, &full[slot], pol);
-        bulk_g2s_evict_first(dst + kSlabBytes, sz + ((int64_t)iseq * G + (islab >> lg)) * 128, kParBytes,
+        bulk_g2s_evict_first(dst + kStPar, sz + ((int64_t)iseq * G + gfirst) * 128, (uint32_t)ng * kParBytes,
                              &full[slot], pol);
-        if (++islab == open0) {
+        ileft -= cnt;
+        if ((islab += cnt) == open0) {
             islab = 0;
             ++iseq;
         }
     };
-    const int n = (int)(w1 - w0);
     if (lane == 0)
-        for (int s = 0; s < kMmaStages - 1 && s < n; ++s) issue(s);
+        for (int s = 0; s < kMmaStages - 1 && ileft > 0; ++s) issue(s);
     int seq = (int)(w0 / open0), slab = (int)(w0 - (int64_t)seq * open0);
     int b = seq / hkv, h = seq - b * hkv;
     lane_q<T, HPG>(q + ((int64_t)b * hq + h * HPG) * 128, L);
     float* out = scores + ((int64_t)b * hq + h * HPG) * ld;
-    for (int i = 0; i < n; ++i) {
+    int64_t left = n;
+    for (int i = 0; left > 0; ++i) {
         const int slot = i % kMmaStages;
-        if (lane == 0 && i + kMmaStages - 1 < n) issue((i + kMmaStages - 1) % kMmaStages);
+        if (lane == 0 && ileft > 0) issue((i + kMmaStages - 1) % kMmaStages);
         mbar_wait(&full[slot], (uint32_t)((i / kMmaStages) & 1));
         uint8_t* stg = ring + (size_t)slot * kStage;
-        const int t0 = slab * 32;
-        {  // skewed, paired copy of the group's (s, z) row (skew_params)
-            const uint4* row = reinterpret_cast<const uint4*>(stg + kSlabBytes);
-            skew_params(stg + kSlabBytes + kParBytes, [&](int u) { return reinterpret_cast<const uint2*>(row)[u]; });
-            __syncwarp();
+        const int cnt = stage_len(slab, left);
+#pragma unroll
+        for (int u = 0; u < kSps; ++u) {
+            if (u < cnt) {  // skewed, paired copy of the group's (s, z) row (skew_params)
+                const uint2* row =
+                    reinterpret_cast<const uint2*>(stg + kStPar + (((slab + u) >> lg) - (slab >> lg)) * kParBytes);
+                skew_params(stg + kStSkew + u * kParStage, [&](int v) { return row[v]; });
+            }
         }
-        score_slab_mma<HPG>(L, stg, stg + kSlabBytes + kParBytes, t0, min(32, tokens - t0), out, ld);
+        __syncwarp();
+#pragma unroll
+        for (int u = 0; u < kSps; ++u) {
+            if (u < cnt) {
+                const int t0 = (slab + u) * 32;
+                score_slab_mma<HPG>(L, stg + u * kSlabBytes, stg + kStSkew + u * kParStage, t0, min(32, tokens - t0),
+                                    out, ld);
+            }
+        }
         __syncwarp();  // every lane is done with `slot` before lane 0 refills it
-        if (++slab == open0 && i + 1 < n) {
+        left -= cnt;
+        if ((slab += cnt) == open0 && left > 0) {
             slab = 0;
             ++seq;
             b = seq / hkv;
