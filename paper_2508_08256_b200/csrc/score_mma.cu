@@ -34,7 +34,7 @@ namespace fier_cuda {
 
 constexpr int kMmaWarps = 8;      // consumer warps per CTA (one slab each per stage)
 #ifndef FIER_MMA_STAGES
-#define FIER_MMA_STAGES 3
+#define FIER_MMA_STAGES 2
 #endif
 constexpr int kMmaStages = FIER_MMA_STAGES;  // ring depth
 constexpr int kSlabBytes = 32 * 16;  // bits of one 32-token slab (d = 128)
@@ -46,11 +46,11 @@ constexpr int kParBytes = 128 * 4;   // (s, z) half2 of one group (d = 128)
 constexpr int kParWordStride = 144;
 constexpr int kParStage = 4 * kParWordStride;
 // A ring stage holds up to kSps consecutive slabs of one sequence: their bit rows
-// (contiguous), their groups' (s, z) rows as copied (contiguous), the skewed copies.  Two
-// slabs per stage halve the per-slab cost of the bulk-copy issue and the mbarrier wait
+// (contiguous), their groups' (s, z) rows as copied (contiguous), the skewed copies.  Four
+// slabs per stage cut the per-slab cost of the bulk-copy issue and the mbarrier wait
 // (~60 of ~310 warp-instructions per slab with one slab per stage).
 #ifndef FIER_MMA_SPS
-#define FIER_MMA_SPS 2
+#define FIER_MMA_SPS 4
 #endif
 constexpr int kSps = FIER_MMA_SPS;
 constexpr int kStPar = kSps * kSlabBytes;
@@ -253,7 +253,8 @@ __device__ __forceinline__ void score_slab_mma(const LaneConst<HPG>& L, const ui
 // issues the two bulk copies (the stage's bit rows, its groups' parameters) of stage
 // i + kMmaStages - 1 while the warp scores stage i; completion is an mbarrier per ring
 // slot.  No CTA-wide barrier in the main loop.  (A/B, K2 us C4 / C3 / C5: 1 slab x 4
-// stages 126.8 / 21.7 / 125.9, 2 x 4 120.9 / 22.4 / 120.3, 2 x 3 120.3 / 21.5 / 119.5.)
+// stages 126.8 / 21.7 / 125.9, 2 x 4 120.9 / 22.4 / 120.3, 2 x 3 120.3 / 21.5 / 119.5,
+// 2 x 2 119.8 / 20.9 / -, 4 x 2 113.5 / 21.2 / -; 4 x 2 = 102 KB per CTA, two CTAs per SM.)
 template <int HPG>
 constexpr size_t mma_smem() {
     return (size_t)kMmaWarps * kMmaStages * kStage + (size_t)kMmaWarps * kMmaStages * 8;
