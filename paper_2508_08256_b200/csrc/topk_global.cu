@@ -477,13 +477,15 @@ struct TrShared {
             int32_t ri[2][kTrRefine];
         } r;                     // refinement, after the histogram is dead
     } u;
-    uint32_t ck[kTrCand];
+    uint32_t ck[kTrCand];  // (ck + ci: one array for the output staging)
     int32_t ci[kTrCand];
     uint32_t bm[kTrMaxTokens / 32];
     uint32_t tot[kT2Bins];
     uint32_t wsum[32], wsuf[32], res[8];
     uint32_t ncand;
 };
+
+static_assert(offsetof(TrShared, ci) == offsetof(TrShared, ck) + sizeof(uint32_t) * kTrCand, "");
 
 __global__ void __launch_bounds__(kTrThreads) tr_row_kernel(const float* __restrict__ scores, int tokens, int64_t ld,
                                                              int k, int32_t* __restrict__ sel) {
@@ -631,9 +633,20 @@ __global__ void __launch_bounds__(kTrThreads) tr_row_kernel(const float* __restr
     }
     uint32_t tot = 0;
     uint32_t o = tg_scan<NT>(c, S, &tot);
+    if (tot <= 2u * kTrCand) {
+        // staged in the dead candidate arrays, then written out coalesced (each thread's
+        // run of ~k/256 scattered stores was 13% of the kernel's warp samples)
+        int32_t* stage = reinterpret_cast<int32_t*>(S.ck);  // ck and ci are contiguous (static_assert at TrShared)
 #pragma unroll
-    for (int j = 0; j < WPT; ++j)
-        for (uint32_t m = wv[j]; m; m &= m - 1) out[o++] = 32 * (tid * wpt + j) + __ffs(m) - 1;
+        for (int j = 0; j < WPT; ++j)
+            for (uint32_t m = wv[j]; m; m &= m - 1) stage[o++] = 32 * (tid * wpt + j) + __ffs(m) - 1;
+        __syncthreads();
+        for (uint32_t i = tid; i < tot; i += NT) out[i] = stage[i];
+    } else {
+#pragma unroll
+        for (int j = 0; j < WPT; ++j)
+            for (uint32_t m = wv[j]; m; m &= m - 1) out[o++] = 32 * (tid * wpt + j) + __ffs(m) - 1;
+    }
 }
 
 bool topk_rows_applies(int rows, int tokens, int k) {
