@@ -145,13 +145,11 @@ __device__ __noinline__ void fused_fallback_select(cg::cluster_group& cluster, c
                                                    int wbase, uint32_t* cbase, uint32_t* ccount) {
     const int lane = threadIdx.x & 31;
     const T2Threshold th = t2_radix_select<kFsThreads>(cluster, keys, k, S);
-    uint32_t base = 0;
     t2_compact<kFsThreads>(cluster, keys, th, S, cbase, ccount, [&](uint32_t slot, int j) {
         const int local = wbase + 32 * j + lane;
         selrow[slot] = s0 + local;
         sidx[slot - *cbase] = (uint16_t)local;
     });
-    (void)base;
 }
 
 template <typename T>
@@ -211,49 +209,11 @@ __global__ void __launch_bounds__(kFsThreads, 1) step_fused_kernel(const FsArgs 
         S.gclaim = 0u;
     }
     rx_clear<kFsThreads>(S);  // the scorer counts every key into the digit-1 histogram
-    float* qrot = reinterpret_cast<float*>(smem + kFsQrot);  // this head's query, rotated (RoPE)
-    if (tid < kFsD) {
-        const T* qh = static_cast<const T*>(a.q) + (int64_t)row * kFsD;
-        // rotated in fp32, rounded to the cache dtype like the rotated k row (rope.cuh)
-        qrot[tid] = to_f32(T(rope_channel(a.rope, tid, [&](int j) { return to_f32(qh[j]); })));
-        // the query's logits cannot be finite ("softmax: non-finite logit", core.hpp:122)
-        if (a.nonfinite && rank == 0 && __any_sync(0xffffffffu, !isfinite(qrot[tid])) && (tid & 31) == 0)
-            atomicOr(a.nonfinite, 2);
-    }
-    __syncthreads();
-    asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
-    if (warp == 0) asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
-    FS_MARK(0);
-
     T* Kseq = static_cast<T*>(a.K) + seq * a.cap * D;
     T* Vseq = static_cast<T*>(a.V) + seq * a.cap * D;
     uint32_t* bseq = a.bits + seq * a.cap * 4;
     __half2* zseq = a.sz + seq * a.G * D;
 
-    // ---- phase A: append (the CTA whose slice holds pos; warps 0..3 re-pack the open
-    // group while the other warps start scoring; the open group's slabs are scored last) ----
-    if (appender && tid < D) {
-        const T kv = T(rope_channel(a.rope, tid, [&](int j) { return to_f32(j == tid ? knr : knp); }));
-        const T vv = vnr;
-        // "quantize: non-finite key entry" (quant1bit.hpp:68) for the appended row
-        if (a.nonfinite && __any_sync(0xffffffffu, !isfinite(to_f32(kv))) && (tid & 31) == 0) atomicOr(a.nonfinite, 1);
-        FS_MARK(16);
-        if (a.g <= 32)
-            pack_open_group32<T>(D, a.g, a.pos / a.g, a.pos + 1, bseq, zseq, to_f32(kv), a.pos, vpre);
-        else  // (an out-of-line call here measured +1 us on the whole step: register ABI)
-            pack_open_group<T>(Kseq, D, a.g, a.pos / a.g, a.pos + 1, bseq, zseq, to_f32(kv), a.pos);
-        FS_MARK(21);
-        Kseq[(int64_t)a.pos * D + tid] = kv;  // after the re-pack: its loads do not queue behind this store
-        Vseq[(int64_t)a.pos * D + tid] = vv;
-    }
-
-    FS_MARK(1);
-    // ---- phase B: score this CTA's slice into shared-memory keys ----
-    float qv[4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) qv[i] = qrot[4 * lane + i];
-    const uint32_t tab0 = base + kFsLut + warp * kFsLutBytes;  // one table per warp (trace: 10.75 vs 11.0 us double-buffered)
-    float* srow = a.scores ? a.scores + (int64_t)row * a.ld : nullptr;
     // Scoring is assigned per slab (32 tokens), independently of which warp owns the
     // slab's keys in phase C (keys are stored token-ordered: slab sl -> keys_s[32 sl ..]).
     // Sealed slabs are split into contiguous per-warp ranges; in the appending CTA the
@@ -279,6 +239,60 @@ __global__ void __launch_bounds__(kFsThreads, 1) step_fused_kernel(const FsArgs 
             cnt = q + (w < r ? 1 : 0);
         }
     }
+#ifdef FIER_FS_L2PF
+    // The first slabs of every non-append warp are prefetched into L2 before the query read
+    // (a PCIe round trip when q is host-resident): one bulk prefetch of their bit rows and
+    // one of their groups' (s, z) rows per warp, nothing held in registers.
+    if (lane == 0 && !(appender && warp < 4) && cnt > 0 && a.g_shift >= 0) {
+        const int nf = min(cnt, FIER_FS_L2PF);
+        const int t0 = s0 + 32 * start;
+        if (t0 + 32 * nf <= a.tokens) {
+            const int g0 = t0 >> a.g_shift, g1 = (t0 + 32 * nf - 1) >> a.g_shift;
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(bseq + (int64_t)t0 * 4),
+                         "r"((uint32_t)nf * 512u) : "memory");
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(zseq + (int64_t)g0 * D),
+                         "r"((uint32_t)(g1 - g0 + 1) * 512u) : "memory");
+        }
+    }
+#endif
+    float* qrot = reinterpret_cast<float*>(smem + kFsQrot);  // this head's query, rotated (RoPE)
+    if (tid < kFsD) {
+        const T* qh = static_cast<const T*>(a.q) + (int64_t)row * kFsD;
+        // rotated in fp32, rounded to the cache dtype like the rotated k row (rope.cuh)
+        qrot[tid] = to_f32(T(rope_channel(a.rope, tid, [&](int j) { return to_f32(qh[j]); })));
+        // the query's logits cannot be finite ("softmax: non-finite logit", core.hpp:122)
+        if (a.nonfinite && rank == 0 && __any_sync(0xffffffffu, !isfinite(qrot[tid])) && (tid & 31) == 0)
+            atomicOr(a.nonfinite, 2);
+    }
+    __syncthreads();
+    asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+    if (warp == 0) asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
+    FS_MARK(0);
+
+    // ---- phase A: append (the CTA whose slice holds pos; warps 0..3 re-pack the open
+    // group while the other warps start scoring; the open group's slabs are scored last) ----
+    if (appender && tid < D) {
+        const T kv = T(rope_channel(a.rope, tid, [&](int j) { return to_f32(j == tid ? knr : knp); }));
+        const T vv = vnr;
+        // "quantize: non-finite key entry" (quant1bit.hpp:68) for the appended row
+        if (a.nonfinite && __any_sync(0xffffffffu, !isfinite(to_f32(kv))) && (tid & 31) == 0) atomicOr(a.nonfinite, 1);
+        FS_MARK(16);
+        if (a.g <= 32)
+            pack_open_group32<T>(D, a.g, a.pos / a.g, a.pos + 1, bseq, zseq, to_f32(kv), a.pos, vpre);
+        else  // (an out-of-line call here measured +1 us on the whole step: register ABI)
+            pack_open_group<T>(Kseq, D, a.g, a.pos / a.g, a.pos + 1, bseq, zseq, to_f32(kv), a.pos);
+        FS_MARK(21);
+        Kseq[(int64_t)a.pos * D + tid] = kv;  // after the re-pack: its loads do not queue behind this store
+        Vseq[(int64_t)a.pos * D + tid] = vv;
+    }
+
+    FS_MARK(1);
+    // ---- phase B: score this CTA's slice into shared-memory keys ----
+    float qv[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) qv[i] = qrot[4 * lane + i];
+    const uint32_t tab0 = base + kFsLut + warp * kFsLutBytes;  // one table per warp (trace: 10.75 vs 11.0 us double-buffered)
+    float* srow = a.scores ? a.scores + (int64_t)row * a.ld : nullptr;
     auto score_slab = [&](int sl, int u, const uint4& p, const uint4& bw) {
         const int t0 = s0 + 32 * sl, t = t0 + lane;
         uint32_t key = 0u;  // 0 = empty slot (past the row end, or NaN)
