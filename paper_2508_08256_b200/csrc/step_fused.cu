@@ -239,10 +239,15 @@ __global__ void __launch_bounds__(kFsThreads, 1) step_fused_kernel(const FsArgs 
             cnt = q + (w < r ? 1 : 0);
         }
     }
-#ifdef FIER_FS_L2PF
+#ifndef FIER_FS_L2PF
+#define FIER_FS_L2PF 4
+#endif
+#if FIER_FS_L2PF > 0
     // The first slabs of every non-append warp are prefetched into L2 before the query read
     // (a PCIe round trip when q is host-resident): one bulk prefetch of their bit rows and
-    // one of their groups' (s, z) rows per warp, nothing held in registers.
+    // one of their groups' (s, z) rows per warp, nothing held in registers (loads into
+    // registers here spilled at the 128-register cap).  A/B x3 on one box, C2 step / e2e us:
+    // none 31.01 / 33.90, 3 slabs 30.71 / 33.64, 4 30.65 / 33.39, 6 30.73 / 33.29, 8 30.82 / 33.17.
     if (lane == 0 && !(appender && warp < 4) && cnt > 0 && a.g_shift >= 0) {
         const int nf = min(cnt, FIER_FS_L2PF);
         const int t0 = s0 + 32 * start;
