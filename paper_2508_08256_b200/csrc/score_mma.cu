@@ -70,8 +70,12 @@ struct AppendArgs2 {  // K == nullptr: no fused append
 };
 
 // sealed slabs fewer per warp of an appending CTA (C3 sweep, K2: 0 -> 75.3 us,
-// 6 -> 71.6 us, 8-12 -> 73.2 us)
-constexpr int kMmaRebalance = 6;
+// 6 -> 71.6 us, 8-12 -> 73.2 us with one slab per ring stage; with four-slab stages, C3 / C4
+// step us: 0 72.2 / 478.8, 6 68.64 / 477.9, 12 68.18 / 477.1, 20 68.58 / 477.5)
+#ifndef FIER_MMA_REBALANCE
+#define FIER_MMA_REBALANCE 12
+#endif
+constexpr int kMmaRebalance = FIER_MMA_REBALANCE;
 
 __device__ __forceinline__ void mma_f16(float* d, uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t b0,
                                         uint32_t b1) {

@@ -301,6 +301,24 @@ def test_score_tensor_core_shapes(cuda, port, hpg, g, L, dtype):
             assert score_err(s[b, h], ref) <= SCORE_TOL, (b, h)
 
 
+@pytest.mark.parametrize("g", [32, 64, 128])
+def test_score_tensor_core_multi_slab_stages(cuda, port, g):
+    """K2's ring stages of up to 4 slabs: enough slabs per warp that stages hold 1..4 slabs, cross
+    sequence boundaries (a stage never does: it is cut there) and, for g > 32, cover 1..3 groups."""
+    F = fier()
+    torch.manual_seed(g)
+    B, Hkv, hpg, L, d = 1, 8, 4, 40013, 128
+    K = (torch.randn(B, Hkv, L, d, device=cuda) * 3).to(torch.bfloat16)
+    q = torch.randn(B, Hkv * hpg, d, device=cuda).to(torch.bfloat16)
+    pk = F.quantize(K, g)
+    s = F.approx_scores(q, pk).cpu().numpy().astype(np.float64)
+    for kv in range(Hkv):
+        buf = pk.to_fier(0, kv)
+        for h in range(kv * hpg, (kv + 1) * hpg):
+            ref = port.approx_scores_fier(q[0, h].double().cpu().numpy(), buf)
+            assert score_err(s[0, h], ref) <= SCORE_TOL, (g, h)
+
+
 @pytest.mark.parametrize("hpg,g,pos", [(1, 32, 4100), (4, 32, 4127), (4, 64, 4097), (8, 128, 4000),
                                        (2, 32, 31), (1, 32, 0)])
 def test_fused_append_score_tensor_core(cuda, port, hpg, g, pos):
