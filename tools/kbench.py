@@ -71,6 +71,16 @@ def main():
         _lib.check(lib.fier_full_attention(C.byref(lay.shape), _p(q), _p(lay.K), _p(lay.V), pos + 1,
                                            1 / math.sqrt(d), _p(out[i]), _p(fws), fwb, _stream()))
 
+    def k_chain(i):  # the separate kernels back to back, no append
+        k_score(i), k_topk(i), k_attn(i)
+
+    def k_append_chain(i):  # fier_append then the chain (the step's work in four launches)
+        k_append(i), k_chain(i)
+
+    def k_step(i):  # the decode step itself (fused append in the scorer on the GQA path)
+        lay, (q, kn, vn) = layers[i], inp[i]
+        lay.step(q, kn, vn, pos, n, out=out[i], sel=sel[i])
+
     for i in range(a.layers):  # populate scores/selections
         k_append(i), k_score(i), k_topk(i)
     torch.cuda.synchronize()
@@ -78,7 +88,7 @@ def main():
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
     for name, fn in [("append", k_append), ("score", k_score), ("topk", k_topk), ("sparse_attn", k_attn),
-                     ("full_attn", k_full)]:
+                     ("full_attn", k_full), ("chain", k_chain), ("append+chain", k_append_chain), ("step", k_step)]:
         res = []
         for mode in ("same", "rotate"):
             # one CUDA graph of `reps` launches: GPU time without host launch overhead
