@@ -465,9 +465,18 @@ __global__ void __launch_bounds__(kTgRowThreads) tg_row_kernel(const float* __re
 // variant -- 2048 sampled keys bound the collection, no full histogram -- needed 75 KB of
 // shared memory for the collected keys and ran 150 us.)
 constexpr int kTrThreads = 256;
-constexpr int kTrCand = 2048;          // candidates of a row (digit 1 == b1)
-constexpr int kTrRefine = 1024;        // survivors of the first refinement level
-constexpr int kTrMaxTokens = 65536;    // bitmap of the row's indices (8 KB)
+#ifndef FIER_TR_CAND
+#define FIER_TR_CAND 1024
+#endif
+constexpr int kTrCand = FIER_TR_CAND;      // candidates of a row (digit 1 == b1); more: exact fallback
+constexpr int kTrRefine = kTrCand / 2;     // survivors of the first refinement level
+constexpr int kTrMaxTokens = 32768;        // bitmap of the row's indices (4 KB)
+// Six CTAs per SM (30 KB of shared memory, <= 40 registers): 888 rows in flight, and the
+// smaller carveout leaves L1 for the second pass's re-reads.  C4 K3 by footprint: 42 KB / 48
+// registers (5 per SM) 88.9 us; 34 KB (1536 candidates), 6 per SM 87.9 us; 30 KB (1024), 6 per
+// SM 82.2 us; 7 per SM (36 registers, 184 B of spill) 99 us; no register cap (84 registers,
+// 3 per SM) 111 us.  A row with more candidates in its digit-1 bin takes the exact fallback.
+constexpr int kTrMinBlocks = 6;
 
 struct TrShared {
     union {
@@ -477,7 +486,7 @@ struct TrShared {
             int32_t ri[2][kTrRefine];
         } r;                     // refinement, after the histogram is dead
     } u;
-    uint32_t ck[kTrCand];  // (ck + ci: one array for the output staging)
+    uint32_t ck[kTrCand];
     int32_t ci[kTrCand];
     uint32_t bm[kTrMaxTokens / 32];
     uint32_t tot[kT2Bins];
@@ -485,9 +494,7 @@ struct TrShared {
     uint32_t ncand;
 };
 
-static_assert(offsetof(TrShared, ci) == offsetof(TrShared, ck) + sizeof(uint32_t) * kTrCand, "");
-
-__global__ void __launch_bounds__(kTrThreads) tr_row_kernel(const float* __restrict__ scores, int tokens, int64_t ld,
+__global__ void __launch_bounds__(kTrThreads, kTrMinBlocks) tr_row_kernel(const float* __restrict__ scores, int tokens, int64_t ld,
                                                              int k, int32_t* __restrict__ sel) {
     extern __shared__ __align__(16) uint8_t smem_raw[];
     TrShared& S = *reinterpret_cast<TrShared*>(smem_raw);
@@ -633,10 +640,10 @@ __global__ void __launch_bounds__(kTrThreads) tr_row_kernel(const float* __restr
     }
     uint32_t tot = 0;
     uint32_t o = tg_scan<NT>(c, S, &tot);
-    if (tot <= 2u * kTrCand) {
-        // staged in the dead candidate arrays, then written out coalesced (each thread's
-        // run of ~k/256 scattered stores was 13% of the kernel's warp samples)
-        int32_t* stage = reinterpret_cast<int32_t*>(S.ck);  // ck and ci are contiguous (static_assert at TrShared)
+    if (tot <= (uint32_t)kTgBins) {
+        // staged in the dead histogram / refinement union, then written out coalesced (each
+        // thread's run of ~k/256 scattered stores was 13% of the kernel's warp samples)
+        int32_t* stage = reinterpret_cast<int32_t*>(S.u.hist);
 #pragma unroll
         for (int j = 0; j < WPT; ++j)
             for (uint32_t m = wv[j]; m; m &= m - 1) stage[o++] = 32 * (tid * wpt + j) + __ffs(m) - 1;
