@@ -671,7 +671,7 @@ __device__ __forceinline__ RxResult rx_resolve(cg::cluster_group& cluster, int s
 
 // The select warps: emit(slot, kw, j) for every kept key (key-warp kw < KW, slot j, this
 // lane) from amask | kmask, slots ascending with the index.
-template <int NT, int KW, typename Bar, typename Emit>
+template <int NT, int KW, int KMAX, typename Bar, typename Emit>
 __device__ __forceinline__ void rx_emit_masks(const RxResult& R, int kpt, const uint32_t* amask,
                                               const uint32_t* kmask, RxShared& S, Emit&& emit) {
     static_assert(KW <= 32, "");
@@ -680,7 +680,9 @@ __device__ __forceinline__ void rx_emit_masks(const RxResult& R, int kpt, const 
         uint32_t c = 0;
         if (lane < KW) {
             c = S.wab[lane];
-            for (int j = 0; j < kpt; ++j) c += __popc(kmask[lane * kpt + j]);
+#pragma unroll
+            for (int j = 0; j < KMAX; ++j)
+                if (j < kpt) c += __popc(kmask[lane * kpt + j]);
         }
         uint32_t pre = c;
 #pragma unroll
@@ -694,10 +696,15 @@ __device__ __forceinline__ void rx_emit_masks(const RxResult& R, int kpt, const 
     const uint32_t lt = t2_lanemask_lt();
     for (int kw = warp; kw < KW; kw += NT / 32) {
         uint32_t run = R.cta_base + S.wsum[kw];
-        for (int j = 0; j < kpt; ++j) {
-            const uint32_t m = amask[kw * kpt + j] | kmask[kw * kpt + j];
-            if ((m >> lane) & 1u) emit(run + __popc(m & lt), kw, j);
-            run += __popc(m);
+        // every slot's mask loaded first: one shared-memory latency per key-warp instead of kpt
+        // (the fused step: 30.63 -> 30.30 us, the emit runs next to the gather warps)
+        uint32_t mm[KMAX];
+#pragma unroll
+        for (int j = 0; j < KMAX; ++j) mm[j] = j < kpt ? (amask[kw * kpt + j] | kmask[kw * kpt + j]) : 0u;
+#pragma unroll
+        for (int j = 0; j < KMAX; ++j) {
+            if ((mm[j] >> lane) & 1u) emit(run + __popc(mm[j] & lt), kw, j);
+            run += __popc(mm[j]);
         }
     }
 }

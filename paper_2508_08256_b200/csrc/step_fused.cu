@@ -476,7 +476,7 @@ __global__ void __launch_bounds__(kFsThreads, 1) step_fused_kernel(const FsArgs 
         const RxResult rx = rx_resolve<kFsSelThreads, SelBar>(cluster, s0, slice, f.krem, S, P, kmask, sidx + nlist);
         FS_MARK(3);
         mbar_arrive_local(kready);  // release: this thread's kept-list entries and S.nkept
-        rx_emit_masks<kFsSelThreads, kFsWarps, SelBar>(rx, kpt, amask, kmask, S, [&](uint32_t slot, int kw, int j) {
+        rx_emit_masks<kFsSelThreads, kFsWarps, kFsMaxKpt, SelBar>(rx, kpt, amask, kmask, S, [&](uint32_t slot, int kw, int j) {
             selrow[slot] = s0 + kw * 32 * kpt + 32 * j + lane;
         });
         FS_MARK(4);
