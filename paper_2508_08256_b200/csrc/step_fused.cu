@@ -156,9 +156,11 @@ template <typename T>
 __global__ void __launch_bounds__(kFsThreads, 1) step_fused_kernel(const FsArgs a) {
     constexpr int D = kFsD;
 #ifndef FIER_FS_PF
-#define FIER_FS_PF 4
+#define FIER_FS_PF 2
 #endif
-    constexpr int PF = FIER_FS_PF;  // slabs in flight per warp
+    // slabs in flight per warp in the register ring (A/B x3, C2 us: 1 30.99, 2 29.64, 3 30.01,
+    // 4 30.24, 6 33.15 -- fewer live registers next to the L2 prefetch at kernel entry)
+    constexpr int PF = FIER_FS_PF;
     cg::cluster_group cluster = cg::this_cluster();
     const int rank = (int)cluster.block_rank();
     const int nct = (int)cluster.num_blocks();
